@@ -1,0 +1,449 @@
+#!/usr/bin/env python
+"""Benchmark: sparse AA D3Q19 TRT fp64 stream-collide, MFLUPS on B200.
+
+Workload (BASELINE.json configs[1]): 512^3 cells per GPU, fully periodic
+packed bed of overlapping spheres (d = 16, porosity ~0.30, seed 1), D3Q19
+TRT (omega 1.2, lambda_odd from the magic parameter 3/16), AA in-place
+streaming, fp64 PDFs, uint32 index list.  One "step" = one sweep over every
+fluid cell (AA alternates the index-list and the cell-local sweep, so K is
+kept even).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun, one rank per GPU) is weak scaling: the global box is
+N x 512^3 cut into one 512^3 block per rank along x, halo exchange by NCCL
+send/recv overlapped with the interior sweep.
+
+The JSON line carries: value (device-resident throughput, CUDA events,
+max over ranks), e2e (same metric through the public Python API with host
+buffers, H2D of the initial state + D2H of the macroscopic fields inside
+the timed region), roofline of the dominant kernel (index-list AA sweep)
+vs MEASURED_PEAKS.json, cpu_baseline (the oracle port, i.e. the reference
+algorithm in numpy, on a bounded sample), clocks sampled during the timed
+region, and gpu_launches.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "MFLUPS (fluid cell updates/s) at 1/2/4/8 B200; % of HBM roofline"
+EDGE = 512
+POROSITY = 0.30
+DIAMETER = 16.0
+SEED = 1
+OMEGA = 1.2
+Q = 19
+B_PDF, B_IDX = 8, 4
+# algorithmic bytes per fluid-cell update (model.py:59-78, GPU rows)
+BYTES_EVEN = 2 * Q * B_PDF + (Q - 1) * B_IDX  # 376: index-list sweep
+BYTES_ODD = 2 * Q * B_PDF  # 304: cell-local sweep
+
+
+def magic_lambda(omega, magic=3.0 / 16.0):
+    return 1.0 / (magic / (1.0 / omega - 0.5) + 0.5)
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ---------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.t0 = self.t1 = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu=timestamp,{self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append((time.time(), [x.strip() for x in line.split(",")]))
+
+    def mark(self, which):
+        setattr(self, which, time.time())
+
+    def stop(self):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = [r for t, r in self.rows if self.t0 is None or (self.t0 - 0.3 <= t <= (self.t1 or t) + 0.3)]
+        if not rows:
+            rows = [r for _, r in self.rows]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > 4 + i and "Active" in r[4 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------- workload
+
+
+def make_flags(edge, device, dims=None):
+    from paper_2408_06880_b200 import geometry
+
+    dims = dims or (edge, edge, edge)
+    return geometry.packed_bed_flags(dims, POROSITY, DIAMETER, SEED, periodic=True, device=device)
+
+
+def cpu_sample_edge(steps_total):
+    """Edge of the bounded CPU sample: ~150 s of oracle work at ~0.6 MFLUPS."""
+    target_fluid = 0.6e6 * 150.0 / max(steps_total, 1)
+    edge = int(round((target_fluid / POROSITY) ** (1.0 / 3.0)))
+    return max(32, min(160, edge - edge % 8))
+
+
+def run_cpu_reference(steps, warmup, edge):
+    """The reference algorithm (oracle port, numpy, single thread) timed on
+    host cores: the CPU baseline.  Returns (mfluops, n_fluid, build_s)."""
+    from oracle.sparse_ref import OracleSparseEngine
+    from paper_2408_06880_b200.collision import CollisionParams
+    from paper_2408_06880_b200.lattice import make_stencil
+
+    fl = make_flags(edge, None)
+    st = make_stencil("d3q19")
+    p = CollisionParams(OMEGA, "trt", magic_lambda(OMEGA))
+    t0 = time.perf_counter()
+    eng = OracleSparseEngine(fl, st, p, "aa")
+    build_s = time.perf_counter() - t0
+    eng.init_equilibrium(1.0, np.array([0.01, 0.0, 0.0]))
+    for _ in range(warmup):
+        eng.refresh_boundary(eng.parity)
+        eng.step()
+        eng.finish_step()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        eng.refresh_boundary(eng.parity)
+        eng.step()
+        eng.finish_step()
+    dt = time.perf_counter() - t0
+    return eng.n_fluid * steps / dt / 1e6, eng.n_fluid, build_s
+
+
+def impl_reference(args, rank, world):
+    if rank != 0:
+        return
+    steps = args.steps
+    edge = cpu_sample_edge(steps + args.warmup)
+    mflups, nf, build_s = run_cpu_reference(steps, args.warmup, edge)
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": round(mflups, 4),
+        "unit": "MFLUPS",
+        "n_gpus": args.gpus,
+        "steps": steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(nf / mflups / 1e3, 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"D3Q19 TRT AA sparse, periodic overlapping-sphere bed porosity "
+                               f"{POROSITY} d={DIAMETER:g}; reference CPU sample {edge}^3 "
+                               f"(n_fluid {nf}) of the {EDGE}^3/GPU workload"},
+        "cpu_baseline": {"value": round(mflups, 4), "unit": "MFLUPS", "cores": 1, "kind": "port",
+                         "sample": f"{edge}^3 bed, {steps} timed + {args.warmup} warm-up AA steps, "
+                                   f"build {build_s:.1f}s; numpy single-thread restatement of "
+                                   f"sparse.py (oracle/sparse_ref.py, pinned bitwise to the "
+                                   f"reference) of {os.cpu_count()} host cores"},
+        "e2e": {"value": round(mflups, 4), "unit": "MFLUPS", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+
+
+def time_kernels(eng, torch, pairs=4):
+    """Per-kernel durations (ms) of the two AA sweeps, CUDA events on the
+    engine's stream (outside the main timed region)."""
+    stream = torch.cuda.ExternalStream(eng.stream())
+    out = {0: [], 1: []}
+    for _ in range(2 * pairs):
+        parity = eng.parity.value
+        eng.refresh_boundary(eng.parity)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        eng.step()
+        b.record(stream)
+        eng.finish_step()
+        b.synchronize()
+        out[parity].append(a.elapsed_time(b))
+    return statistics.median(out[0]), statistics.median(out[1])
+
+
+def impl_ours(args, rank, world, local_rank):
+    import torch
+
+    from paper_2408_06880_b200.collision import CollisionParams
+    from paper_2408_06880_b200.engine import SparseEngine
+    from paper_2408_06880_b200.lattice import make_stencil
+
+    torch.cuda.set_device(local_rank)
+    dev = local_rank
+    st = make_stencil("d3q19")
+    p = CollisionParams(OMEGA, "trt", magic_lambda(OMEGA))
+    steps, warmup = args.steps, args.warmup
+    if steps % 2:
+        steps += 1  # AA pairs
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+    t_build = time.perf_counter()
+    if world == 1:
+        fl = make_flags(EDGE, dev)
+        eng = SparseEngine(fl, st, p, "aa", device=dev, check="deferred")
+        runner = eng
+        n_fluid_local = eng.n_fluid
+    else:
+        from paper_2408_06880_b200.domain import DistributedDomain
+
+        runner = DistributedDomain.weak_scaling_bed(
+            (EDGE, EDGE, EDGE), world, rank, st, p, POROSITY, DIAMETER, SEED, device=dev)
+        eng = runner.local_engines()[0]
+        n_fluid_local = runner.local_fluid()
+    build_s = time.perf_counter() - t_build
+
+    runner.init_equilibrium(1.0, np.array([0.01, 0.0, 0.0]))
+    runner.run(warmup)
+    runner.synchronize()
+
+    clocks = ClockSampler(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(dev)).split(",")[0])
+                          if os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")[0].isdigit()
+                          else dev)
+    clocks.start()
+    time.sleep(0.6)
+    stream = torch.cuda.ExternalStream(eng.stream())
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    clocks.mark("t0")
+    ev0.record(stream)
+    runner.run(steps)
+    ev1.record(stream)
+    runner.synchronize()
+    torch.cuda.synchronize()
+    clocks.mark("t1")
+    ms = ev0.elapsed_time(ev1)
+    if dist is not None:
+        t = torch.tensor([ms], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    runner.poll()
+
+    # per-kernel roofline (index-list sweep = dominant kernel)
+    t_even, t_odd = time_kernels(eng, torch)
+    clocks.stop()
+    csum = clocks.summary()
+
+    total_fluid = n_fluid_local
+    if dist is not None:
+        t = torch.tensor([n_fluid_local], device=f"cuda:{dev}", dtype=torch.float64)
+        dist.all_reduce(t)
+        total_fluid = int(t.item())
+    value = total_fluid * steps / (ms / 1e3) / 1e6
+
+    # e2e through the public API with host buffers (rank 0 engine, N = 1)
+    e2e = None
+    if world == 1:
+        e2e = e2e_run(eng, steps, torch)
+
+    launches_per_step = 2 + (1 if eng.n_ubb_slots else 0)
+    hbm, hbm_src = peaks()
+    ach_even = eng.n_fluid * BYTES_EVEN / (t_even / 1e3) / 1e9
+    ach_odd = eng.n_fluid * BYTES_ODD / (t_odd / 1e3) / 1e9
+    pair = eng.n_fluid * (BYTES_EVEN + BYTES_ODD) / ((t_even + t_odd) / 1e3) / 1e9
+    traffic = load_traffic()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        edge = 64
+        c_steps = 6
+        mfl, nf, bs = run_cpu_reference(c_steps, 2, edge)
+        cpu = {"value": round(mfl, 4), "unit": "MFLUPS", "cores": 1, "kind": "port",
+               "sample": f"{edge}^3 bed of the same law (n_fluid {nf}), {c_steps} timed AA steps "
+                         f"after 2 warm-up, build {bs:.1f}s; oracle/sparse_ref.py numpy "
+                         f"restatement of sparse.py on 1 of {os.cpu_count()} host cores"}
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC,
+        "value": round(value, 2),
+        "unit": "MFLUPS",
+        "n_gpus": world,
+        "steps": steps,
+        "warmup": warmup,
+        "ms_per_step": round(ms / steps, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {
+            "workload": f"D3Q19 TRT AA sparse stream-collide, {EDGE}^3 cells per GPU, periodic "
+                        f"overlapping-sphere packed bed porosity {POROSITY} (d={DIAMETER:g}, "
+                        f"seed {SEED})",
+            "n_fluid_per_gpu": eng.n_fluid,
+            "porosity": round(eng.n_fluid / EDGE**3, 4),
+            "decomposition": f"{world}x1x1 blocks of {EDGE}^3",
+            "l2": "inputs larger than L2 (PDF + index list ~9 GB per GPU)",
+            "build_s": round(build_s, 2),
+            "omega": OMEGA,
+            "lambda_odd": round(magic_lambda(OMEGA), 6),
+        },
+        "roofline": {
+            "bound": "hbm",
+            "kernel": "k_aa_even<D3Q19,TRT> (index-list AA sweep)",
+            "achieved": round(ach_even, 1),
+            "peak": hbm,
+            "unit": "GB/s",
+            "frac": round(ach_even / hbm, 4),
+            "traffic": traffic,
+            "bytes_per_cell": BYTES_EVEN,
+            "peak_source": hbm_src,
+            "ms_per_launch": round(t_even, 4),
+            "odd_kernel": {"kernel": "k_aa_odd<D3Q19,TRT>", "achieved": round(ach_odd, 1),
+                           "frac": round(ach_odd / hbm, 4), "bytes_per_cell": BYTES_ODD,
+                           "ms_per_launch": round(t_odd, 4)},
+            "pair_frac": round(pair / hbm, 4),
+        },
+        "clocks": csum,
+        "gpu_launches": launches_per_step * steps,
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+
+
+def e2e_run(eng, steps, torch):
+    """Same metric through the public engine API: initial state from pinned
+    host memory (H2D), K steps driven from Python exactly like the
+    reference's drive() loop (refresh_boundary/step/finish_step, instability
+    polled every step), macroscopic fields read back (D2H)."""
+    q, n = eng.stencil.q, eng.n_fluid
+    host = torch.empty((q, n), dtype=torch.float64, pin_memory=True).numpy()
+    w = eng.stencil.w
+    for r in range(q):
+        host[r].fill(w[r])
+    eng.check = "step"
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    eng.init_canonical(host)
+    for _ in range(steps):
+        eng.refresh_boundary(eng.parity)
+        eng.step()
+        eng.finish_step()
+    rho, u = eng.macroscopic_fields()
+    dt = time.perf_counter() - t0
+    eng.check = "deferred"
+    cells = int(np.prod(eng.dims))
+    return {"value": round(n * steps / dt / 1e6, 2), "unit": "MFLUPS",
+            "h2d_bytes_per_step": int(q * n * 8 // steps),
+            "d2h_bytes_per_step": int((rho.nbytes + u.nbytes) // steps),
+            "seconds": round(dt, 4), "steps": steps,
+            "note": f"init_canonical({q}x{n} f64 pinned) + {steps} x Python drive loop + "
+                    f"macroscopic_fields({cells} cells)"}
+
+
+def load_traffic():
+    """ncu dram bytes per launch of the dominant kernel, if a summary is
+    committed under profiles/ (written by tools/ncu_summary.py)."""
+    path = os.path.join(ROOT, "profiles", "latest_traffic.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return d.get("k_aa_even_dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        impl_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    impl_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,211 @@
+/*
+ * slbm_b200 — C-ABI of the B200 (sm_100a) sparse lattice-Boltzmann engine.
+ *
+ * The reference package has no FFI: its drop-in boundary is the duck-typed
+ * block-engine protocol of pkg/src/slbm/sparse.py (SparseEngine, :48-383),
+ * consumed by Domain (domain.py:109-114), the halo EdgePlans/pack/unpack
+ * (exchange.py:125-253) and the drivers (exchange.py:330-374).  Every entry
+ * point below replaces one method/attribute of that protocol; the Python
+ * class paper_2408_06880_b200.engine.SparseEngine wraps them 1:1 (ctypes).
+ *
+ * Conventions
+ *   - plain pointers and sizes only; "host" pointers are ordinary CPU
+ *     memory, "dev" pointers are device memory on the engine's GPU;
+ *   - every function returns an SLBM_* status; slbm_last_error() returns the
+ *     message of the last failure on the calling thread;
+ *   - an engine handle is not thread-safe (one owner per block, like the
+ *     reference); work is issued on the engine's stream
+ *     (slbm_engine_stream / slbm_engine_set_stream);
+ *   - slot ids, cell ids (cid) and the index list are identical to the
+ *     reference's (sparse.py:97-195), so exported arrays compare with
+ *     np.array_equal.
+ */
+#ifndef SLBM_B200_H
+#define SLBM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes -> exceptions of pkg/src/slbm/errors.py:4-29 */
+#define SLBM_OK 0
+#define SLBM_ECONFIG 1   /* ConfigurationError */
+#define SLBM_EEMPTY 2    /* EmptyBlockError */
+#define SLBM_EUNSTABLE 3 /* NumericalInstabilityError */
+#define SLBM_EPROTOCOL 4 /* ProtocolError */
+#define SLBM_ECUDA 5     /* RuntimeError */
+
+/* collision models (core.py:66-74 has srt/trt; cumulant is new, unpinned) */
+#define SLBM_SRT 0
+#define SLBM_TRT 1
+#define SLBM_CUMULANT 2
+
+/* streaming patterns (sparse.py:45) */
+#define SLBM_PULL 0
+#define SLBM_AA 1
+
+/* sweep phases (sparse.py:226-231) */
+#define SLBM_PHASE_ALL 0
+#define SLBM_PHASE_INTERIOR 1
+#define SLBM_PHASE_FRAME 2
+
+/* storage parity (core.py:32-47) */
+#define SLBM_EVEN 0
+#define SLBM_ODD 1
+
+typedef struct SlbmEngine SlbmEngine;
+typedef struct SlbmHalo SlbmHalo;
+
+typedef struct SlbmInfo {
+  int32_t q, dim, pattern, parity;
+  int32_t has_split, model;
+  int64_t n_fluid;       /* sparse.py:75 */
+  int64_t total_slots;   /* sparse.py:131 */
+  int64_t n_ubb_slots;   /* sparse.py:136 */
+  int64_t n_ghost_slots; /* sparse.py:137 */
+  int64_t n_interior, n_frame; /* sparse.py:377-383 */
+  int64_t base[28];      /* sparse.py:130, length q+1 used */
+  int64_t n_ubb_q[27];
+  int64_t n_ghost_q[27];
+  int64_t device_bytes;  /* bytes of device memory held by the engine */
+} SlbmInfo;
+
+/* ---- construction: SparseEngine.__init__ (sparse.py:51-93) ----------------
+ * tags_pad  host uint8 tags on the padded box, C order over reversed axes
+ *           ((Z+2,Y+2,X+2) for 3-d, (Y+2,X+2) for 2-d)          flags.py:111-125
+ * ubb_u_pad host float64 wall velocities, tags_pad shape + (dim,); may be NULL
+ *           when no tag is UBB
+ * dims      public extents (x, y[, z]); periodic: per public axis (0/1)
+ * q         9 (d2q9, dim 2), 19 or 27 (dim 3)
+ * frame_width per public axis, or NULL for no interior/frame split
+ *           (flags.py:83-108; widths >= 1, clamped to the extent)
+ * Runs the whole list build on the GPU: fluid enumeration, index list with
+ * no-slip folding, UBB and ghost slot allocation, the ownership-uniqueness
+ * check (sparse.py:182-185) and the split lists.  PDFs start NaN-poisoned
+ * (sparse.py:90-91).                                                        */
+int slbm_engine_create(const uint8_t* tags_pad, const double* ubb_u_pad, int dim,
+                       const int32_t* dims, const uint8_t* periodic, int q, int model,
+                       double omega, double lambda_odd, int pattern,
+                       const int32_t* frame_width, int device, SlbmEngine** out);
+int slbm_engine_destroy(SlbmEngine* eng);
+int slbm_engine_info(const SlbmEngine* eng, SlbmInfo* info);
+/* cudaStream_t as void*; set_stream(NULL) restores the engine's own stream */
+int slbm_engine_stream(const SlbmEngine* eng, void** stream);
+int slbm_engine_set_stream(SlbmEngine* eng, void* stream);
+int slbm_engine_set_params(SlbmEngine* eng, int model, double omega, double lambda_odd);
+
+/* ---- exported lists (for parity checks against the reference) -----------
+ * idx: (q-1, n_fluid) uint32 (sparse.py:186); fluid_coords: (n_fluid, dim)
+ * int64 public coords (sparse.py:76); ubb_*: n_ubb_slots (sparse.py:188-191);
+ * ghost_q/ghost_pflat/ghost_slot: n_ghost_slots entries of the reference's
+ * _ghost_slots dict (sparse.py:179), in slot order.  Any pointer may be NULL. */
+int slbm_export_lists(const SlbmEngine* eng, uint32_t* idx, int64_t* fluid_coords,
+                      int64_t* ubb_slot, int64_t* ubb_partner, double* ubb_corr,
+                      int64_t* ghost_q, int64_t* ghost_pflat, int64_t* ghost_slot);
+/* frame / interior cell ids (sparse.py:80-88); NULL pointers skipped */
+int slbm_export_split(const SlbmEngine* eng, int64_t* interior, int64_t* frame);
+
+/* ---- state (sparse.py:199-222, :308-331) --------------------------------- */
+/* values: host (q, n_fluid) float64 canonical state; parity -> EVEN */
+int slbm_init_canonical(SlbmEngine* eng, const double* values);
+/* device-pointer variant of init_canonical (values already on the GPU) */
+int slbm_init_canonical_dev(SlbmEngine* eng, const double* dev_values);
+/* equilibrium from per-cell rho (n) and u (dim, n), host pointers; rho/u may
+ * be scalars when the *_scalar flag is 1 (u then has dim entries)           */
+int slbm_init_equilibrium(SlbmEngine* eng, const double* rho, int rho_scalar,
+                          const double* u, int u_scalar);
+/* host (q, n_fluid); at ODD parity refreshes UBB partners first (:317)     */
+int slbm_canonical_state(SlbmEngine* eng, double* values);
+/* host rho (rev_shape) and u (rev_shape + (dim,)), zeros at non-fluid cells;
+ * SLBM_EUNSTABLE when a density is <= 0 or non-finite (core.py:108-111)    */
+int slbm_macroscopic(SlbmEngine* eng, double* rho, double* u);
+/* sum over fluid cells and directions of the canonical state (mass), fp64 */
+int slbm_total_mass(SlbmEngine* eng, double* mass);
+
+/* ---- stepping (sparse.py:226-304) ---------------------------------------- */
+int slbm_refresh_boundary(SlbmEngine* eng, int parity);
+/* launches one sweep; does not synchronize */
+int slbm_step(SlbmEngine* eng, int phase);
+int slbm_finish_step(SlbmEngine* eng);
+/* n full single-block steps (refresh_boundary + step(all) + finish_step), no
+ * host sync; use_graph=1 replays a captured CUDA graph of one step pair.   */
+int slbm_run(SlbmEngine* eng, int64_t n, int use_graph);
+/* blocks until the engine's stream is idle, then reports the first unstable
+ * step (SLBM_EUNSTABLE, *first_bad_step set) or SLBM_OK (-1).  Clears.     */
+int slbm_poll_instability(SlbmEngine* eng, int64_t* first_bad_step);
+int slbm_synchronize(SlbmEngine* eng);
+int slbm_parity(const SlbmEngine* eng, int* parity);
+int slbm_set_parity(SlbmEngine* eng, int parity);
+
+/* ---- slot access for halo plans (sparse.py:335-366) ---------------------- */
+/* pflat: padded flat index of the cell (C order over the padded box)       */
+int slbm_slot_index(const SlbmEngine* eng, const int64_t* qs, const int64_t* pflat,
+                    int64_t n, int64_t* out);
+int slbm_ghost_slot_index(const SlbmEngine* eng, const int64_t* qs, const int64_t* pflat,
+                          int64_t n, int64_t* out);
+int slbm_read_slots(SlbmEngine* eng, const int64_t* slots, int64_t n, double* out);
+int slbm_write_slots(SlbmEngine* eng, const int64_t* slots, int64_t n, const double* in);
+/* raw device pointer of the active PDF buffer (pull swaps it every step) */
+int slbm_pdf_pointer(const SlbmEngine* eng, double** dev_pdf);
+
+/* ---- halo exchange (exchange.py:125-374) ---------------------------------
+ * A halo is the per-rank exchange program for one phase set: a list of
+ * directed edges, each a (sender engine, receiver engine) pair with the
+ * sender's read slots and the receiver's write slots per phase
+ * (EdgePlan._build, exchange.py:148-219).  Edges whose two engines live in
+ * this process are moved by one fused gather-scatter kernel; edges with a
+ * remote end are packed into / unpacked from per-peer contiguous buffers
+ * that travel with ncclSend/ncclRecv (one message per peer per phase).    */
+int slbm_halo_create(int device, SlbmHalo** out);
+int slbm_halo_destroy(SlbmHalo* halo);
+/* local edge: both engines here. send[n_send] on src, take[n_tgt] indexes
+ * the send list (exchange.py:199-201), tgt[n_tgt] on dst.                 */
+int slbm_halo_add_local(SlbmHalo* halo, int phase, SlbmEngine* src, SlbmEngine* dst,
+                        const int64_t* send, int64_t n_send, const int64_t* take,
+                        const int64_t* tgt, int64_t n_tgt);
+/* remote send: values of send[n] on src go to peer rank `peer`, appended to
+ * that peer's message for this phase in call order                         */
+int slbm_halo_add_send(SlbmHalo* halo, int phase, SlbmEngine* src, int peer,
+                       const int64_t* send, int64_t n);
+/* remote receive: the next n_wire values of peer's message; take[n_tgt]
+ * picks the stored ones, written to tgt on dst                              */
+int slbm_halo_add_recv(SlbmHalo* halo, int phase, SlbmEngine* dst, int peer,
+                       int64_t n_wire, const int64_t* take, const int64_t* tgt, int64_t n_tgt);
+/* finalize: allocates device buffers; nccl_comm may be NULL when the halo
+ * has no remote edges.  nccl_comm is an ncclComm_t created by the caller
+ * or by slbm_nccl_comm_init.                                                */
+int slbm_halo_commit(SlbmHalo* halo, void* nccl_comm);
+/* start the exchange for `phase` on the halo's comm stream after the work
+ * already queued on `after_stream` (NULL = none); pack + send/recv + unpack */
+int slbm_halo_start(SlbmHalo* halo, int phase, void* after_stream);
+/* make `stream` wait for the exchange started last */
+int slbm_halo_wait(SlbmHalo* halo, void* stream);
+/* host-staged transport for tests without NCCL: pack into host buffers
+ * per peer / unpack from host buffers (byte counts via halo_peer_sizes)   */
+int slbm_halo_peer_sizes(const SlbmHalo* halo, int phase, int npeers, int64_t* send_counts,
+                         int64_t* recv_counts);
+int slbm_halo_pack_host(SlbmHalo* halo, int phase, int peer, double* host_out);
+int slbm_halo_unpack_host(SlbmHalo* halo, int phase, int peer, const double* host_in);
+int slbm_halo_local(SlbmHalo* halo, int phase); /* only the local edges, on comm stream */
+
+/* NCCL communicator from a 128-byte ncclUniqueId (broadcast by the caller) */
+int slbm_nccl_comm_init(const void* unique_id, int nranks, int rank, int device, void** comm);
+int slbm_nccl_get_unique_id(void* unique_id_out);
+int slbm_nccl_comm_destroy(void* comm);
+
+/* ---- geometry helper: overlapping-sphere voxelizer on the GPU -----------
+ * Same rasterization rule as geometry.py:150-178 (cell solid iff its centre
+ * lies strictly inside a sphere; resolution 1).  solid: host uint8 over
+ * rev_shape(dims) (1 = solid).  centers: (n, 3) public-order float64.     */
+int slbm_voxelize_spheres(const int32_t* dims, const double* centers, int64_t n,
+                          double diameter, int device, uint8_t* solid);
+
+const char* slbm_last_error(void);
+const char* slbm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLBM_B200_H */

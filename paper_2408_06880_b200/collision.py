@@ -1,0 +1,82 @@
+"""Collision configuration and in-place storage parity.
+
+``CollisionParams`` validates like the reference (``pkg/src/slbm/core.py:
+50-74``) and adds the cumulant model the reference lacks (
+its parity is *unpinned*).  The arithmetic itself lives in
+the CUDA kernels (``csrc/collide.cuh``); there is deliberately no host
+implementation of it in the product package.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from enum import Enum
+
+from . import errors
+from .lattice import CS2
+
+UBB_WALL_DENSITY = 1.0
+
+MODELS = ("srt", "trt", "cumulant")
+MODEL_CODE = {"srt": 0, "trt": 1, "cumulant": 2}
+
+
+class Parity(Enum):
+    """EVEN: slot (q, cell) holds the value moving along q.  ODD: the state
+    left by the combined (index-list) AA step, values parked in the
+    opposite-direction slots.  The reference names the combined step's
+    input EVEN (``core.py:32-47``; the paper calls that step "odd")."""
+
+    EVEN = 0
+    ODD = 1
+
+    def flipped(self) -> "Parity":
+        return Parity.ODD if self is Parity.EVEN else Parity.EVEN
+
+
+@dataclass
+class CollisionParams:
+    omega: float
+    model: str = "srt"
+    lambda_odd: float | None = None
+
+    def __post_init__(self) -> None:
+        if not (0.0 < self.omega < 2.0):
+            raise errors.make("ConfigurationError", f"omega must lie in (0, 2), got {self.omega}")
+        if self.model not in MODELS:
+            raise errors.make("ConfigurationError", f"unknown collision model {self.model!r}")
+        if self.model == "trt":
+            if self.lambda_odd is None:
+                raise errors.make("ConfigurationError", "trt requires lambda_odd")
+            if not (0.0 < self.lambda_odd < 2.0):
+                raise errors.make(
+                    "ConfigurationError", f"lambda_odd must lie in (0, 2), got {self.lambda_odd}"
+                )
+
+
+def omega_from_viscosity(nu: float) -> float:
+    if nu <= 0.0:
+        raise errors.make("ConfigurationError", f"viscosity must be positive, got {nu}")
+    return 1.0 / (nu / CS2 + 0.5)
+
+
+def viscosity_from_omega(omega: float) -> float:
+    if not (0.0 < omega < 2.0):
+        raise errors.make("ConfigurationError", f"omega must lie in (0, 2), got {omega}")
+    return CS2 * (1.0 / omega - 0.5)
+
+
+def trt_magic_lambda(omega: float, magic: float = 3.0 / 16.0) -> float:
+    """Odd rate giving the TRT "magic" parameter Lambda = (1/w_e - 1/2)(1/w_o - 1/2)."""
+    even = 1.0 / omega - 0.5
+    return 1.0 / (magic / even + 0.5)
+
+
+def params_code(params) -> tuple[int, float, float]:
+    """(model code, omega, lambda_odd) for the C-ABI; accepts the
+    reference's CollisionParams too (duck-typed)."""
+    model = getattr(params, "model", "srt")
+    if model not in MODEL_CODE:
+        raise errors.make("ConfigurationError", f"unknown collision model {model!r}")
+    lam = getattr(params, "lambda_odd", None)
+    return MODEL_CODE[model], float(params.omega), float(lam if lam is not None else params.omega)

@@ -1,0 +1,501 @@
+// GPU list builder: fluid enumeration, index list with no-slip folding,
+// moving-wall (UBB) and halo (ghost) slot allocation, ownership check and
+// interior/frame split.  Reproduces pkg/src/slbm/sparse.py:72-195 bit for
+// bit:
+//
+//   cells      fluid cells of the interior in C order over (z, y, x)
+//              (sparse.py:72-76)  -> cub::DeviceSelect over the interior
+//   pass 1     upwind tag of every (q >= 1, cell) read, wrapping periodic
+//              axes first (sparse.py:110-126) -> per-q UBB / ghost counts
+//   base       prefix sum of N_F + n_ubb[q] + n_ghost[q] (sparse.py:128-137)
+//   pass 2     FLUID  -> base[q] + cid(upwind)             (sparse.py:149-152)
+//              NOSLIP -> base[inv q] + cid                  (:154-155)
+//              UBB    -> base[q] + N_F + rank in cid order  (:157-164)
+//              EXCH.  -> base[q] + N_F + n_ubb[q] + rank by (ring offset,
+//                        padded flat index)                 (:166-179)
+//   unique     every slot owned by exactly one (direction, cell) read
+//              (:182-185) -> atomic bitset
+//   split      frame = within the per-axis width of a face (flags.py:83-108)
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstring>
+
+#include "engine.cuh"
+
+namespace slbm {
+namespace {
+
+constexpr uint8_t kFluid = 0, kNoslip = 1, kUbb = 2, kExchange = 3;
+
+__host__ __device__ inline int64_t wrap(int64_t v, int64_t n) {
+  int64_t r = v % n;
+  return r < 0 ? r + n : r;
+}
+
+struct Upwind {
+  Geometry g;
+  DirTable d;
+  // padded flat index of the cell a direction-q read of (x, y, z) comes from
+  __device__ __forceinline__ int64_t operator()(int q, int64_t x, int64_t y, int64_t z) const {
+    int64_t s[3] = {x - d.c[q][0], y - d.c[q][1], z - d.c[q][2]};
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      if (g.periodic[a]) s[a] = wrap(s[a], g.n[a]);
+    return g.padded_flat(s[0], s[1], s[2]);
+  }
+};
+
+struct InteriorToPadded {
+  Geometry g;
+  __host__ __device__ uint32_t operator()(int64_t i) const {
+    int64_t x = i % g.n[0];
+    int64_t r = i / g.n[0];
+    int64_t y = r % g.n[1];
+    int64_t z = r / g.n[1];
+    return uint32_t(g.padded_flat(x, y, z));
+  }
+};
+
+struct FluidAt {
+  const uint8_t* tags;
+  __device__ bool operator()(uint32_t p) const { return tags[p] == kFluid; }
+};
+
+// selects cells whose direction-q read hits tag `want`
+struct ReadsTag {
+  const uint8_t* tags;
+  const uint32_t* x_flat;
+  Upwind up;
+  int q;
+  uint8_t want;
+  __device__ bool operator()(uint32_t c) const {
+    int64_t x, y, z;
+    up.g.coords(x_flat[c], x, y, z);
+    return tags[up(q, x, y, z)] == want;
+  }
+};
+
+struct InFrame {
+  const uint32_t* x_flat;
+  Geometry g;
+  int32_t w[3];
+  bool want;
+  __device__ bool operator()(uint32_t c) const {
+    int64_t v[3];
+    g.coords(x_flat[c], v[0], v[1], v[2]);
+    bool in = false;
+    for (int a = 0; a < g.dim; ++a) in |= (v[a] < w[a]) || (v[a] >= g.n[a] - w[a]);
+    return in == want;
+  }
+};
+
+__global__ void k_cid_map(const uint32_t* x_flat, int64_t n, int32_t* cid_map) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) cid_map[x_flat[i]] = int32_t(i);
+}
+
+// pass 1: per-direction UBB / ghost counts and sanity of every upwind tag
+__global__ void k_count(const uint8_t* tags, const int32_t* cid_map, const uint32_t* x_flat,
+                        int64_t n, Upwind up, unsigned long long* counts, int* err) {
+  __shared__ unsigned int s_cnt[54];
+  for (int i = threadIdx.x; i < 54; i += blockDim.x) s_cnt[i] = 0;
+  __syncthreads();
+  for (int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < n;
+       c += int64_t(gridDim.x) * blockDim.x) {
+    int64_t x, y, z;
+    up.g.coords(x_flat[c], x, y, z);
+    for (int q = 1; q < up.d.q; ++q) {
+      int64_t p = up(q, x, y, z);
+      uint8_t tag = tags[p];
+      if (tag == kUbb) {
+        atomicAdd(&s_cnt[2 * q], 1u);
+      } else if (tag == kExchange) {
+        atomicAdd(&s_cnt[2 * q + 1], 1u);
+      } else if (tag == kFluid) {
+        if (cid_map[p] < 0) atomicOr(err, 1);
+      } else if (tag != kNoslip) {
+        atomicOr(err, 2);
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 54; i += blockDim.x)
+    if (s_cnt[i]) atomicAdd(&counts[i], (unsigned long long)s_cnt[i]);
+}
+
+struct Bases {
+  uint32_t b[28];
+};
+
+// pass 2 for in-list reads: FLUID -> neighbour slot, NOSLIP -> own opposite
+// slot; UBB / EXCHANGE entries are assigned by the ranked passes below
+__global__ void k_fill(const uint8_t* tags, const int32_t* cid_map, const uint32_t* x_flat,
+                       int64_t n, Upwind up, Bases bases, uint32_t* idx) {
+  int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  int64_t x, y, z;
+  up.g.coords(x_flat[c], x, y, z);
+  for (int q = 1; q < up.d.q; ++q) {
+    int64_t p = up(q, x, y, z);
+    uint8_t tag = tags[p];
+    uint32_t v = 0xffffffffu;
+    if (tag == kFluid)
+      v = bases.b[q] + uint32_t(cid_map[p]);
+    else if (tag == kNoslip)
+      v = bases.b[up.d.inv[q]] + uint32_t(c);
+    idx[(q - 1) * n + c] = v;
+  }
+}
+
+__device__ int64_t find_sorted(const uint32_t* keys, int64_t n, uint32_t key) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (keys[mid] < key)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return (lo < n && keys[lo] == key) ? lo : -1;
+}
+
+// UBB reads of direction q, `sel` = cells in cid order (sparse.py:157-164)
+__global__ void k_ubb_assign(const uint32_t* sel, int64_t cnt, int q, const uint32_t* x_flat,
+                             int64_t n, Upwind up, Bases bases, const uint32_t* wall_flat,
+                             const double* wall_u, int64_t n_wall, uint32_t* idx,
+                             uint32_t* ubb_slot, uint32_t* ubb_partner, double* ubb_corr,
+                             int* err) {
+  int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= cnt) return;
+  uint32_t c = sel[k];
+  uint32_t slot = bases.b[q] + uint32_t(n) + uint32_t(k);
+  idx[(q - 1) * n + c] = slot;
+  ubb_slot[k] = slot;
+  ubb_partner[k] = bases.b[up.d.inv[q]] + c;
+  int64_t x, y, z;
+  up.g.coords(x_flat[c], x, y, z);
+  uint32_t p = uint32_t(up(q, x, y, z));
+  int64_t at = find_sorted(wall_flat, n_wall, p);
+  if (at < 0) {
+    atomicOr(err, 4);
+    return;
+  }
+  // core.py:173-188: cu accumulated from 0 by +/- u_a; 2*w*rho_w*cu/cs2
+  double cu = 0.0;
+  for (int a = 0; a < up.g.dim; ++a) {
+    if (up.d.c[q][a] == 1) cu = cu + wall_u[at * 3 + a];
+    if (up.d.c[q][a] == -1) cu = cu - wall_u[at * 3 + a];
+  }
+  const double cs2 = 1.0 / 3.0;
+  ubb_corr[k] = (((2.0 * up.d.w[q]) * 1.0) * cu) / cs2;
+}
+
+// ghost keys: (ring offset of the upwind halo cell, its padded flat index)
+__global__ void k_ghost_keys(const uint32_t* sel, int64_t cnt, int q, const uint32_t* x_flat,
+                             Upwind up, uint64_t* keys) {
+  int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= cnt) return;
+  int64_t x, y, z;
+  up.g.coords(x_flat[sel[k]], x, y, z);
+  int64_t p = up(q, x, y, z);
+  int64_t v[3];
+  up.g.coords(p, v[0], v[1], v[2]);
+  int sig = 0;
+  for (int a = 0; a < 3; ++a) {
+    int s = 0;
+    if (a < up.g.dim) s = v[a] < 0 ? -1 : (v[a] >= up.g.n[a] ? 1 : 0);
+    sig = sig * 3 + (s + 1);
+  }
+  keys[k] = (uint64_t(sig) << 32) | uint64_t(p);
+}
+
+__global__ void k_ghost_assign(const uint32_t* sorted_cells, int64_t cnt, int q, int64_t n,
+                               uint32_t first_slot, uint32_t* idx) {
+  int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= cnt) return;
+  idx[(q - 1) * n + sorted_cells[k]] = first_slot + uint32_t(k);
+}
+
+__global__ void k_unique(const uint32_t* idx, int64_t n, int q, uint64_t total,
+                         unsigned int* bits, int* err) {
+  int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= int64_t(q) * n) return;
+  uint64_t slot = (t < n) ? uint64_t(t) : uint64_t(idx[t - n]);
+  if (slot >= total) {
+    atomicOr(err, 8);
+    return;
+  }
+  unsigned int bit = 1u << (slot & 31);
+  unsigned int old = atomicOr(&bits[slot >> 5], bit);
+  if (old & bit) atomicOr(err, 16);
+}
+
+inline unsigned grid_for(int64_t n, int block) {
+  int64_t g = (n + block - 1) / block;
+  return unsigned(std::max<int64_t>(g, 1));
+}
+
+// cub select into `out` (capacity n); returns the count on the host
+template <class InIt, class Pred, class T>
+int select_if(InIt in, T* out, int64_t n, Pred pred, int64_t* count, cudaStream_t s) {
+  int64_t* d_num = nullptr;
+  SLBM_CUDA_TRY(cudaMallocAsync(&d_num, sizeof(int64_t), s));
+  size_t tmp_bytes = 0;
+  SLBM_CUDA_TRY(cub::DeviceSelect::If(nullptr, tmp_bytes, in, out, d_num, n, pred, s));
+  void* tmp = nullptr;
+  SLBM_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, s));
+  SLBM_CUDA_TRY(cub::DeviceSelect::If(tmp, tmp_bytes, in, out, d_num, n, pred, s));
+  SLBM_CUDA_TRY(cudaMemcpyAsync(count, d_num, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  SLBM_CUDA_TRY(cudaFreeAsync(tmp, s));
+  SLBM_CUDA_TRY(cudaFreeAsync(d_num, s));
+  SLBM_CUDA_TRY(cudaStreamSynchronize(s));
+  return SLBM_OK;
+}
+
+template <class T>
+int dalloc(SlbmEngine* e, T** p, int64_t count) {
+  size_t bytes = size_t(std::max<int64_t>(count, 1)) * sizeof(T);
+  cudaError_t err = cudaMalloc(p, bytes);
+  if (err != cudaSuccess)
+    return fail(SLBM_ECUDA, std::string("cudaMalloc of ") + std::to_string(bytes) +
+                                " bytes failed: " + cudaGetErrorString(err));
+  e->device_bytes += int64_t(bytes);
+  return SLBM_OK;
+}
+
+std::string dims_str(const Geometry& g) {
+  std::string s = "(" + std::to_string(g.n[0]) + ", " + std::to_string(g.n[1]);
+  if (g.dim == 3) s += ", " + std::to_string(g.n[2]);
+  return s + ")";
+}
+
+}  // namespace
+
+int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
+                const int32_t* frame_width) {
+  const Geometry& g = e->geo;
+  const DirTable& d = e->dirs;
+  cudaStream_t s = e->stream;
+  const int64_t n_pad = g.n_padded();
+  if (n_pad >= (int64_t(1) << 32) - 1)
+    return fail(SLBM_ECONFIG, "padded block has >= 2^32 cells; use smaller blocks");
+
+  // moving-wall velocity table: padded positions tagged UBB, ascending
+  std::vector<uint32_t> wall_flat;
+  std::vector<double> wall_u;
+  for (int64_t p = 0; p < n_pad; ++p) {
+    if (tags_pad[p] != kUbb) continue;
+    if (!ubb_u_pad) return fail(SLBM_ECONFIG, "UBB tags present but no wall velocity array");
+    wall_flat.push_back(uint32_t(p));
+    for (int a = 0; a < 3; ++a) wall_u.push_back(a < g.dim ? ubb_u_pad[p * g.dim + a] : 0.0);
+  }
+
+  uint8_t* d_tags = nullptr;
+  SLBM_CUDA_TRY(cudaMalloc(&d_tags, n_pad));
+  SLBM_CUDA_TRY(cudaMemcpyAsync(d_tags, tags_pad, n_pad, cudaMemcpyHostToDevice, s));
+
+  // -- fluid enumeration (sparse.py:72-76) --
+  const int64_t n_cells = g.n_cells();
+  uint32_t* sel_buf = nullptr;  // reused selection buffer, capacity max(n_cells, ...)
+  SLBM_CUDA_TRY(cudaMalloc(&sel_buf, sizeof(uint32_t) * std::max<int64_t>(n_cells, 1)));
+  auto interior = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0),
+                                                  InteriorToPadded{g});
+  int64_t n_fluid = 0;
+  SLBM_TRY(select_if(interior, sel_buf, n_cells, FluidAt{d_tags}, &n_fluid, s));
+  if (n_fluid == 0) {
+    cudaFree(sel_buf);
+    cudaFree(d_tags);
+    return fail(SLBM_EEMPTY, "block " + dims_str(g) + " has no fluid cells");
+  }
+  e->n_fluid = n_fluid;
+  const int64_t n = n_fluid;
+  SLBM_TRY(dalloc(e, &e->x_flat, n));
+  SLBM_CUDA_TRY(cudaMemcpyAsync(e->x_flat, sel_buf, n * sizeof(uint32_t),
+                                cudaMemcpyDeviceToDevice, s));
+  SLBM_TRY(dalloc(e, &e->cid_map, n_pad));
+  SLBM_CUDA_TRY(cudaMemsetAsync(e->cid_map, 0xff, n_pad * sizeof(int32_t), s));
+  k_cid_map<<<grid_for(n, 256), 256, 0, s>>>(e->x_flat, n, e->cid_map);
+
+  // -- pass 1: counts --
+  Upwind up{g, d};
+  unsigned long long* d_counts = nullptr;
+  int* d_err = nullptr;
+  SLBM_CUDA_TRY(cudaMalloc(&d_counts, 54 * sizeof(unsigned long long)));
+  SLBM_CUDA_TRY(cudaMalloc(&d_err, sizeof(int)));
+  SLBM_CUDA_TRY(cudaMemsetAsync(d_counts, 0, 54 * sizeof(unsigned long long), s));
+  SLBM_CUDA_TRY(cudaMemsetAsync(d_err, 0, sizeof(int), s));
+  {
+    int dev_sms = 148;
+    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, e->device);
+    unsigned blocks = std::min<unsigned>(grid_for(n, 256), unsigned(dev_sms) * 8);
+    k_count<<<blocks, 256, 0, s>>>(d_tags, e->cid_map, e->x_flat, n, up, d_counts, d_err);
+  }
+  unsigned long long h_counts[54];
+  int h_err = 0;
+  SLBM_CUDA_TRY(cudaMemcpyAsync(h_counts, d_counts, sizeof(h_counts), cudaMemcpyDeviceToHost, s));
+  SLBM_CUDA_TRY(cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SLBM_CUDA_TRY(cudaStreamSynchronize(s));
+  auto cleanup = [&]() {
+    cudaFree(d_counts);
+    cudaFree(d_err);
+    cudaFree(sel_buf);
+    cudaFree(d_tags);
+  };
+  if (h_err & 1) {
+    cleanup();
+    return fail(SLBM_ECONFIG, "fluid upwind cell missing from cell list (fluid tag in the ring "
+                              "of a non-periodic axis)");
+  }
+  if (h_err & 2) {
+    cleanup();
+    return fail(SLBM_ECONFIG, "unknown tag value upwind of a fluid cell");
+  }
+
+  // -- slot budget (sparse.py:128-137) --
+  int64_t total = 0;
+  e->base[0] = 0;
+  for (int q = 0; q < d.q; ++q) {
+    int64_t nu = q ? int64_t(h_counts[2 * q]) : 0;
+    int64_t ng = q ? int64_t(h_counts[2 * q + 1]) : 0;
+    e->n_ubb_q[q] = nu;
+    e->n_ghost_q[q] = ng;
+    total += n + nu + ng;
+    e->base[q + 1] = total;
+  }
+  e->total_slots = total;
+  e->n_ubb = e->n_ghost = 0;
+  e->ubb_off[0] = e->ghost_off[0] = 0;
+  for (int q = 0; q < d.q; ++q) {
+    e->n_ubb += e->n_ubb_q[q];
+    e->n_ghost += e->n_ghost_q[q];
+    e->ubb_off[q + 1] = e->n_ubb;
+    e->ghost_off[q + 1] = e->n_ghost;
+  }
+  if (total >= (int64_t(1) << 32)) {
+    cleanup();
+    return fail(SLBM_ECONFIG, std::to_string(total) +
+                                  " slots exceed the 4-byte location table range");
+  }
+  Bases bases{};
+  for (int q = 0; q <= d.q && q < 28; ++q) bases.b[q] = uint32_t(e->base[q]);
+
+  // -- pass 2: index list --
+  SLBM_TRY(dalloc(e, &e->idx, int64_t(d.q - 1) * n));
+  k_fill<<<grid_for(n, 256), 256, 0, s>>>(d_tags, e->cid_map, e->x_flat, n, up, bases, e->idx);
+
+  SLBM_TRY(dalloc(e, &e->ubb_slot, e->n_ubb));
+  SLBM_TRY(dalloc(e, &e->ubb_partner, e->n_ubb));
+  SLBM_TRY(dalloc(e, &e->ubb_corr, e->n_ubb));
+  uint32_t* d_wall_flat = nullptr;
+  double* d_wall_u = nullptr;
+  if (e->n_ubb) {
+    SLBM_CUDA_TRY(cudaMalloc(&d_wall_flat, wall_flat.size() * sizeof(uint32_t)));
+    SLBM_CUDA_TRY(cudaMalloc(&d_wall_u, wall_u.size() * sizeof(double)));
+    SLBM_CUDA_TRY(cudaMemcpyAsync(d_wall_flat, wall_flat.data(),
+                                  wall_flat.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    SLBM_CUDA_TRY(cudaMemcpyAsync(d_wall_u, wall_u.data(), wall_u.size() * sizeof(double),
+                                  cudaMemcpyHostToDevice, s));
+  }
+  for (int q = 1; q < d.q; ++q) {
+    if (!e->n_ubb_q[q]) continue;
+    int64_t cnt = 0;
+    SLBM_TRY(select_if(thrust::counting_iterator<uint32_t>(0), sel_buf, n,
+                       ReadsTag{d_tags, e->x_flat, up, q, kUbb}, &cnt, s));
+    k_ubb_assign<<<grid_for(cnt, 256), 256, 0, s>>>(
+        sel_buf, cnt, q, e->x_flat, n, up, bases, d_wall_flat, d_wall_u,
+        int64_t(wall_flat.size()), e->idx, e->ubb_slot + e->ubb_off[q],
+        e->ubb_partner + e->ubb_off[q], e->ubb_corr + e->ubb_off[q], d_err);
+  }
+
+  SLBM_TRY(dalloc(e, &e->ghost_key, e->n_ghost));
+  e->ghost_key_host.assign(size_t(e->n_ghost), 0);
+  if (e->n_ghost) {
+    int64_t max_g = 0;
+    for (int q = 1; q < d.q; ++q) max_g = std::max(max_g, e->n_ghost_q[q]);
+    uint64_t *k_in = nullptr, *k_out = nullptr;
+    uint32_t* c_out = nullptr;
+    SLBM_CUDA_TRY(cudaMalloc(&k_in, max_g * sizeof(uint64_t)));
+    SLBM_CUDA_TRY(cudaMalloc(&k_out, max_g * sizeof(uint64_t)));
+    SLBM_CUDA_TRY(cudaMalloc(&c_out, max_g * sizeof(uint32_t)));
+    for (int q = 1; q < d.q; ++q) {
+      if (!e->n_ghost_q[q]) continue;
+      int64_t cnt = 0;
+      SLBM_TRY(select_if(thrust::counting_iterator<uint32_t>(0), sel_buf, n,
+                         ReadsTag{d_tags, e->x_flat, up, q, kExchange}, &cnt, s));
+      k_ghost_keys<<<grid_for(cnt, 256), 256, 0, s>>>(sel_buf, cnt, q, e->x_flat, up, k_in);
+      size_t tmp_bytes = 0;
+      SLBM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k_in, k_out, sel_buf,
+                                                    c_out, cnt, 0, 37, s));
+      void* tmp = nullptr;
+      SLBM_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, s));
+      SLBM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k_in, k_out, sel_buf, c_out,
+                                                    cnt, 0, 37, s));
+      SLBM_CUDA_TRY(cudaFreeAsync(tmp, s));
+      uint32_t first = uint32_t(e->base[q] + n + e->n_ubb_q[q]);
+      k_ghost_assign<<<grid_for(cnt, 256), 256, 0, s>>>(c_out, cnt, q, n, first, e->idx);
+      SLBM_CUDA_TRY(cudaMemcpyAsync(e->ghost_key + e->ghost_off[q], k_out,
+                                    cnt * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+    }
+    SLBM_CUDA_TRY(cudaMemcpyAsync(e->ghost_key_host.data(), e->ghost_key,
+                                  e->n_ghost * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    SLBM_CUDA_TRY(cudaStreamSynchronize(s));
+    cudaFree(k_in);
+    cudaFree(k_out);
+    cudaFree(c_out);
+  }
+
+  // -- ownership uniqueness (sparse.py:182-185) --
+  {
+    unsigned int* bits = nullptr;
+    int64_t words = (total + 31) / 32;
+    SLBM_CUDA_TRY(cudaMalloc(&bits, words * sizeof(unsigned int)));
+    SLBM_CUDA_TRY(cudaMemsetAsync(bits, 0, words * sizeof(unsigned int), s));
+    int64_t entries = int64_t(d.q) * n;
+    k_unique<<<grid_for(entries, 256), 256, 0, s>>>(e->idx, n, d.q, uint64_t(total), bits,
+                                                     d_err);
+    SLBM_CUDA_TRY(cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SLBM_CUDA_TRY(cudaStreamSynchronize(s));
+    cudaFree(bits);
+  }
+  if (d_wall_flat) cudaFree(d_wall_flat);
+  if (d_wall_u) cudaFree(d_wall_u);
+  if (h_err & 4) {
+    cleanup();
+    return fail(SLBM_ECONFIG, "UBB tag without a wall velocity entry");
+  }
+  if (h_err & (8 | 16)) {
+    cleanup();
+    return fail(SLBM_ECONFIG, "each slot must belong to exactly one (direction, cell) pair");
+  }
+
+  // -- interior / frame split (sparse.py:80-88) --
+  if (frame_width) {
+    InFrame fr{e->x_flat, g, {1, 1, 1}, true};
+    for (int a = 0; a < 3; ++a) {
+      int32_t w = a < g.dim ? frame_width[a] : 1;
+      fr.w[a] = std::min<int32_t>(w, g.n[a]);
+    }
+    int64_t nf = 0, ni = 0;
+    SLBM_TRY(select_if(thrust::counting_iterator<uint32_t>(0), sel_buf, n, fr, &nf, s));
+    SLBM_TRY(dalloc(e, &e->frame_cids, nf));
+    SLBM_CUDA_TRY(cudaMemcpyAsync(e->frame_cids, sel_buf, nf * sizeof(uint32_t),
+                                  cudaMemcpyDeviceToDevice, s));
+    fr.want = false;
+    SLBM_TRY(select_if(thrust::counting_iterator<uint32_t>(0), sel_buf, n, fr, &ni, s));
+    SLBM_TRY(dalloc(e, &e->interior_cids, ni));
+    SLBM_CUDA_TRY(cudaMemcpyAsync(e->interior_cids, sel_buf, ni * sizeof(uint32_t),
+                                  cudaMemcpyDeviceToDevice, s));
+    e->n_frame = nf;
+    e->n_interior = ni;
+    e->has_split = true;
+  }
+  SLBM_CUDA_TRY(cudaStreamSynchronize(s));
+  cleanup();
+  return SLBM_OK;
+}
+
+}  // namespace slbm

@@ -1,0 +1,79 @@
+// Internal state of one sparse block engine (the object behind SlbmEngine*).
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+
+struct SlbmEngine {
+  int device = 0;
+  int dim = 3, q = 19;
+  int model = SLBM_SRT;
+  double omega = 1.0, lambda_odd = 1.0;
+  int pattern = SLBM_PULL;
+  int parity = SLBM_EVEN;
+  slbm::Geometry geo{};
+  slbm::DirTable dirs{};
+
+  int64_t n_fluid = 0, total_slots = 0, n_ubb = 0, n_ghost = 0;
+  int64_t n_interior = 0, n_frame = 0;
+  bool has_split = false;
+  int64_t base[28] = {0};
+  int64_t n_ubb_q[27] = {0}, n_ghost_q[27] = {0};
+  int64_t ubb_off[28] = {0}, ghost_off[28] = {0};
+
+  // device memory
+  double* pdf = nullptr;   // active buffer
+  double* tmp = nullptr;   // pull: second buffer
+  uint32_t* idx = nullptr;  // (q-1) x n_fluid
+  uint32_t* x_flat = nullptr;  // cid -> padded flat
+  int32_t* cid_map = nullptr;  // padded flat -> cid or -1
+  uint32_t* ubb_slot = nullptr;
+  uint32_t* ubb_partner = nullptr;
+  double* ubb_corr = nullptr;
+  uint64_t* ghost_key = nullptr;  // per q sorted (sigma_key << 32 | pflat)
+  std::vector<uint64_t> ghost_key_host;
+  uint32_t* interior_cids = nullptr;
+  uint32_t* frame_cids = nullptr;
+  unsigned long long* d_bad = nullptr;   // first unstable step (ULLONG_MAX = none)
+  unsigned long long* d_step = nullptr;  // step counter read by the sweeps
+  double* d_scratch = nullptr;           // staging for host transfers
+  size_t scratch_bytes = 0;
+  int64_t device_bytes = 0;
+
+  unsigned long long* h_bad = nullptr;   // pinned copy for polling
+
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+
+  // CUDA graphs of one step pair, keyed by starting state (0/1)
+  cudaGraphExec_t graph[2] = {nullptr, nullptr};
+  int64_t steps_done = 0;
+
+  int ensure_scratch(size_t bytes);
+};
+
+namespace slbm {
+
+// kernels / launchers implemented in kernels.cu
+int launch_step(SlbmEngine* e, int phase);
+int launch_refresh(SlbmEngine* e, int parity);
+int launch_advance(SlbmEngine* e);
+int launch_canonical(SlbmEngine* e, double* dev_out);  // (q, n) at current parity
+int launch_macroscopic(SlbmEngine* e, const double* dev_canon, double* dev_rho, double* dev_u);
+int launch_gather(const double* src, const uint32_t* slots, int64_t n, double* out,
+                  cudaStream_t s);
+int launch_scatter(double* dst, const uint32_t* slots, int64_t n, const double* in,
+                   cudaStream_t s);
+int launch_fill(double* p, int64_t n, double v, cudaStream_t s);
+int launch_equilibrium(SlbmEngine* e, const double* rho, int rho_scalar, const double* u,
+                       int u_scalar, double* dev_out);
+int launch_sum(const double* p, int64_t n, double* dev_out, cudaStream_t s);
+int launch_slot_lookup(SlbmEngine* e, const int64_t* d_qs, const int64_t* d_pflat, int64_t n,
+                       int64_t* d_out, int* d_err);
+
+// builder.cu
+int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
+                const int32_t* frame_width);
+
+}  // namespace slbm

@@ -1,0 +1,208 @@
+"""Cell tags and the padded flag box (input format of the list builder).
+
+Same semantics as the reference (``pkg/src/slbm/flags.py``): a uint8 tag
+per cell on a box padded by one ring cell per side, stored with axes in
+reverse public order (``(z, y, x)`` for public ``(x, y, z)``), plus a
+per-cell wall velocity that only matters where the tag is UBB.  Tag
+values (``flags.py:27-30``) are part of the contract with the CUDA
+builder.
+
+Ring painting (``flags.py:196-249``): axes are padded in array order, so
+for two meeting walls the later-padded axis wins the corner; periodic axes
+copy the wrapped image of the opposite side (including already-painted
+ring cells of earlier axes).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from enum import Enum
+
+import numpy as np
+
+from . import errors
+
+FLUID = 0
+NOSLIP = 1
+UBB = 2
+EXCHANGE = 3
+TAG_NAMES = {FLUID: "fluid", NOSLIP: "noslip", UBB: "ubb", EXCHANGE: "exchange"}
+
+
+class FaceKind(Enum):
+    WALL = "wall"
+    PERIODIC = "periodic"
+    EXCHANGE = "exchange"
+
+
+@dataclass(frozen=True)
+class FaceSpec:
+    kind: FaceKind
+    velocity: tuple[float, ...] | None = None
+
+
+WALL = FaceSpec(FaceKind.WALL)
+PERIODIC = FaceSpec(FaceKind.PERIODIC)
+
+
+def rev_shape(dims) -> tuple[int, ...]:
+    return tuple(int(d) for d in dims)[::-1]
+
+
+def ring_offset(pos, dims) -> tuple[int, ...]:
+    """-1 / 0 / +1 per public axis: below, inside, or above the box."""
+    return tuple(-1 if p < 0 else (1 if p >= d else 0) for p, d in zip(pos, dims))
+
+
+def frame_mask(dims, width) -> np.ndarray:
+    """Cells within ``width`` (per public axis, clamped to the extent) of a
+    box face, as a bool array over ``rev_shape(dims)``
+    (``flags.py:83-108``)."""
+    nd = len(dims)
+    widths = (width,) * nd if isinstance(width, (int, np.integer)) else tuple(int(w) for w in width)
+    if len(widths) != nd:
+        raise errors.make(
+            "ConfigurationError",
+            f"need one frame width per axis, got {len(widths)} for {nd} axes",
+        )
+    if min(widths) < 1:
+        raise errors.make("ConfigurationError", f"frame widths must be >= 1, got {widths}")
+    grids = np.ogrid[tuple(slice(0, int(n)) for n in rev_shape(dims))]
+    mask = np.zeros(rev_shape(dims), dtype=bool)
+    for axis in range(nd):
+        n = int(dims[axis])
+        w = min(widths[axis], n)
+        g = grids[nd - 1 - axis]
+        mask |= (g < w) | (g >= n - w)
+    return mask
+
+
+@dataclass
+class FlagField:
+    dims: tuple[int, ...]
+    tags: np.ndarray  # uint8, rev_shape(dims) + 2 per axis
+    ubb_u: np.ndarray  # float64, tags.shape + (dim,)
+    periodic: tuple[bool, ...]
+
+    @property
+    def ndim(self) -> int:
+        return len(self.dims)
+
+    @property
+    def core(self) -> tuple[slice, ...]:
+        return tuple(slice(1, n + 1) for n in rev_shape(self.dims))
+
+    @property
+    def tags_interior(self) -> np.ndarray:
+        return self.tags[self.core]
+
+    def fluid_count(self) -> int:
+        return int(np.count_nonzero(self.tags_interior == FLUID))
+
+    def cell_count(self) -> int:
+        return int(np.prod(self.dims, dtype=np.int64))
+
+    def porosity(self) -> float:
+        return self.fluid_count() / self.cell_count()
+
+    def _padded_index(self, coord):
+        return tuple(int(coord[a]) + 1 for a in reversed(range(self.ndim)))
+
+    def tag_at(self, coord) -> int:
+        return int(self.tags[self._padded_index(coord)])
+
+    def ubb_at(self, coord) -> np.ndarray:
+        return self.ubb_u[self._padded_index(coord)]
+
+
+def _wall_tag(spec: FaceSpec) -> int:
+    if spec.velocity is not None and any(float(v) != 0.0 for v in spec.velocity):
+        return UBB
+    return NOSLIP
+
+
+def _check_faces(dims, faces):
+    nd = len(dims)
+    if len(faces) != nd:
+        raise errors.make(
+            "ConfigurationError", f"need one face pair per axis, got {len(faces)} for {nd} axes"
+        )
+    for axis, (lo, hi) in enumerate(faces):
+        for spec in (lo, hi):
+            if spec.kind is FaceKind.EXCHANGE:
+                raise errors.make("ConfigurationError", "exchange faces only arise from partitioning")
+            if spec.velocity is not None:
+                if spec.kind is not FaceKind.WALL:
+                    raise errors.make("ConfigurationError", "velocity is only valid on wall faces")
+                if len(spec.velocity) != nd:
+                    raise errors.make(
+                        "ConfigurationError",
+                        f"wall velocity needs {nd} components, got {len(spec.velocity)}",
+                    )
+        if (lo.kind is FaceKind.PERIODIC) ^ (hi.kind is FaceKind.PERIODIC):
+            raise errors.make(
+                "ConfigurationError", f"axis {axis}: periodic must be set on both sides or neither"
+            )
+
+
+def make_flags(dims, faces, solid: np.ndarray | None = None) -> FlagField:
+    """Padded tag box for a domain with the given per-axis face pairs
+    (``flags.py:196-249``)."""
+    dims = tuple(int(d) for d in dims)
+    nd = len(dims)
+    if nd not in (2, 3):
+        raise errors.make("ConfigurationError", f"dims must have 2 or 3 axes, got {nd}")
+    if min(dims) < 1:
+        raise errors.make("ConfigurationError", f"all extents must be positive, got {dims}")
+    _check_faces(dims, faces)
+    shape = rev_shape(dims)
+    if solid is not None and tuple(solid.shape) != shape:
+        raise errors.make("ConfigurationError", f"solid mask shape {solid.shape} != {shape}")
+
+    padded = tuple(n + 2 for n in shape)
+    tags = np.zeros(padded, dtype=np.uint8)
+    moving = any(_wall_tag(s) == UBB for pair in faces for s in pair)
+    if moving:
+        vel = np.zeros(padded + (nd,), dtype=np.float64)
+    else:
+        # no moving wall: a read-only zero view instead of 24 B/cell of zeros
+        vel = np.broadcast_to(np.zeros((), dtype=np.float64), padded + (nd,))
+    inner = tuple(slice(1, n + 1) for n in shape)
+    if solid is not None:
+        tags[inner][np.asarray(solid, dtype=bool)] = NOSLIP
+
+    # grow the painted region one array axis at a time (z, then y, then x);
+    # `done` tracks the extent already valid on every axis
+    lo_idx = [1] * nd
+    hi_idx = [n + 1 for n in shape]
+    for arr_axis in range(nd):
+        axis = nd - 1 - arr_axis
+        lo, hi = faces[axis]
+        region = [slice(lo_idx[a], hi_idx[a]) for a in range(nd)]
+        n = shape[arr_axis]
+        dst_lo = list(region)
+        dst_hi = list(region)
+        dst_lo[arr_axis] = slice(0, 1)
+        dst_hi[arr_axis] = slice(n + 1, n + 2)
+        if lo.kind is FaceKind.PERIODIC:
+            src_lo = list(region)
+            src_hi = list(region)
+            src_lo[arr_axis] = slice(n, n + 1)
+            src_hi[arr_axis] = slice(1, 2)
+            tags[tuple(dst_lo)] = tags[tuple(src_lo)]
+            tags[tuple(dst_hi)] = tags[tuple(src_hi)]
+            if moving:
+                vel[tuple(dst_lo)] = vel[tuple(src_lo)]
+                vel[tuple(dst_hi)] = vel[tuple(src_hi)]
+        else:
+            tags[tuple(dst_lo)] = _wall_tag(lo)
+            tags[tuple(dst_hi)] = _wall_tag(hi)
+            if moving:
+                vel[tuple(dst_lo)] = 0.0 if lo.velocity is None else np.asarray(lo.velocity, np.float64)
+                vel[tuple(dst_hi)] = 0.0 if hi.velocity is None else np.asarray(hi.velocity, np.float64)
+        lo_idx[arr_axis] = 0
+        hi_idx[arr_axis] = n + 2
+    if moving:
+        vel[tags != UBB] = 0.0
+    periodic = tuple(faces[a][0].kind is FaceKind.PERIODIC for a in range(nd))
+    return FlagField(dims=dims, tags=tags, ubb_u=vel, periodic=periodic)
