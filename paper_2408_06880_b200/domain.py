@@ -1,0 +1,528 @@
+"""Block decomposition and the time-step drivers on the GPU.
+
+``Domain`` mirrors the reference's (``pkg/src/slbm/domain.py``): uniform
+blocks cut from one padded global flag box, all-solid blocks dropped,
+remote fluid in each block's ring retagged EXCHANGE (only on axes that do
+not wrap inside the block), z-major block ids, edges over the stencil's
+offsets, and the sequential / overlapped drivers of
+``exchange.py:330-374``.  Every block engine is a CUDA
+:class:`~paper_2408_06880_b200.engine.SparseEngine`; halo traffic is the
+device exchange program of :class:`~paper_2408_06880_b200.halo.DeviceHalo`
+(no host mailbox).
+
+``DistributedDomain`` is the one-process-per-GPU version: every rank
+derives the same partition and edge list, builds engines only for the
+blocks assigned to it, and exchanges cross-rank edges with NCCL send/recv
+(one message per peer per phase) on a comm stream that overlaps the
+interior sweep.
+
+Only the sparse layout is built in this tier (policy "sparse"); dense and
+hybrid blocks are the next row.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import errors
+from .collision import Parity
+from .counters import Counters
+from .engine import SparseEngine, default_device
+from .halo import DeviceHalo, EdgePlan, NcclComm, Phase, phase_for
+from .tags import EXCHANGE, FLUID, NOSLIP, FlagField, rev_shape
+
+POLICIES = ("sparse", "dense", "hybrid")
+DEFAULT_PHI_S = 0.8
+
+
+@dataclass
+class Block:
+    bid: int
+    grid_pos: tuple[int, ...]
+    origin: tuple[int, ...]
+    flags: FlagField
+    n_fluid: int
+    kind: str = "sparse"
+    engine: object = None
+    rank: int = 0
+    neighbors: dict = field(default_factory=dict)
+
+    @property
+    def porosity(self) -> float:
+        return self.n_fluid / self.flags.cell_count()
+
+
+# ---------------------------------------------------------------- partition helpers
+
+
+def grid_positions(grid):
+    """z-major enumeration of block grid positions (domain.py:359-367)."""
+    nd = len(grid)
+    for flat in range(int(np.prod(grid))):
+        pos, rem = [], flat
+        for a in range(nd):
+            pos.append(rem % grid[a])
+            rem //= grid[a]
+        yield tuple(pos)
+
+
+def grid_linear(pos, grid) -> int:
+    out = 0
+    for a in reversed(range(len(grid))):
+        out = out * grid[a] + pos[a]
+    return out
+
+
+def pad_to_multiple(gf: FlagField, block_size) -> FlagField:
+    """NOSLIP filler up to a block multiple on walled axes (domain.py:407-429)."""
+    nd = len(gf.dims)
+    pads = []
+    for a in range(nd):
+        rem = gf.dims[a] % block_size[a]
+        pad = 0 if rem == 0 else block_size[a] - rem
+        if pad and gf.periodic[a]:
+            raise errors.make(
+                "ConfigurationError",
+                f"axis {a} extent {gf.dims[a]} not divisible by block size {block_size[a]} and "
+                "periodic; padding would break the wrap",
+            )
+        pads.append(pad)
+    if not any(pads):
+        return gf
+    new_dims = tuple(gf.dims[a] + pads[a] for a in range(nd))
+    tags = np.full(tuple(n + 2 for n in rev_shape(new_dims)), NOSLIP, dtype=np.uint8)
+    ubb = np.zeros(tags.shape + (nd,))
+    region = tuple(slice(0, s) for s in gf.tags.shape)
+    tags[region] = gf.tags
+    ubb[region] = gf.ubb_u
+    return FlagField(dims=new_dims, tags=tags, ubb_u=ubb, periodic=gf.periodic)
+
+
+def slice_block(gf: FlagField, origin, size, block_periodic) -> FlagField:
+    nd = len(size)
+    sel = tuple(slice(origin[a], origin[a] + size[a] + 2) for a in reversed(range(nd)))
+    tags = gf.tags[sel].copy()
+    ubb = gf.ubb_u[sel]
+    ubb = ubb.copy() if ubb.flags.writeable else ubb
+    # halo fluid -> EXCHANGE on axes that leave the block (domain.py:390-404)
+    ring = np.zeros(tags.shape, dtype=bool)
+    for arr_axis in range(nd):
+        if block_periodic[nd - 1 - arr_axis]:
+            continue
+        lo = [slice(None)] * nd
+        lo[arr_axis] = 0
+        ring[tuple(lo)] = True
+        lo[arr_axis] = tags.shape[arr_axis] - 1
+        ring[tuple(lo)] = True
+    tags[ring & (tags == FLUID)] = EXCHANGE
+    return FlagField(dims=tuple(size), tags=tags, ubb_u=ubb, periodic=tuple(block_periodic))
+
+
+# ---------------------------------------------------------------- load balancing
+
+
+def hilbert_key(coords, bits: int) -> int:
+    """Position on the Hilbert curve of a 2**bits box (Skilling transpose)."""
+    x = [int(c) for c in coords]
+    n = len(x)
+    top = 1 << (bits - 1)
+    q = top
+    while q > 1:
+        p = q - 1
+        for i in range(n):
+            if x[i] & q:
+                x[0] ^= p
+            else:
+                t = (x[0] ^ x[i]) & p
+                x[0] ^= t
+                x[i] ^= t
+        q >>= 1
+    for i in range(1, n):
+        x[i] ^= x[i - 1]
+    t = 0
+    q = top
+    while q > 1:
+        if x[n - 1] & q:
+            t ^= q - 1
+        q >>= 1
+    x = [v ^ t for v in x]
+    h = 0
+    for b in range(bits - 1, -1, -1):
+        for v in x:
+            h = (h << 1) | ((v >> b) & 1)
+    return h
+
+
+def morton_key(coords, bits: int) -> int:
+    h = 0
+    for b in range(bits - 1, -1, -1):
+        for c in coords:
+            h = (h << 1) | ((int(c) >> b) & 1)
+    return h
+
+
+def curve_key(pos, grid) -> int:
+    """Hilbert over the non-trivial axes when they form an equal power-of-two
+    box, Morton otherwise (domain.py:517-530)."""
+    act = [a for a in range(len(grid)) if grid[a] > 1]
+    if not act:
+        return 0
+    coords = [pos[a] for a in act]
+    ext = [grid[a] for a in act]
+    if len(coords) == 1:
+        return coords[0]
+    if len(set(ext)) == 1 and ext[0] & (ext[0] - 1) == 0:
+        return hilbert_key(coords, ext[0].bit_length() - 1)
+    return morton_key(coords, max(max(e - 1 for e in ext).bit_length(), 1))
+
+
+def greedy_segments(loads, n_workers: int) -> list[int]:
+    """Contiguous cuts against the running per-worker target
+    (domain.py:446-465)."""
+    seats = []
+    remaining = float(sum(loads))
+    left = n_workers
+    target = remaining / left
+    w, acc = 0, 0.0
+    for load in loads:
+        if w < n_workers - 1 and acc > 0 and acc + load / 2.0 > target:
+            w += 1
+            left -= 1
+            target = remaining / left if left else 0.0
+            acc = 0.0
+        seats.append(w)
+        acc += load
+        remaining -= load
+    return seats
+
+
+# ---------------------------------------------------------------- domain
+
+
+class Domain:
+    """Whole-geometry solver on one GPU (all blocks in this process)."""
+
+    def __init__(self, global_flags, block_size, stencil, params, pattern: str = "pull",
+                 policy: str = "sparse", phi_s: float = DEFAULT_PHI_S, frame_width=None,
+                 device: int | None = None, check: str = "step", _rank: int = 0, _world: int = 1,
+                 _assignment=None, _comm=None):
+        if policy not in POLICIES:
+            raise errors.make("ConfigurationError", f"unknown layout policy {policy!r}")
+        if policy != "sparse":
+            raise errors.make("ConfigurationError",
+                              f"layout policy {policy!r}: dense blocks are not built on the GPU "
+                              "in this tier (sparse only)")
+        self.stencil, self.params, self.pattern = stencil, params, pattern
+        self.policy, self.phi_s, self.frame_width = policy, phi_s, frame_width
+        self.device = default_device() if device is None else int(device)
+        self.check = check
+        self.rank, self.world = _rank, _world
+        dim = stencil.dim
+        if isinstance(block_size, (int, np.integer)):
+            block_size = (int(block_size),) * dim
+        if len(block_size) != dim or min(block_size) < 1:
+            raise errors.make("ConfigurationError", f"bad block size {block_size}")
+        self.block_size = tuple(int(s) for s in block_size)
+        gf = pad_to_multiple(global_flags, self.block_size)
+        self.global_flags = gf
+        self.global_dims = gf.dims
+        self.periodic = gf.periodic
+        self.grid = tuple(self.global_dims[a] // self.block_size[a] for a in range(dim))
+        self._block_periodic = tuple(gf.periodic[a] and self.grid[a] == 1 for a in range(dim))
+
+        self.blocks: dict[int, Block] = {}
+        for pos in grid_positions(self.grid):
+            bid = grid_linear(pos, self.grid)
+            origin = tuple(pos[a] * self.block_size[a] for a in range(dim))
+            fl = slice_block(gf, origin, self.block_size, self._block_periodic)
+            nf = fl.fluid_count()
+            if nf == 0:
+                continue
+            self.blocks[bid] = Block(bid, pos, origin, fl, nf)
+        if not self.blocks:
+            raise errors.make("ConfigurationError", "geometry has no fluid cells")
+
+        self.assignment = dict(_assignment) if _assignment else {b: 0 for b in self.blocks}
+        for bid, blk in self.blocks.items():
+            blk.rank = self.assignment.get(bid, 0)
+            if blk.rank == self.rank:
+                blk.engine = SparseEngine(blk.flags, stencil, params, pattern=pattern,
+                                          frame_width=frame_width, device=self.device,
+                                          check="deferred")
+        engines = self.local_engines()
+        self._stream = engines[0].stream() if engines else 0
+        for e in engines[1:]:
+            e.set_stream(self._stream)
+
+        self._edges = self._adjacency()
+        self.edge_plans: list[EdgePlan] = []
+        for a, b, sigma in self._edges:
+            ba, bb = self.blocks[a], self.blocks[b]
+            if ba.rank != self.rank and bb.rank != self.rank:
+                continue
+            self.edge_plans.append(EdgePlan(a, b, sigma, stencil, ba.flags, bb.flags, pattern,
+                                            ba.engine, bb.engine))
+        self._comm = _comm
+        self._halo = self._build_halo()
+        self.overlap_samples: list[tuple[float, float]] = []
+        self.steps_done = 0
+
+    # -- construction ------------------------------------------------------------
+
+    def _adjacency(self):
+        dim = self.stencil.dim
+        offsets = sorted({tuple(0 if self._block_periodic[a] else int(self.stencil.c[k][a])
+                                for a in range(dim)) for k in range(1, self.stencil.q)}
+                         - {(0,) * dim})
+        edges = []
+        for bid, blk in sorted(self.blocks.items()):
+            for sigma in offsets:
+                npos = []
+                for a in range(dim):
+                    p = blk.grid_pos[a] + sigma[a]
+                    if self.periodic[a]:
+                        p %= self.grid[a]
+                    elif not 0 <= p < self.grid[a]:
+                        break
+                    npos.append(p)
+                else:
+                    nbid = grid_linear(tuple(npos), self.grid)
+                    if nbid in self.blocks:
+                        blk.neighbors[sigma] = nbid
+                        edges.append((bid, nbid, sigma))
+        return edges
+
+    def _build_halo(self):
+        halo = DeviceHalo(self.device)
+        for plan in self.edge_plans:
+            src, dst = self.blocks[plan.src_bid], self.blocks[plan.dst_bid]
+            for ph, pp in plan.phases.items():
+                if src.rank == self.rank and dst.rank == self.rank:
+                    halo.add_local(ph, src.engine, dst.engine, pp)
+                elif src.rank == self.rank:
+                    halo.add_send(ph, src.engine, dst.rank, pp)
+                else:
+                    halo.add_recv(ph, dst.engine, src.rank, pp)
+        halo.commit(self._comm.handle if self._comm is not None else None)
+        return halo
+
+    # -- access -----------------------------------------------------------------
+
+    def local_blocks(self):
+        return [b for _, b in sorted(self.blocks.items()) if b.rank == self.rank]
+
+    def local_engines(self):
+        return [b.engine for b in self.local_blocks()]
+
+    def local_fluid(self) -> int:
+        return sum(b.n_fluid for b in self.local_blocks())
+
+    def total_fluid(self) -> int:
+        return sum(b.n_fluid for b in self.blocks.values())
+
+    @property
+    def parity(self):
+        return self.local_engines()[0].parity
+
+    def stream(self) -> int:
+        return self._stream
+
+    # -- state init ---------------------------------------------------------------
+
+    def init_equilibrium(self, rho: float = 1.0, u=None) -> None:
+        for e in self.local_engines():
+            e.init_equilibrium(rho, u)
+
+    def init_random(self, seed: int, amplitude: float = 0.005) -> None:
+        """domain.py:191-206: near-equilibrium state drawn over the global
+        grid (decomposition-invariant); the equilibrium is evaluated on the
+        device with the reference's operation order."""
+        rng = np.random.default_rng(seed)
+        shape = rev_shape(self.global_dims)
+        rho_g = 1.0 + amplitude * rng.standard_normal(shape)
+        u_g = amplitude * rng.standard_normal((self.stencil.dim,) + shape)
+        for blk in self.local_blocks():
+            coords = blk.engine.fluid_coords + np.asarray(blk.origin, dtype=np.int64)
+            flat = np.ravel_multi_index(coords[:, ::-1].T, shape)
+            blk.engine.init_equilibrium(rho_g.reshape(-1)[flat],
+                                        u_g.reshape(self.stencil.dim, -1)[:, flat])
+
+    # -- stepping -----------------------------------------------------------------
+
+    def _count_exchange(self, phase: Phase):
+        for plan in self.edge_plans:
+            src = self.blocks[plan.src_bid]
+            if src.rank == self.rank:
+                src.engine.counters.values_exchanged += plan.phases[phase].n_wire
+                src.engine.counters.messages += 1
+
+    def _sweep(self, phase: str):
+        for e in self.local_engines():
+            e.step(phase)
+
+    def step_sequential(self) -> None:
+        """exchange.py:330-346 on the device: exchange, then whole-block sweeps."""
+        phase = phase_for(self.pattern, self.parity)
+        self._halo.start(phase, self._stream)
+        self._halo.wait(self._stream)
+        self._count_exchange(phase)
+        for e in self.local_engines():
+            e.refresh_boundary(e.parity)
+        self._sweep("all")
+        for e in self.local_engines():
+            e.finish_step()
+
+    def step_overlapped(self) -> None:
+        """exchange.py:349-374: pack/send/recv/unpack on the comm stream while
+        the interior sweep runs on the compute stream; frame after the join."""
+        phase = phase_for(self.pattern, self.parity)
+        self._halo.start(phase, self._stream)
+        self._count_exchange(phase)
+        for e in self.local_engines():
+            e.refresh_boundary(e.parity)
+        self._sweep("interior")
+        self._halo.wait(self._stream)
+        self._sweep("frame")
+        for e in self.local_engines():
+            e.finish_step()
+
+    def run(self, steps: int, driver: str = "sequential") -> None:
+        fn = self._driver(driver)
+        for _ in range(int(steps)):
+            fn()
+            if self.check == "step":
+                self._poll_or_raise()
+            self.steps_done += 1
+
+    def _driver(self, name: str):
+        if name == "sequential":
+            return self.step_sequential
+        if name == "overlapped":
+            if self.frame_width is None:
+                raise errors.make("ConfigurationError", "overlapped driver needs frame_width at construction")
+            return self.step_overlapped
+        raise errors.make("ConfigurationError", f"unknown driver {name!r}")
+
+    def _poll_or_raise(self):
+        try:
+            for e in self.local_engines():
+                e.poll()
+        except errors.error_class("NumericalInstabilityError") as exc:
+            raise errors.make("NumericalInstabilityError", f"unstable at step {self.steps_done}: {exc}") from exc
+
+    def poll(self) -> None:
+        self._poll_or_raise()
+
+    def synchronize(self) -> None:
+        for e in self.local_engines():
+            e.synchronize()
+
+    # -- observation ----------------------------------------------------------------
+
+    def fluid_mask(self) -> np.ndarray:
+        return self.global_flags.tags_interior == FLUID
+
+    def gather_macroscopics(self):
+        shape = rev_shape(self.global_dims)
+        rho = np.zeros(shape)
+        u = np.zeros(shape + (self.stencil.dim,))
+        for blk in self.local_blocks():
+            r, v = blk.engine.macroscopic_fields()
+            sel = tuple(slice(blk.origin[a], blk.origin[a] + self.block_size[a])
+                        for a in reversed(range(self.stencil.dim)))
+            rho[sel] = r
+            u[sel] = v
+        return rho, u
+
+    def gather_canonical(self) -> np.ndarray:
+        shape = rev_shape(self.global_dims)
+        out = np.zeros((self.stencil.q,) + shape)
+        flat_out = out.reshape(self.stencil.q, -1)
+        for blk in self.local_blocks():
+            coords = blk.engine.fluid_coords + np.asarray(blk.origin, dtype=np.int64)
+            flat = np.ravel_multi_index(coords[:, ::-1].T, shape)
+            flat_out[:, flat] = blk.engine.canonical_state()
+        return out
+
+    def counters(self) -> Counters:
+        total = Counters()
+        for e in self.local_engines():
+            total.add(e.counters)
+        return total
+
+    # -- balancing --------------------------------------------------------------------
+
+    def workload(self, bid: int) -> int:
+        """model.workload_sparse: Q x fluid cells"""
+        return self.stencil.q * self.blocks[bid].n_fluid
+
+    def curve_order(self) -> list[int]:
+        return sorted(self.blocks, key=lambda b: (curve_key(self.blocks[b].grid_pos, self.grid), b))
+
+    def balance(self, n_workers: int) -> dict[int, int]:
+        if n_workers < 1:
+            raise errors.make("ConfigurationError", "need at least one worker")
+        order = self.curve_order()
+        seats = greedy_segments([self.workload(b) for b in order], n_workers)
+        return {b: int(w) for b, w in zip(order, seats)}
+
+
+class DistributedDomain(Domain):
+    """One process per GPU.  Blocks go to ranks by ``assignment`` (default:
+    the reference's Hilbert/greedy ``balance``); cross-rank edges use NCCL
+    through the library's own communicator."""
+
+    def __init__(self, global_flags, block_size, stencil, params, pattern="aa", frame_width=1,
+                 rank: int | None = None, world: int | None = None, device: int | None = None,
+                 assignment=None, check: str = "deferred", comm=None):
+        import torch.distributed as dist
+
+        rank = dist.get_rank() if rank is None else rank
+        world = dist.get_world_size() if world is None else world
+        if assignment is None:
+            probe = Domain.__new__(Domain)
+            assignment = _balance_without_engines(global_flags, block_size, stencil, world)
+            del probe
+        if comm is None and world > 1:
+            comm = NcclComm(rank, world, default_device() if device is None else device)
+        super().__init__(global_flags, block_size, stencil, params, pattern=pattern,
+                         frame_width=frame_width, device=device, check=check, _rank=rank,
+                         _world=world, _assignment=assignment, _comm=comm)
+
+    @classmethod
+    def weak_scaling_bed(cls, block_edge, world, rank, stencil, params, porosity, diameter, seed,
+                         device=None):
+        """world blocks of ``block_edge`` along x, fully periodic
+        overlapping-sphere bed over the whole box, block i on rank i."""
+        from .geometry import packed_bed_flags
+
+        bx, by, bz = block_edge
+        dims = (bx * world, by, bz)
+        fl = packed_bed_flags(dims, porosity, diameter, seed, periodic=True,
+                              device=default_device() if device is None else device)
+        assignment = {i: i for i in range(world)}
+        return cls(fl, (bx, by, bz), stencil, params, pattern="aa", frame_width=1, rank=rank,
+                   world=world, device=device, assignment=assignment)
+
+    def run(self, steps: int, driver: str = "overlapped") -> None:
+        super().run(steps, driver)
+
+
+def _balance_without_engines(gf, block_size, stencil, n_workers):
+    dim = stencil.dim
+    if isinstance(block_size, (int, np.integer)):
+        block_size = (int(block_size),) * dim
+    gf = pad_to_multiple(gf, tuple(block_size))
+    grid = tuple(gf.dims[a] // block_size[a] for a in range(dim))
+    loads = {}
+    for pos in grid_positions(grid):
+        sel = tuple(slice(1 + pos[a] * block_size[a], 1 + (pos[a] + 1) * block_size[a])
+                    for a in reversed(range(dim)))
+        nf = int(np.count_nonzero(gf.tags[sel] == FLUID))
+        if nf:
+            loads[grid_linear(pos, grid)] = (pos, nf)
+    order = sorted(loads, key=lambda b: (curve_key(loads[b][0], grid), b))
+    seats = greedy_segments([stencil.q * loads[b][1] for b in order], n_workers)
+    return {b: int(w) for b, w in zip(order, seats)}
