@@ -202,6 +202,10 @@ int slbm_nccl_comm_destroy(void* comm);
 int slbm_voxelize_spheres(const int32_t* dims, const double* centers, int64_t n,
                           double diameter, int device, uint8_t* solid);
 
+/* kernel-variant knobs for tuning experiments: knob 0 = index-list sweep
+ * variant, knob 1 = cell-local sweep variant (0 = default)                 */
+int slbm_set_tuning(int knob, int value);
+
 const char* slbm_last_error(void);
 const char* slbm_version(void);
 

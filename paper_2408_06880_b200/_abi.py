@@ -90,6 +90,7 @@ SIGNATURES = {
     "slbm_nccl_get_unique_id": [vp],
     "slbm_nccl_comm_destroy": [vp],
     "slbm_voxelize_spheres": [c_i32p, c_dp, C.c_int64, C.c_double, C.c_int, c_u8p],
+    "slbm_set_tuning": [C.c_int, C.c_int],
     "slbm_last_error": [],
     "slbm_version": [],
 }

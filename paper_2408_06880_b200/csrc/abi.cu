@@ -88,7 +88,7 @@ int check_model(int q, int model) {
   if (model == SLBM_SRT || model == SLBM_TRT) return SLBM_OK;
   if (model == SLBM_CUMULANT) {
     if (q != 27) return fail(SLBM_ECONFIG, "cumulant collision needs the d3q27 stencil");
-    return SLBM_OK;
+    return fail(SLBM_ECONFIG, "cumulant collision is not available in this build yet");
   }
   return fail(SLBM_ECONFIG, "unknown collision model code " + std::to_string(model));
 }
@@ -120,6 +120,8 @@ extern "C" {
 
 const char* slbm_last_error(void) { return last_error(); }
 const char* slbm_version(void) { return "slbm_b200 0.1 sm_100a"; }
+
+int slbm_set_tuning(int knob, int value) { return set_tuning(knob, value); }
 
 int slbm_engine_create(const uint8_t* tags_pad, const double* ubb_u_pad, int dim,
                        const int32_t* dims, const uint8_t* periodic, int q, int model,

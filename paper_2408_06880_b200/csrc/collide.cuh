@@ -28,8 +28,10 @@ struct Moments {
   bool bad;
 };
 
-template <class L>
-__device__ __forceinline__ Moments<L> moments(const double (&t)[L::Q]) {
+// `t` is anything indexable by direction: a register array, or a view onto
+// the shared-memory staging buffer of the asynchronous gather kernel.
+template <class L, class TV>
+__device__ __forceinline__ Moments<L> moments(const TV& t) {
   Moments<L> m;
   double rho = t[0] + t[1];
   sfor<2, L::Q>([&](auto q) { rho = rho + t[q]; });
@@ -79,9 +81,8 @@ __device__ __forceinline__ double feq(const Moments<L>& m) {
 }
 
 // returns true when the cell is unstable (the values are still produced)
-template <class L, int MODEL, class Sink>
-__device__ __forceinline__ bool collide(const double (&t)[L::Q], double omega, double lam,
-                                        Sink&& sink) {
+template <class L, int MODEL, class TV, class Sink>
+__device__ __forceinline__ bool collide(const TV& t, double omega, double lam, Sink&& sink) {
   if constexpr (MODEL == SLBM_CUMULANT) {
     return cumulant_collide<L>(t, omega, sink);
   } else {

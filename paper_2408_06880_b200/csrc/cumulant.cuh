@@ -7,9 +7,8 @@
 
 namespace slbm {
 
-template <class L, class Sink>
-__device__ __forceinline__ bool cumulant_collide(const double (&t)[L::Q], double omega,
-                                                 Sink&& sink) {
+template <class L, class TV, class Sink>
+__device__ __forceinline__ bool cumulant_collide(const TV& t, double omega, Sink&& sink) {
   sfor<0, L::Q>([&](auto q) { sink(q, t[q]); });
   return true;
 }

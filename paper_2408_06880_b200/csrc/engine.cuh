@@ -72,6 +72,8 @@ int launch_sum(const double* p, int64_t n, double* dev_out, cudaStream_t s);
 int launch_slot_lookup(SlbmEngine* e, const int64_t* d_qs, const int64_t* d_pflat, int64_t n,
                        int64_t* d_out, int* d_err);
 
+int set_tuning(int knob, int value);
+
 // builder.cu
 int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
                 const int32_t* frame_width);

@@ -310,6 +310,7 @@ int slbm_halo_local(SlbmHalo* h, int phase) {
                                                        p.d_lds, p.n_local);
     SLBM_CUDA_TRY(cudaGetLastError());
   }
+  SLBM_CUDA_TRY(cudaEventRecord(h->ev_done, h->comm));
   return SLBM_OK;
 }
 

@@ -16,6 +16,7 @@
 //              gather as k_aa_even, dst[base[r] + c] = out_r; 376 B/cell
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <climits>
 
 #include "collide.cuh"
@@ -44,26 +45,168 @@ __device__ __forceinline__ void flag_bad(const SweepArgs& a) {
   atomicMin(a.bad, *a.step);
 }
 
-template <class L, int MODEL>
-__global__ void __launch_bounds__(kBlock) k_aa_even(const SweepArgs a) {
+// idx loads: the first read keeps the row in L1 (evict_last) so the RELOAD
+// variant can re-read the slot right before its store instead of holding
+// all Q-1 slot ids in registers through the collision.
+__device__ __forceinline__ uint32_t ld_idx_keep(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::evict_last.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_idx_again(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::evict_first.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+// tuning knobs (slbm_set_tuning): even-sweep variant
+int g_even_variant = 0;
+int g_odd_variant = 0;
+
+template <class L, int MODEL, int MINB, bool RELOAD>
+__global__ void __launch_bounds__(kBlock, MINB) k_aa_even(const SweepArgs a) {
   const uint32_t i = blockIdx.x * kBlock + threadIdx.x;
   if (i >= a.n_cells) return;
   const uint32_t c = a.cids ? a.cids[i] : i;
   uint32_t s[L::Q];
   double t[L::Q];
   s[0] = c;
-  sfor<1, L::Q>([&](auto q) { s[q] = __ldcs(a.idx + size_t(q - 1) * a.n_fluid + c); });
+  if constexpr (RELOAD) {
+    sfor<1, L::Q>([&](auto q) { s[q] = ld_idx_keep(a.idx + size_t(q - 1) * a.n_fluid + c); });
+  } else {
+    sfor<1, L::Q>([&](auto q) { s[q] = __ldcs(a.idx + size_t(q - 1) * a.n_fluid + c); });
+  }
   sfor<0, L::Q>([&](auto q) { t[q] = a.pdf[s[q]]; });
   double* pdf = a.pdf;
   const bool bad = collide<L, MODEL>(t, a.omega, a.lam, [&](auto q, double v) {
+    constexpr int qb = L::INV[decltype(q)::value];
+    if constexpr (RELOAD && qb != 0) {
+      pdf[ld_idx_again(a.idx + size_t(qb - 1) * a.n_fluid + c)] = v;
+    } else {
+      pdf[s[qb]] = v;
+    }
+  });
+  if (bad) flag_bad(a);
+}
+
+// ---- asynchronous-gather variant of the index-list sweep -------------------
+// The register-resident kernel above is latency bound (ncu r01: long
+// scoreboard 9 of 14 cycles/issue at 25% occupancy, 126 registers for 19
+// PDFs + 18 slot ids).  Here each thread gathers its 19 PDFs straight into
+// shared memory with cp.async (LDGSTS: no destination registers), so the
+// collision can run at 4 CTAs/SM with 2x the bytes in flight; values are
+// read back from shared memory as the collision consumes them.
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem_src));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+struct SmemColumn {
+  const double* p;  // this thread's column: p[q * kBlock]
+  __device__ __forceinline__ double operator[](int q) const { return p[q * kBlock]; }
+};
+
+template <class L, int MODEL, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) k_aa_even_async(const SweepArgs a) {
+  extern __shared__ double stage[];  // [Q][kBlock]
+  const uint32_t i = blockIdx.x * kBlock + threadIdx.x;
+  if (i >= a.n_cells) return;
+  const uint32_t c = a.cids ? a.cids[i] : i;
+  uint32_t s[L::Q];
+  s[0] = c;
+  sfor<1, L::Q>([&](auto q) { s[q] = __ldcs(a.idx + size_t(q - 1) * a.n_fluid + c); });
+  double* col = stage + threadIdx.x;
+  sfor<0, L::Q>([&](auto q) { cp_async8(col + q * kBlock, a.pdf + s[q]); });
+  cp_async_wait_all();
+  double* pdf = a.pdf;
+  const bool bad = collide<L, MODEL>(SmemColumn{col}, a.omega, a.lam, [&](auto q, double v) {
     constexpr int qb = L::INV[decltype(q)::value];
     pdf[s[qb]] = v;
   });
   if (bad) flag_bad(a);
 }
 
-template <class L, int MODEL>
-__global__ void __launch_bounds__(kBlock) k_aa_odd(const SweepArgs a) {
+// ---- persistent variant with the index list prefetched one cell ahead ------
+// Each thread walks cells i, i + stride, ...; while it gathers and collides
+// cell k, the Q-1 slot ids of cell k+1 are already travelling into its own
+// shared-memory column (cp.async, double buffered), so the idx -> pdf
+// dependent DRAM round trip is paid once per thread, not once per cell.
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gmem_src) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem_src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <class L, int MODEL, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) k_aa_even_pf(const SweepArgs a) {
+  extern __shared__ uint32_t pf_raw[];  // [2][Q-1][kBlock]
+  auto pf = reinterpret_cast<uint32_t(*)[L::Q - 1][kBlock]>(pf_raw);
+  const uint32_t stride = gridDim.x * kBlock;
+  uint32_t i = blockIdx.x * kBlock + threadIdx.x;
+  auto prefetch = [&](uint32_t cell, int buf) {
+    const uint32_t c = a.cids ? a.cids[cell] : cell;
+    sfor<1, L::Q>([&](auto q) {
+      cp_async4(&pf[buf][q - 1][threadIdx.x], a.idx + size_t(q - 1) * a.n_fluid + c);
+    });
+  };
+  if (i < a.n_cells) prefetch(i, 0);
+  cp_async_commit();
+  int buf = 0;
+  bool bad = false;
+  double* pdf = a.pdf;
+  for (; i < a.n_cells; i += stride) {
+    const uint32_t nxt = i + stride;
+    if (nxt < a.n_cells) prefetch(nxt, buf ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    const uint32_t c = a.cids ? a.cids[i] : i;
+    uint32_t s[L::Q];
+    double t[L::Q];
+    s[0] = c;
+    sfor<1, L::Q>([&](auto q) { s[q] = pf[buf][q - 1][threadIdx.x]; });
+    sfor<0, L::Q>([&](auto q) { t[q] = pdf[s[q]]; });
+    bad |= collide<L, MODEL>(t, a.omega, a.lam, [&](auto q, double v) {
+      constexpr int qb = L::INV[decltype(q)::value];
+      pdf[s[qb]] = v;
+    });
+    buf ^= 1;
+  }
+  cp_async_wait<0>();
+  if (bad) flag_bad(a);
+}
+
+// ---- memory-pattern probes (tuning only; they do NOT compute LBM) ----------
+// MODE 0: index-list gather + scatter back through the same slots, no math
+// MODE 1: index-list gather, coalesced writes to the cell's own groups
+template <class L, int MODE>
+__global__ void __launch_bounds__(kBlock) k_probe(const SweepArgs a) {
+  const uint32_t i = blockIdx.x * kBlock + threadIdx.x;
+  if (i >= a.n_cells) return;
+  const uint32_t c = i;
+  uint32_t s[L::Q];
+  double t[L::Q];
+  s[0] = c;
+  sfor<1, L::Q>([&](auto q) { s[q] = __ldcs(a.idx + size_t(q - 1) * a.n_fluid + c); });
+  sfor<0, L::Q>([&](auto q) { t[q] = a.pdf[s[q]]; });
+  sfor<0, L::Q>([&](auto q) {
+    constexpr int qb = L::INV[q];
+    if constexpr (MODE == 0)
+      a.pdf[s[qb]] = t[q];
+    else
+      a.pdf[a.base[qb] + c] = t[q];
+  });
+}
+
+template <class L, int MODEL, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) k_aa_odd(const SweepArgs a) {
+
   const uint32_t i = blockIdx.x * kBlock + threadIdx.x;
   if (i >= a.n_cells) return;
   const uint32_t c = a.cids ? a.cids[i] : i;
@@ -98,14 +241,75 @@ __global__ void __launch_bounds__(kBlock) k_pull(const SweepArgs a) {
 
 enum Kind { kPull = 0, kEven = 1, kOdd = 2 };
 
+template <class L, int MODEL, int MINB>
+void launch_async(const SweepArgs& a, unsigned grid, cudaStream_t s) {
+  constexpr int bytes = L::Q * kBlock * sizeof(double);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_aa_even_async<L, MODEL, MINB>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    configured = true;
+  }
+  k_aa_even_async<L, MODEL, MINB><<<grid, kBlock, bytes, s>>>(a);
+}
+
+int g_num_sms = 0;
+
+template <class L, int MODEL, int MINB>
+void launch_pf(const SweepArgs& a, unsigned grid, cudaStream_t s) {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  constexpr int bytes = 2 * (L::Q - 1) * kBlock * sizeof(uint32_t);
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaFuncSetAttribute(k_aa_even_pf<L, MODEL, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         bytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_aa_even_pf<L, MODEL, MINB>, kBlock,
+                                                  bytes);
+    per_sm = std::max(per_sm, 1);
+  }
+  const unsigned persistent = unsigned(per_sm * g_num_sms);
+  k_aa_even_pf<L, MODEL, MINB><<<std::min(grid, persistent), kBlock, bytes, s>>>(a);
+}
+
 template <class L, int MODEL>
 void launch_kind(int kind, const SweepArgs& a, unsigned grid, cudaStream_t s) {
-  if (kind == kPull)
+  if (kind == kPull) {
     k_pull<L, MODEL><<<grid, kBlock, 0, s>>>(a);
-  else if (kind == kEven)
-    k_aa_even<L, MODEL><<<grid, kBlock, 0, s>>>(a);
-  else
-    k_aa_odd<L, MODEL><<<grid, kBlock, 0, s>>>(a);
+  } else if (kind == kEven) {
+    if constexpr (L::Q == 9) {
+      k_aa_even<L, MODEL, 1, false><<<grid, kBlock, 0, s>>>(a);
+    } else {
+      switch (g_even_variant) {
+        case 1: k_aa_even<L, MODEL, 3, false><<<grid, kBlock, 0, s>>>(a); break;
+        case 2: k_aa_even<L, MODEL, 4, false><<<grid, kBlock, 0, s>>>(a); break;
+        case 3: k_aa_even<L, MODEL, 3, true><<<grid, kBlock, 0, s>>>(a); break;
+        case 4: k_aa_even<L, MODEL, 4, true><<<grid, kBlock, 0, s>>>(a); break;
+        case 5: launch_async<L, MODEL, 4>(a, grid, s); break;
+        case 6: launch_async<L, MODEL, 3>(a, grid, s); break;
+        case 7: launch_async<L, MODEL, 2>(a, grid, s); break;
+        case 8: launch_pf<L, MODEL, 2>(a, grid, s); break;
+        case 9: launch_pf<L, MODEL, 1>(a, grid, s); break;
+        case 10: launch_pf<L, MODEL, 3>(a, grid, s); break;
+        case 11: k_probe<L, 0><<<grid, kBlock, 0, s>>>(a); break;
+        case 12: k_probe<L, 1><<<grid, kBlock, 0, s>>>(a); break;
+        default: k_aa_even<L, MODEL, 2, false><<<grid, kBlock, 0, s>>>(a); break;
+      }
+    }
+  } else {
+    if constexpr (L::Q == 9) {
+      k_aa_odd<L, MODEL, 1><<<grid, kBlock, 0, s>>>(a);
+    } else {
+      switch (g_odd_variant) {
+        case 1: k_aa_odd<L, MODEL, 3><<<grid, kBlock, 0, s>>>(a); break;
+        case 2: k_aa_odd<L, MODEL, 4><<<grid, kBlock, 0, s>>>(a); break;
+        default: k_aa_odd<L, MODEL, 2><<<grid, kBlock, 0, s>>>(a); break;
+      }
+    }
+  }
 }
 
 template <class L>
@@ -239,6 +443,13 @@ void by_lattice(int q, F&& f) {
 }
 
 }  // namespace
+
+int set_tuning(int knob, int value) {
+  if (knob == 0) g_even_variant = value;
+  else if (knob == 1) g_odd_variant = value;
+  else return fail(SLBM_ECONFIG, "unknown tuning knob");
+  return SLBM_OK;
+}
 
 int launch_slot_lookup(SlbmEngine* e, const int64_t* d_qs, const int64_t* d_pflat, int64_t n,
                        int64_t* d_out, int* d_err) {

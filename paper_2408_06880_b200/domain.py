@@ -207,7 +207,7 @@ class Domain:
     def __init__(self, global_flags, block_size, stencil, params, pattern: str = "pull",
                  policy: str = "sparse", phi_s: float = DEFAULT_PHI_S, frame_width=None,
                  device: int | None = None, check: str = "step", _rank: int = 0, _world: int = 1,
-                 _assignment=None, _comm=None):
+                 _assignment=None, _comm=None, engine_factory=None, halo_factory=None):
         if policy not in POLICIES:
             raise errors.make("ConfigurationError", f"unknown layout policy {policy!r}")
         if policy != "sparse":
@@ -245,16 +245,18 @@ class Domain:
             raise errors.make("ConfigurationError", "geometry has no fluid cells")
 
         self.assignment = dict(_assignment) if _assignment else {b: 0 for b in self.blocks}
+        make_engine = engine_factory or _cuda_engine
         for bid, blk in self.blocks.items():
             blk.rank = self.assignment.get(bid, 0)
             if blk.rank == self.rank:
-                blk.engine = SparseEngine(blk.flags, stencil, params, pattern=pattern,
-                                          frame_width=frame_width, device=self.device,
-                                          check="deferred")
+                blk.engine = make_engine(blk.flags, stencil, params, pattern, frame_width,
+                                         self.device)
         engines = self.local_engines()
-        self._stream = engines[0].stream() if engines else 0
+        self._stream = engines[0].stream() if engines and hasattr(engines[0], "stream") else 0
         for e in engines[1:]:
-            e.set_stream(self._stream)
+            if hasattr(e, "set_stream"):
+                e.set_stream(self._stream)
+        self._halo_factory = halo_factory or DeviceHalo
 
         self._edges = self._adjacency()
         self.edge_plans: list[EdgePlan] = []
@@ -295,11 +297,19 @@ class Domain:
         return edges
 
     def _build_halo(self):
-        halo = DeviceHalo(self.device)
+        """Registers every planned edge, in edge order, with the exchange
+        program.  Remote ends append to the peer's single per-phase message
+        in this order on both ranks (one message per peer per phase)."""
+        halo = self._halo_factory(self.device)
+        loopback = getattr(self, "_loopback", False)
         for plan in self.edge_plans:
             src, dst = self.blocks[plan.src_bid], self.blocks[plan.dst_bid]
             for ph, pp in plan.phases.items():
-                if src.rank == self.rank and dst.rank == self.rank:
+                if loopback:
+                    # test mode: every edge travels as a message to this rank
+                    halo.add_send(ph, src.engine, self.rank, pp)
+                    halo.add_recv(ph, dst.engine, self.rank, pp)
+                elif src.rank == self.rank and dst.rank == self.rank:
                     halo.add_local(ph, src.engine, dst.engine, pp)
                 elif src.rank == self.rank:
                     halo.add_send(ph, src.engine, dst.rank, pp)
@@ -469,27 +479,137 @@ class Domain:
         return {b: int(w) for b, w in zip(order, seats)}
 
 
+def _cuda_engine(flags, stencil, params, pattern, frame_width, device):
+    return SparseEngine(flags, stencil, params, pattern=pattern, frame_width=frame_width,
+                        device=device, check="deferred")
+
+
+class HostStagedHalo:
+    """DeviceHalo whose cross-rank messages travel through host memory and a
+    torch.distributed (gloo) group instead of NCCL: for tests with several
+    ranks on one GPU (NCCL refuses duplicate devices) and for hosts without
+    peer access.  Same message layout and order as the NCCL path."""
+
+    def __init__(self, device, group=None, world=1):
+        self.inner = DeviceHalo(device)
+        self.group = group
+        self.world = world
+
+    def add_local(self, *a):
+        self.inner.add_local(*a)
+
+    def add_send(self, *a):
+        self.inner.add_send(*a)
+
+    def add_recv(self, *a):
+        self.inner.add_recv(*a)
+
+    def commit(self, nccl_comm=None):
+        self.inner.commit(None)
+
+    def start(self, phase, after_stream):
+        import torch
+        import torch.distributed as dist
+
+        _abi_sync_stream(after_stream)
+        self.inner.local_only(phase)
+        sends, recvs = self.inner.peer_sizes(phase, self.world)
+        reqs, bufs = [], {}
+        for peer in range(self.world):
+            if sends[peer]:
+                out = np.empty(int(sends[peer]), dtype=np.float64)
+                self.inner.pack_host(phase, peer, out)
+                reqs.append(dist.isend(torch.from_numpy(out), dst=peer, group=self.group))
+                bufs[("s", peer)] = out
+            if recvs[peer]:
+                buf = torch.empty(int(recvs[peer]), dtype=torch.float64)
+                reqs.append(dist.irecv(buf, src=peer, group=self.group))
+                bufs[("r", peer)] = buf
+        for r in reqs:
+            r.wait()
+        for peer in range(self.world):
+            if recvs[peer]:
+                self.inner.unpack_host(phase, peer, bufs[("r", peer)].numpy())
+
+    def wait(self, stream):
+        self.inner.wait(stream)
+
+    def close(self):
+        self.inner.close()
+
+
+def _abi_sync_stream(stream):
+    """Wait until the compute stream has finished the previous sweep."""
+    if stream:
+        import ctypes as C
+
+        _cudart().cudaStreamSynchronize(C.c_void_p(stream))
+
+
+_CUDART = None
+
+
+def _cudart():
+    global _CUDART
+    if _CUDART is None:
+        import ctypes as C
+        import ctypes.util
+
+        for name in ("libcudart.so.12", "libcudart.so", ctypes.util.find_library("cudart")):
+            if not name:
+                continue
+            try:
+                _CUDART = C.CDLL(name)
+                break
+            except OSError:
+                continue
+    return _CUDART
+
+
 class DistributedDomain(Domain):
     """One process per GPU.  Blocks go to ranks by ``assignment`` (default:
     the reference's Hilbert/greedy ``balance``); cross-rank edges use NCCL
-    through the library's own communicator."""
+    through the library's own communicator (``transport="nccl"``), or host
+    staging over a gloo group (``transport="host"``)."""
 
     def __init__(self, global_flags, block_size, stencil, params, pattern="aa", frame_width=1,
                  rank: int | None = None, world: int | None = None, device: int | None = None,
-                 assignment=None, check: str = "deferred", comm=None):
+                 assignment=None, check: str = "deferred", comm=None, transport: str = "nccl",
+                 engine_factory=None, halo_factory=None, loopback: bool = False):
         import torch.distributed as dist
 
         rank = dist.get_rank() if rank is None else rank
         world = dist.get_world_size() if world is None else world
+        # loopback (tests): all edges become NCCL messages from this rank to itself
+        self._loopback = bool(loopback)
+        if loopback and comm is None:
+            comm = NcclComm(rank, 1, default_device() if device is None else device)
         if assignment is None:
-            probe = Domain.__new__(Domain)
             assignment = _balance_without_engines(global_flags, block_size, stencil, world)
-            del probe
-        if comm is None and world > 1:
+        if transport not in ("nccl", "host"):
+            raise errors.make("ConfigurationError", f"unknown transport {transport!r}")
+        if halo_factory is None and transport == "host":
+            group = dist.new_group(backend="gloo") if dist.get_backend() != "gloo" else None
+            halo_factory = lambda dev: HostStagedHalo(dev, group, world)  # noqa: E731
+        if comm is None and world > 1 and transport == "nccl" and halo_factory is None:
             comm = NcclComm(rank, world, default_device() if device is None else device)
         super().__init__(global_flags, block_size, stencil, params, pattern=pattern,
                          frame_width=frame_width, device=device, check=check, _rank=rank,
-                         _world=world, _assignment=assignment, _comm=comm)
+                         _world=world, _assignment=assignment, _comm=comm,
+                         engine_factory=engine_factory, halo_factory=halo_factory)
+
+    def gather_canonical_global(self) -> np.ndarray:
+        """gather_canonical summed over ranks (rank 0 gets the full field)."""
+        import torch
+        import torch.distributed as dist
+
+        local = torch.from_numpy(self.gather_canonical())
+        if dist.get_backend() == "nccl":
+            t = local.cuda()
+            dist.all_reduce(t)
+            return t.cpu().numpy()
+        dist.all_reduce(local)
+        return local.numpy()
 
     @classmethod
     def weak_scaling_bed(cls, block_edge, world, rank, stencil, params, porosity, diameter, seed,

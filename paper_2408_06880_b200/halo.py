@@ -247,14 +247,19 @@ class NcclComm:
     unique id travels through any torch.distributed backend."""
 
     def __init__(self, rank: int, world: int, device: int, group=None):
-        import torch.distributed as dist
-
         uid = (C.c_char * 128)()
-        if rank == 0:
+        if world == 1:
+            # single-rank communicator (loopback tests): no rendezvous needed
             _abi.call("slbm_nccl_get_unique_id", C.cast(uid, C.c_void_p))
-        payload = [bytes(uid)]
-        dist.broadcast_object_list(payload, src=0, group=group)
-        uid = (C.c_char * 128).from_buffer_copy(payload[0])
+            rank = 0
+        else:
+            import torch.distributed as dist
+
+            if rank == 0:
+                _abi.call("slbm_nccl_get_unique_id", C.cast(uid, C.c_void_p))
+            payload = [bytes(uid)]
+            dist.broadcast_object_list(payload, src=0, group=group)
+            uid = (C.c_char * 128).from_buffer_copy(payload[0])
         comm = C.c_void_p()
         _abi.call("slbm_nccl_comm_init", C.cast(uid, C.c_void_p), world, rank, device, C.byref(comm))
         self.handle = comm.value

@@ -1,0 +1,74 @@
+"""Multi-rank paths on one GPU:
+
+* loopback: every halo edge travels as a real NCCL message (ncclSend /
+  ncclRecv inside one group on the comm stream) from rank 0 to itself, so
+  pack kernel -> NCCL -> unpack kernel is exercised exactly as between GPUs;
+* two processes sharing the GPU with the host-staged transport (gloo),
+  blocks split between the ranks by the reference's balance.
+
+Both must reproduce the reference's single-process golden bit for bit."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from conftest import flags_of, golden_files, load_golden, params_of, stencil_of
+
+pytestmark = pytest.mark.gpu
+
+DOMAIN = {os.path.basename(p)[:-4]: p for p in golden_files("domain")}
+
+
+@pytest.mark.parametrize("pattern", ["aa", "pull"])
+@pytest.mark.parametrize("name", ["domain_d3q19_2x2x2", "domain_d3q27_riverbed",
+                                  "domain_d2q9_riverbed"])
+def test_nccl_loopback_matches_golden(name, pattern, gpu_lib):
+    from paper_2408_06880_b200.domain import DistributedDomain
+
+    rec = load_golden(DOMAIN[name])
+    dom = DistributedDomain(flags_of(rec), tuple(int(b) for b in rec["block"]), stencil_of(rec),
+                            params_of(rec), pattern=pattern, frame_width=1, rank=0, world=1,
+                            device=0, loopback=True)
+    dom.init_random(int(rec["seed"]))
+    dom.run(int(rec["steps"]), driver="overlapped")
+    np.testing.assert_array_equal(dom.gather_canonical(), rec[f"{pattern}_final"])
+
+
+def _worker(rank, world, port, path, pattern, out_dir):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2408_06880_b200.domain import DistributedDomain
+
+    rec = load_golden(path)
+    dom = DistributedDomain(flags_of(rec), tuple(int(b) for b in rec["block"]), stencil_of(rec),
+                            params_of(rec), pattern=pattern, frame_width=1, rank=rank, world=world,
+                            device=0, transport="host")
+    dom.init_random(int(rec["seed"]))
+    dom.run(int(rec["steps"]), driver="overlapped")
+    full = dom.gather_canonical_global()
+    if rank == 0:
+        np.save(os.path.join(out_dir, "full.npy"), full)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("name,pattern", [("domain_d3q19_2x2x2", "aa"),
+                                          ("domain_d3q19_walled_strips", "pull")])
+def test_two_ranks_host_staged_match_golden(name, pattern, tmp_path, gpu_lib):
+    path = DOMAIN[name]
+    mp.start_processes(_worker, args=(2, _free_port(), path, pattern, str(tmp_path)), nprocs=2,
+                       join=True, start_method="spawn")
+    rec = load_golden(path)
+    np.testing.assert_array_equal(np.load(tmp_path / "full.npy"), rec[f"{pattern}_final"])

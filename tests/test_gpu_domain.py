@@ -1,0 +1,106 @@
+"""Multi-block Domain on the GPU vs the reference's multi-block goldens:
+decomposition, EdgePlan slot lists, device halo exchange (fused local
+gather-scatter kernels), sequential and overlapped drivers — bit for bit."""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import flags_of, golden_files, load_golden, params_of, stencil_of
+
+pytestmark = pytest.mark.gpu
+
+DOMAIN = golden_files("domain")
+
+
+def _id(p):
+    return os.path.basename(p)[:-4]
+
+
+def _domain(rec, pattern, **kw):
+    from paper_2408_06880_b200.domain import Domain
+
+    return Domain(flags_of(rec), tuple(int(b) for b in rec["block"]), stencil_of(rec),
+                  params_of(rec), pattern=pattern, frame_width=1, **kw)
+
+
+@pytest.mark.parametrize("driver", ["overlapped", "sequential"])
+@pytest.mark.parametrize("pattern", ["pull", "aa"])
+@pytest.mark.parametrize("path", DOMAIN, ids=_id)
+def test_domain_run_bit_exact(path, pattern, driver, gpu_lib):
+    rec = load_golden(path)
+    dom = _domain(rec, pattern)
+    assert sorted(dom.blocks) == list(rec[f"{pattern}_blocks"])
+    dom.init_random(int(rec["seed"]))
+    np.testing.assert_array_equal(dom.gather_canonical(), rec[f"{pattern}_init"])
+    rows, send, take, tgt = [], [], [], []
+    for plan in dom.edge_plans:
+        for ph, pp in plan.phases.items():
+            rows.append([plan.src_bid, plan.dst_bid, *plan.sigma, ph.value, pp.n_wire, len(pp.tgt_sel)])
+            send.append(pp.send_sel)
+            take.append(pp.pos_from_sparse)
+            tgt.append(pp.tgt_sel)
+    assert np.array_equal(np.array(rows, dtype=np.int64), rec[f"{pattern}_edges"])
+    assert np.array_equal(np.concatenate(send), rec[f"{pattern}_send"])
+    assert np.array_equal(np.concatenate(take), rec[f"{pattern}_take"])
+    assert np.array_equal(np.concatenate(tgt), rec[f"{pattern}_tgt"])
+    dom.run(int(rec["steps"]), driver=driver)
+    np.testing.assert_array_equal(dom.gather_canonical(), rec[f"{pattern}_final"])
+    rho, u = dom.gather_macroscopics()
+    np.testing.assert_array_equal(rho, rec[f"{pattern}_rho"])
+    np.testing.assert_array_equal(u, rec[f"{pattern}_u"])
+    c = dom.counters()
+    got = [c.steps, c.cells_visited, c.cells_visited_interior, c.cells_visited_frame,
+           c.pdf_accesses, c.idx_reads, c.values_exchanged, c.messages]
+    if driver == "overlapped":
+        assert got == list(rec[f"{pattern}_counters"])
+
+
+def test_decomposition_invariance_and_aa_equals_pull(gpu_lib):
+    """reference tests/test_domain.py:134-173 on the GPU: 1, 2, 4, 8 blocks give
+    the same answer bitwise; AA pairs equal pull."""
+    from paper_2408_06880_b200 import geometry
+    from paper_2408_06880_b200.collision import CollisionParams
+    from paper_2408_06880_b200.domain import Domain
+    from paper_2408_06880_b200.lattice import make_stencil
+
+    st = make_stencil("d3q19")
+    gf = geometry.riverbed_flags((16, 16, 16), (8, 8, 8), 0.5, 3, 0.03)
+    p = CollisionParams(1.3, "trt", 0.9)
+    out = []
+    for pattern in ("aa", "pull"):
+        for block in [(16, 16, 16), (8, 16, 16), (8, 8, 16), (8, 8, 8)]:
+            d = Domain(gf, block, st, p, pattern=pattern, frame_width=1)
+            d.init_random(4)
+            d.run(6, driver="overlapped" if block[0] == 8 else "sequential")
+            out.append(d.gather_canonical())
+    for o in out[1:]:
+        np.testing.assert_array_equal(o, out[0])
+
+
+def test_run_wraps_instability_with_the_step_number(gpu_lib):
+    from paper_2408_06880_b200 import errors, geometry
+    from paper_2408_06880_b200.collision import CollisionParams
+    from paper_2408_06880_b200.domain import Domain
+    from paper_2408_06880_b200.lattice import make_stencil
+
+    gf = geometry.riverbed_flags((16, 16), (8, 8), seed=1, lid_speed=0.5)
+    dom = Domain(gf, (8, 8), make_stencil("d2q9"), CollisionParams(omega=1.99))
+    dom.init_random(1)
+    with pytest.raises(errors.NumericalInstabilityError, match="unstable at step"):
+        dom.run(100)
+
+
+def test_driver_validation(gpu_lib):
+    from paper_2408_06880_b200 import errors, geometry
+    from paper_2408_06880_b200.collision import CollisionParams
+    from paper_2408_06880_b200.domain import Domain
+    from paper_2408_06880_b200.lattice import make_stencil
+
+    dom = Domain(geometry.channel_flags((8, 4)), (4, 4), make_stencil("d2q9"), CollisionParams(1.0))
+    dom.init_equilibrium()
+    with pytest.raises(errors.ConfigurationError, match="frame_width"):
+        dom.run(1, driver="overlapped")
+    with pytest.raises(errors.ConfigurationError, match="unknown driver"):
+        dom.run(1, driver="sideways")

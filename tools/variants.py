@@ -1,0 +1,94 @@
+"""Time the AA sweep kernel variants (slbm_set_tuning) on the bench workload
+and check they are bit-identical.
+
+    python tools/variants.py            # prints a table + JSON
+"""
+
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2408_06880_b200 import _abi  # noqa: E402
+from paper_2408_06880_b200.collision import CollisionParams  # noqa: E402
+from paper_2408_06880_b200.engine import SparseEngine  # noqa: E402
+from paper_2408_06880_b200.lattice import make_stencil  # noqa: E402
+
+
+def time_pair(eng, reps=6):
+    stream = torch.cuda.ExternalStream(eng.stream())
+    out = {0: [], 1: []}
+    for _ in range(2 * reps):
+        par = eng.parity.value
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        eng.refresh_boundary(eng.parity)
+        a.record(stream)
+        eng.step()
+        b.record(stream)
+        eng.finish_step()
+        b.synchronize()
+        out[par].append(a.elapsed_time(b))
+    return statistics.median(out[0]), statistics.median(out[1])
+
+
+def main():
+    q = int(os.environ.get("Q", 19))
+    model = os.environ.get("MODEL", "trt")
+    edge = int(os.environ.get("EDGE", 512))
+    variants = [int(v) for v in os.environ.get("VARIANTS", "0,1,2,3,4").split(",")]
+    odd_variants = [int(v) for v in os.environ.get("ODD_VARIANTS", "0,1,2").split(",")]
+    st = make_stencil("d3q19" if q == 19 else "d3q27")
+    p = CollisionParams(bench.OMEGA, model, bench.magic_lambda(bench.OMEGA))
+    fl = bench.make_flags(edge, 0)
+    eng = SparseEngine(fl, st, p, "aa", device=0, check="deferred")
+    n = eng.n_fluid
+    lib = _abi.load()
+    eng.init_equilibrium(1.0, np.array([0.01, 0.0, 0.0]))
+    eng.run(4, use_graph=False)
+    res = {"n_fluid": n, "q": q, "model": model, "even": {}, "odd": {}}
+    be = 2 * q * 8 + (q - 1) * 4
+    bo = 2 * q * 8
+    hbm = bench.peaks()[0]
+    for v in variants:
+        lib.slbm_set_tuning(0, v)
+        te, _ = time_pair(eng)
+        res["even"][v] = {"ms": te, "gbs": n * be / te / 1e6, "frac": n * be / te / 1e6 / hbm}
+        print(f"even variant {v}: {te:.4f} ms  {n * be / te / 1e6:.0f} GB/s  {n * be / te / 1e6 / hbm:.3f}")
+    lib.slbm_set_tuning(0, 0)
+    for v in odd_variants:
+        lib.slbm_set_tuning(1, v)
+        _, to = time_pair(eng)
+        res["odd"][v] = {"ms": to, "gbs": n * bo / to / 1e6, "frac": n * bo / to / 1e6 / hbm}
+        print(f"odd variant {v}: {to:.4f} ms  {n * bo / to / 1e6:.0f} GB/s  {n * bo / to / 1e6 / hbm:.3f}")
+    lib.slbm_set_tuning(1, 0)
+    eng.poll()
+    # bitwise agreement of all variants on a small bed
+    small = bench.make_flags(48, 0)
+    ref = None
+    for v in variants:
+        for ov in odd_variants:
+            lib.slbm_set_tuning(0, v)
+            lib.slbm_set_tuning(1, ov)
+            e = SparseEngine(small, st, p, "aa", device=0)
+            e.init_equilibrium(1.0, np.array([0.02, 0.01, 0.0]))
+            e.run(6, use_graph=False)
+            s = e.canonical_state()
+            if ref is None:
+                ref = s
+            assert np.array_equal(s, ref), (v, ov)
+    lib.slbm_set_tuning(0, 0)
+    lib.slbm_set_tuning(1, 0)
+    res["bitwise_equal"] = True
+    print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()
