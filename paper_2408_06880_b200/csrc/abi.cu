@@ -70,7 +70,8 @@ DirTable make_dirs(int q) {
 void free_engine(SlbmEngine* e) {
   if (!e) return;
   DeviceGuard g(e->device);
-  if (e->stream) cudaStreamSynchronize(e->stream);
+  // only the stream this engine created; a borrowed stream may already be gone
+  if (e->own_stream) cudaStreamSynchronize(e->own_stream);
   for (auto& gx : e->graph)
     if (gx) cudaGraphExecDestroy(gx);
   void* ptrs[] = {e->pdf,         e->tmp,          e->idx,       e->x_flat,

@@ -306,7 +306,7 @@ void launch_kind(int kind, const SweepArgs& a, unsigned grid, cudaStream_t s) {
       switch (g_odd_variant) {
         case 1: k_aa_odd<L, MODEL, 3><<<grid, kBlock, 0, s>>>(a); break;
         case 2: k_aa_odd<L, MODEL, 4><<<grid, kBlock, 0, s>>>(a); break;
-        default: k_aa_odd<L, MODEL, 2><<<grid, kBlock, 0, s>>>(a); break;
+        default: k_aa_odd<L, MODEL, 3><<<grid, kBlock, 0, s>>>(a); break;
       }
     }
   }
