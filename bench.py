@@ -232,8 +232,8 @@ def impl_ours(args, rank, world, local_rank):
     from paper_2408_06880_b200.engine import SparseEngine
     from paper_2408_06880_b200.lattice import make_stencil
 
-    torch.cuda.set_device(local_rank)
-    dev = local_rank
+    dev = int(os.environ.get("SLBM_DEVICE", local_rank))
+    torch.cuda.set_device(dev)
     st = make_stencil("d3q19")
     p = CollisionParams(OMEGA, "trt", magic_lambda(OMEGA))
     steps, warmup = args.steps, args.warmup
@@ -242,6 +242,14 @@ def impl_ours(args, rank, world, local_rank):
     dist = None
     if world > 1:
         import torch.distributed as dist
+
+    def reduce(x, op="max"):
+        if dist is None:
+            return x
+        on_gpu = dist.get_backend() == "nccl"
+        t = torch.tensor([float(x)], dtype=torch.float64, device=f"cuda:{dev}" if on_gpu else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+        return float(t.item())
 
     t_build = time.perf_counter()
     if world == 1:
@@ -253,10 +261,11 @@ def impl_ours(args, rank, world, local_rank):
         from paper_2408_06880_b200.domain import DistributedDomain
 
         runner = DistributedDomain.weak_scaling_bed(
-            (EDGE, EDGE, EDGE), world, rank, st, p, POROSITY, DIAMETER, SEED, device=dev)
+            (EDGE, EDGE, EDGE), world, rank, st, p, POROSITY, DIAMETER, SEED, device=dev,
+            transport=os.environ.get("SLBM_TRANSPORT", "nccl"))
         eng = runner.local_engines()[0]
         n_fluid_local = runner.local_fluid()
-    build_s = time.perf_counter() - t_build
+    build_s = reduce(time.perf_counter() - t_build)
 
     runner.init_equilibrium(1.0, np.array([0.01, 0.0, 0.0]))
     runner.run(warmup)
@@ -280,11 +289,8 @@ def impl_ours(args, rank, world, local_rank):
     runner.synchronize()
     torch.cuda.synchronize()
     clocks.mark("t1")
-    ms = ev0.elapsed_time(ev1)
+    ms = reduce(ev0.elapsed_time(ev1))
     if dist is not None:
-        t = torch.tensor([ms], device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
         dist.barrier()
     runner.poll()
 
@@ -293,19 +299,18 @@ def impl_ours(args, rank, world, local_rank):
     clocks.stop()
     csum = clocks.summary()
 
-    total_fluid = n_fluid_local
-    if dist is not None:
-        t = torch.tensor([n_fluid_local], device=f"cuda:{dev}", dtype=torch.float64)
-        dist.all_reduce(t)
-        total_fluid = int(t.item())
+    total_fluid = int(reduce(n_fluid_local, "sum"))
     value = total_fluid * steps / (ms / 1e3) / 1e6
 
-    # e2e through the public API with host buffers (rank 0 engine, N = 1)
-    e2e = None
+    # e2e through the public API with host buffers
     if world == 1:
         e2e = e2e_run(eng, steps, torch)
+    else:
+        e2e = e2e_domain(runner, steps, torch, reduce, total_fluid)
 
-    launches_per_step = 2 + (1 if eng.n_ubb_slots else 0)
+    # sweep + step-counter kernel (+ UBB refresh); N > 1 adds the halo pack and
+    # unpack kernels and splits the sweep into interior + frame
+    launches_per_step = 2 + (1 if eng.n_ubb_slots else 0) + (3 if world > 1 else 0)
     hbm, hbm_src = peaks()
     ach_even = eng.n_fluid * BYTES_EVEN / (t_even / 1e3) / 1e9
     ach_odd = eng.n_fluid * BYTES_ODD / (t_odd / 1e3) / 1e9
@@ -404,6 +409,37 @@ def e2e_run(eng, steps, torch):
                     f"macroscopic_fields({cells} cells)"}
 
 
+def e2e_domain(dom, steps, torch, reduce, total_fluid):
+    """N > 1: every rank uploads its blocks' initial state from pinned host
+    memory, runs the overlapped driver from Python, and reads back its
+    macroscopic fields; wall time is the max over ranks."""
+    import torch.distributed as dist
+
+    hosts = []
+    for e in dom.local_engines():
+        h = torch.empty((e.stencil.q, e.n_fluid), dtype=torch.float64, pin_memory=True).numpy()
+        for r in range(e.stencil.q):
+            h[r].fill(e.stencil.w[r])
+        hosts.append(h)
+    dist.barrier()
+    t0 = time.perf_counter()
+    for e, h in zip(dom.local_engines(), hosts):
+        e.init_canonical(h)
+    dom.run(steps)
+    rho_bytes = 0
+    for e in dom.local_engines():
+        rho, u = e.macroscopic_fields()
+        rho_bytes += rho.nbytes + u.nbytes
+    dt = reduce(time.perf_counter() - t0)
+    h2d = reduce(sum(h.nbytes for h in hosts), "sum")
+    d2h = reduce(rho_bytes, "sum")
+    return {"value": round(total_fluid * steps / dt / 1e6, 2), "unit": "MFLUPS",
+            "h2d_bytes_per_step": int(h2d // steps), "d2h_bytes_per_step": int(d2h // steps),
+            "seconds": round(dt, 4), "steps": steps,
+            "note": "per rank: init_canonical from pinned host + DistributedDomain.run (overlapped "
+                    "driver, NCCL halo) + macroscopic_fields; max over ranks"}
+
+
 def load_traffic():
     """ncu dram bytes per launch of the dominant kernel, if a summary is
     committed under profiles/ (written by tools/ncu_summary.py)."""
@@ -436,8 +472,13 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        dev = int(os.environ.get("SLBM_DEVICE", local_rank))
+        torch.cuda.set_device(dev)
+        if os.environ.get("SLBM_TRANSPORT") == "host":
+            # test mode: several ranks on one GPU, halo over host memory + gloo
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
     impl_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist

@@ -613,7 +613,7 @@ class DistributedDomain(Domain):
 
     @classmethod
     def weak_scaling_bed(cls, block_edge, world, rank, stencil, params, porosity, diameter, seed,
-                         device=None):
+                         device=None, transport="nccl"):
         """world blocks of ``block_edge`` along x, fully periodic
         overlapping-sphere bed over the whole box, block i on rank i."""
         from .geometry import packed_bed_flags
@@ -624,7 +624,7 @@ class DistributedDomain(Domain):
                               device=default_device() if device is None else device)
         assignment = {i: i for i in range(world)}
         return cls(fl, (bx, by, bz), stencil, params, pattern="aa", frame_width=1, rank=rank,
-                   world=world, device=device, assignment=assignment)
+                   world=world, device=device, assignment=assignment, transport=transport)
 
     def run(self, steps: int, driver: str = "overlapped") -> None:
         super().run(steps, driver)
