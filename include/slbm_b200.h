@@ -70,6 +70,7 @@ typedef struct SlbmInfo {
   int64_t n_ubb_q[27];
   int64_t n_ghost_q[27];
   int64_t device_bytes;  /* bytes of device memory held by the engine */
+  int64_t n_outlet_slots; /* fixed-density outlet reads (extension, tag 4) */
 } SlbmInfo;
 
 /* ---- construction: SparseEngine.__init__ (sparse.py:51-93) ----------------

@@ -19,7 +19,7 @@ from __future__ import annotations
 import numpy as np
 
 CS2 = 1.0 / 3.0
-FLUID, NOSLIP, UBB, EXCHANGE = 0, 1, 2, 3
+FLUID, NOSLIP, UBB, EXCHANGE, OUTLET = 0, 1, 2, 3, 4
 
 
 class OracleError(Exception):
@@ -77,7 +77,13 @@ def equilibrium(rho, u, st):
 
 
 def collide(t, params, st):
-    """core.py:149-170 (SRT / TRT)"""
+    """core.py:149-170 (SRT / TRT); "cumulant" -> oracle/cumulant_ref.py
+    (not in the reference, unpinned)"""
+    if params.model == "cumulant":
+        from .cumulant_ref import cumulant_collide
+
+        moments(t, st)  # same instability check as every collision
+        return cumulant_collide(t, params.omega, st)
     rho, u = moments(t, st)
     feq = equilibrium(rho, u, st)
     if params.model == "srt":
@@ -153,7 +159,10 @@ def build_lists(flags, st):
     n_ubb = np.array([0] + [int((up_tag[k] == UBB).sum()) for k in range(1, q)], dtype=np.int64)
     n_ghost = np.array([0] + [int((up_tag[k] == EXCHANGE).sum()) for k in range(1, q)],
                        dtype=np.int64)
-    sizes = n + n_ubb + n_ghost
+    # OUTLET (extension, unpinned): slots appended after the ghost slots, so
+    # layouts without outlets are exactly the reference's
+    n_out = np.array([0] + [int((up_tag[k] == OUTLET).sum()) for k in range(1, q)], dtype=np.int64)
+    sizes = n + n_ubb + n_ghost + n_out
     base = np.zeros(q + 1, dtype=np.int64)
     base[1:] = np.cumsum(sizes)
     total = int(base[-1])
@@ -163,6 +172,7 @@ def build_lists(flags, st):
     idx = np.full((q - 1, n), -1, dtype=np.int64)
     ghost = {}
     ubb_s, ubb_p, ubb_c = [], [], []
+    out_s, out_p, out_c, out_q, out_r = [], [], [], [], []
     for k in range(1, q):
         tag = up_tag[k]
         row = idx[k - 1]
@@ -189,6 +199,14 @@ def build_lists(flags, st):
             for r, i in enumerate(order):
                 row[sel[i]] = first + r
                 ghost[(k, int(pf[i]))] = int(first + r)
+        sel = np.nonzero(tag == OUTLET)[0]
+        slots = base[k] + n + n_ubb[k] + n_ghost[k] + np.arange(sel.size)
+        row[sel] = slots
+        out_s.append(slots)
+        out_p.append(base[st.inv[k]] + sel)
+        out_c.append(sel)
+        out_q.append(np.full(sel.size, k))
+        out_r.append(ubb_flat[upwind[k][sel]][:, 0] if sel.size else np.empty(0))
     if np.any(idx < 0):
         raise OracleError("unknown tag upwind of a fluid cell")
     owned = np.concatenate((np.arange(n), idx.ravel()))
@@ -206,6 +224,12 @@ def build_lists(flags, st):
         "ubb_slots": cat(ubb_s, np.int64),
         "ubb_partner": cat(ubb_p, np.int64),
         "ubb_corr": cat(ubb_c, np.float64),
+        "n_out": int(n_out.sum()),
+        "out_slots": cat(out_s, np.int64),
+        "out_partner": cat(out_p, np.int64),
+        "out_cell": cat(out_c, np.int64),
+        "out_q": cat(out_q, np.int64),
+        "out_rho": cat(out_r, np.float64),
         "ghost": ghost,
         "cid_map": cid_map,
         "padded_shape": padded,
@@ -347,12 +371,44 @@ class OracleSparseEngine:
     def refresh_boundary(self, parity):
         parity = getattr(parity, "value", parity)
         L = self._lists
-        if L["ubb_slots"].size == 0:
-            return
+        if L["ubb_slots"].size:
+            if parity == 0:
+                self._pdf[L["ubb_slots"]] = self._pdf[L["ubb_partner"]] + L["ubb_corr"]
+            else:
+                self._pdf[L["ubb_partner"]] = self._pdf[L["ubb_slots"]] + L["ubb_corr"]
+        if L["n_out"]:
+            self._refresh_outlet(parity)
+
+    def _refresh_outlet(self, parity):
+        """Fixed-density outlet (extension; csrc/kernels.cu k_outlet):
+        anti-bounce-back f_q = 2 w_q rho_o (1 + 4.5 (c_q.u)^2 - 1.5 u^2) - f*_inv(q)
+        with u the velocity of the adjacent fluid cell, evaluated from its
+        EVEN-parity slots and kept for the following ODD refresh."""
+        from .cumulant_ref import _seeded_sum
+
+        L, st = self._lists, self.stencil
+        cells = L["out_cell"]
+        if not hasattr(self, "_out_u"):
+            self._out_u = [np.zeros(cells.size) for _ in range(st.dim)]
         if parity == 0:
-            self._pdf[L["ubb_slots"]] = self._pdf[L["ubb_partner"]] + L["ubb_corr"]
+            t = np.stack([self._pdf[self.base[r] + cells] for r in range(st.q)])
+            rho = t[0] + t[1]
+            for r in range(2, st.q):
+                rho = rho + t[r]
+            self._out_u = [_seeded_sum(t, st.c[:, a]) / rho for a in range(st.dim)]
+        u = self._out_u
+        usq = u[0] * u[0]
+        for a in range(1, st.dim):
+            usq = usq + u[a] * u[a]
+        cu = np.empty_like(usq)
+        for i, k in enumerate(L["out_q"]):
+            cu[i] = _seeded_sum([ua[i:i + 1] for ua in u], st.c[k])[0]
+        w = st.w[L["out_q"]]
+        feq_sym = (w * L["out_rho"]) * ((1.0 + (4.5 * cu) * cu) - 1.5 * usq)
+        if parity == 0:
+            self._pdf[L["out_slots"]] = 2.0 * feq_sym - self._pdf[L["out_partner"]]
         else:
-            self._pdf[L["ubb_partner"]] = self._pdf[L["ubb_slots"]] + L["ubb_corr"]
+            self._pdf[L["out_partner"]] = 2.0 * feq_sym - self._pdf[L["out_slots"]]
 
     # inspection
     def canonical_state(self):

@@ -41,6 +41,7 @@ class SlbmInfo(C.Structure):
         ("n_ubb_q", C.c_int64 * 27),
         ("n_ghost_q", C.c_int64 * 27),
         ("device_bytes", C.c_int64),
+        ("n_outlet_slots", C.c_int64),
     ]
 
 

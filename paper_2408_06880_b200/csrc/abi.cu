@@ -77,6 +77,8 @@ void free_engine(SlbmEngine* e) {
   void* ptrs[] = {e->pdf,         e->tmp,          e->idx,       e->x_flat,
                   e->cid_map,     e->ubb_slot,     e->ubb_partner, e->ubb_corr,
                   e->ghost_key,   e->interior_cids, e->frame_cids, e->d_bad,
+                  e->out_slot,    e->out_partner,  e->out_cell,  e->out_dir,
+                  e->out_rho,     e->out_u,
                   e->d_step,      e->d_scratch};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -89,7 +91,7 @@ int check_model(int q, int model) {
   if (model == SLBM_SRT || model == SLBM_TRT) return SLBM_OK;
   if (model == SLBM_CUMULANT) {
     if (q != 27) return fail(SLBM_ECONFIG, "cumulant collision needs the d3q27 stencil");
-    return fail(SLBM_ECONFIG, "cumulant collision is not available in this build yet");
+    return SLBM_OK;
   }
   return fail(SLBM_ECONFIG, "unknown collision model code " + std::to_string(model));
 }
@@ -227,6 +229,7 @@ int slbm_engine_info(const SlbmEngine* e, SlbmInfo* info) {
   info->total_slots = e->total_slots;
   info->n_ubb_slots = e->n_ubb;
   info->n_ghost_slots = e->n_ghost;
+  info->n_outlet_slots = e->n_out;
   info->n_interior = e->has_split ? e->n_interior : e->n_fluid;
   info->n_frame = e->has_split ? e->n_frame : 0;
   for (int q = 0; q <= e->q; ++q) info->base[q] = e->base[q];

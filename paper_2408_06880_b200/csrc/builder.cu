@@ -29,7 +29,8 @@
 namespace slbm {
 namespace {
 
-constexpr uint8_t kFluid = 0, kNoslip = 1, kUbb = 2, kExchange = 3;
+constexpr uint8_t kFluid = 0, kNoslip = 1, kUbb = 2, kExchange = 3, kOutlet = 4;
+constexpr int kCounters = 3 * 27;  // per q: UBB, ghost, outlet
 
 __host__ __device__ inline int64_t wrap(int64_t v, int64_t n) {
   int64_t r = v % n;
@@ -101,8 +102,8 @@ __global__ void k_cid_map(const uint32_t* x_flat, int64_t n, int32_t* cid_map) {
 // pass 1: per-direction UBB / ghost counts and sanity of every upwind tag
 __global__ void k_count(const uint8_t* tags, const int32_t* cid_map, const uint32_t* x_flat,
                         int64_t n, Upwind up, unsigned long long* counts, int* err) {
-  __shared__ unsigned int s_cnt[54];
-  for (int i = threadIdx.x; i < 54; i += blockDim.x) s_cnt[i] = 0;
+  __shared__ unsigned int s_cnt[kCounters];
+  for (int i = threadIdx.x; i < kCounters; i += blockDim.x) s_cnt[i] = 0;
   __syncthreads();
   for (int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < n;
        c += int64_t(gridDim.x) * blockDim.x) {
@@ -112,9 +113,11 @@ __global__ void k_count(const uint8_t* tags, const int32_t* cid_map, const uint3
       int64_t p = up(q, x, y, z);
       uint8_t tag = tags[p];
       if (tag == kUbb) {
-        atomicAdd(&s_cnt[2 * q], 1u);
+        atomicAdd(&s_cnt[3 * q], 1u);
       } else if (tag == kExchange) {
-        atomicAdd(&s_cnt[2 * q + 1], 1u);
+        atomicAdd(&s_cnt[3 * q + 1], 1u);
+      } else if (tag == kOutlet) {
+        atomicAdd(&s_cnt[3 * q + 2], 1u);
       } else if (tag == kFluid) {
         if (cid_map[p] < 0) atomicOr(err, 1);
       } else if (tag != kNoslip) {
@@ -123,7 +126,7 @@ __global__ void k_count(const uint8_t* tags, const int32_t* cid_map, const uint3
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < 54; i += blockDim.x)
+  for (int i = threadIdx.x; i < kCounters; i += blockDim.x)
     if (s_cnt[i]) atomicAdd(&counts[i], (unsigned long long)s_cnt[i]);
 }
 
@@ -192,6 +195,32 @@ __global__ void k_ubb_assign(const uint32_t* sel, int64_t cnt, int q, const uint
   }
   const double cs2 = 1.0 / 3.0;
   ubb_corr[k] = (((2.0 * up.d.w[q]) * 1.0) * cu) / cs2;
+}
+
+// OUTLET reads of direction q, `sel` = cells in cid order; the prescribed
+// density sits in component 0 of the wall table
+__global__ void k_outlet_assign(const uint32_t* sel, int64_t cnt, int q, const uint32_t* x_flat,
+                                int64_t n, Upwind up, Bases bases, uint32_t first,
+                                const uint32_t* wall_flat, const double* wall_u, int64_t n_wall,
+                                uint32_t* idx, uint32_t* o_slot, uint32_t* o_partner,
+                                uint32_t* o_cell, uint8_t* o_dir, double* o_rho, int* err) {
+  int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= cnt) return;
+  uint32_t c = sel[k];
+  uint32_t slot = first + uint32_t(k);
+  idx[(q - 1) * n + c] = slot;
+  o_slot[k] = slot;
+  o_partner[k] = bases.b[up.d.inv[q]] + c;
+  o_cell[k] = c;
+  o_dir[k] = uint8_t(q);
+  int64_t x, y, z;
+  up.g.coords(x_flat[c], x, y, z);
+  int64_t at = find_sorted(wall_flat, n_wall, uint32_t(up(q, x, y, z)));
+  if (at < 0) {
+    atomicOr(err, 4);
+    return;
+  }
+  o_rho[k] = wall_u[at * 3];
 }
 
 // ghost keys: (ring offset of the upwind halo cell, its padded flat index)
@@ -288,8 +317,9 @@ int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
   std::vector<uint32_t> wall_flat;
   std::vector<double> wall_u;
   for (int64_t p = 0; p < n_pad; ++p) {
-    if (tags_pad[p] != kUbb) continue;
-    if (!ubb_u_pad) return fail(SLBM_ECONFIG, "UBB tags present but no wall velocity array");
+    if (tags_pad[p] != kUbb && tags_pad[p] != kOutlet) continue;
+    if (!ubb_u_pad)
+      return fail(SLBM_ECONFIG, "UBB/OUTLET tags present but no wall velocity/density array");
     wall_flat.push_back(uint32_t(p));
     for (int a = 0; a < 3; ++a) wall_u.push_back(a < g.dim ? ubb_u_pad[p * g.dim + a] : 0.0);
   }
@@ -324,9 +354,9 @@ int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
   Upwind up{g, d};
   unsigned long long* d_counts = nullptr;
   int* d_err = nullptr;
-  SLBM_CUDA_TRY(cudaMalloc(&d_counts, 54 * sizeof(unsigned long long)));
+  SLBM_CUDA_TRY(cudaMalloc(&d_counts, kCounters * sizeof(unsigned long long)));
   SLBM_CUDA_TRY(cudaMalloc(&d_err, sizeof(int)));
-  SLBM_CUDA_TRY(cudaMemsetAsync(d_counts, 0, 54 * sizeof(unsigned long long), s));
+  SLBM_CUDA_TRY(cudaMemsetAsync(d_counts, 0, kCounters * sizeof(unsigned long long), s));
   SLBM_CUDA_TRY(cudaMemsetAsync(d_err, 0, sizeof(int), s));
   {
     int dev_sms = 148;
@@ -334,7 +364,7 @@ int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
     unsigned blocks = std::min<unsigned>(grid_for(n, 256), unsigned(dev_sms) * 8);
     k_count<<<blocks, 256, 0, s>>>(d_tags, e->cid_map, e->x_flat, n, up, d_counts, d_err);
   }
-  unsigned long long h_counts[54];
+  unsigned long long h_counts[kCounters];
   int h_err = 0;
   SLBM_CUDA_TRY(cudaMemcpyAsync(h_counts, d_counts, sizeof(h_counts), cudaMemcpyDeviceToHost, s));
   SLBM_CUDA_TRY(cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -358,22 +388,28 @@ int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
   // -- slot budget (sparse.py:128-137) --
   int64_t total = 0;
   e->base[0] = 0;
+  // outlet slots (extension; no reference counterpart) follow the ghost
+  // slots, so blocks without outlets keep the reference layout exactly
   for (int q = 0; q < d.q; ++q) {
-    int64_t nu = q ? int64_t(h_counts[2 * q]) : 0;
-    int64_t ng = q ? int64_t(h_counts[2 * q + 1]) : 0;
+    int64_t nu = q ? int64_t(h_counts[3 * q]) : 0;
+    int64_t ng = q ? int64_t(h_counts[3 * q + 1]) : 0;
+    int64_t no = q ? int64_t(h_counts[3 * q + 2]) : 0;
     e->n_ubb_q[q] = nu;
     e->n_ghost_q[q] = ng;
-    total += n + nu + ng;
+    e->n_out_q[q] = no;
+    total += n + nu + ng + no;
     e->base[q + 1] = total;
   }
   e->total_slots = total;
-  e->n_ubb = e->n_ghost = 0;
-  e->ubb_off[0] = e->ghost_off[0] = 0;
+  e->n_ubb = e->n_ghost = e->n_out = 0;
+  e->ubb_off[0] = e->ghost_off[0] = e->out_off[0] = 0;
   for (int q = 0; q < d.q; ++q) {
     e->n_ubb += e->n_ubb_q[q];
     e->n_ghost += e->n_ghost_q[q];
+    e->n_out += e->n_out_q[q];
     e->ubb_off[q + 1] = e->n_ubb;
     e->ghost_off[q + 1] = e->n_ghost;
+    e->out_off[q + 1] = e->n_out;
   }
   if (total >= (int64_t(1) << 32)) {
     cleanup();
@@ -392,7 +428,7 @@ int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
   SLBM_TRY(dalloc(e, &e->ubb_corr, e->n_ubb));
   uint32_t* d_wall_flat = nullptr;
   double* d_wall_u = nullptr;
-  if (e->n_ubb) {
+  if (e->n_ubb || e->n_out) {
     SLBM_CUDA_TRY(cudaMalloc(&d_wall_flat, wall_flat.size() * sizeof(uint32_t)));
     SLBM_CUDA_TRY(cudaMalloc(&d_wall_u, wall_u.size() * sizeof(double)));
     SLBM_CUDA_TRY(cudaMemcpyAsync(d_wall_flat, wall_flat.data(),
@@ -446,6 +482,27 @@ int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
     cudaFree(k_in);
     cudaFree(k_out);
     cudaFree(c_out);
+  }
+
+  // -- fixed-density outlet reads (extension): cid order within q --
+  SLBM_TRY(dalloc(e, &e->out_slot, e->n_out));
+  SLBM_TRY(dalloc(e, &e->out_partner, e->n_out));
+  SLBM_TRY(dalloc(e, &e->out_cell, e->n_out));
+  SLBM_TRY(dalloc(e, &e->out_dir, e->n_out));
+  SLBM_TRY(dalloc(e, &e->out_rho, e->n_out));
+  SLBM_TRY(dalloc(e, &e->out_u, 3 * e->n_out));
+  SLBM_CUDA_TRY(cudaMemsetAsync(e->out_u, 0, 3 * std::max<int64_t>(e->n_out, 1) * sizeof(double), s));
+  for (int q = 1; q < d.q; ++q) {
+    if (!e->n_out_q[q]) continue;
+    int64_t cnt = 0;
+    SLBM_TRY(select_if(thrust::counting_iterator<uint32_t>(0), sel_buf, n,
+                       ReadsTag{d_tags, e->x_flat, up, q, kOutlet}, &cnt, s));
+    const uint32_t first = uint32_t(e->base[q] + n + e->n_ubb_q[q] + e->n_ghost_q[q]);
+    const int64_t off = e->out_off[q];
+    k_outlet_assign<<<grid_for(cnt, 256), 256, 0, s>>>(
+        sel_buf, cnt, q, e->x_flat, n, up, bases, first, d_wall_flat, d_wall_u,
+        int64_t(wall_flat.size()), e->idx, e->out_slot + off, e->out_partner + off,
+        e->out_cell + off, e->out_dir + off, e->out_rho + off, d_err);
   }
 
   // -- ownership uniqueness (sparse.py:182-185) --

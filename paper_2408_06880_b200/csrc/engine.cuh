@@ -21,6 +21,7 @@ struct SlbmEngine {
   int64_t base[28] = {0};
   int64_t n_ubb_q[27] = {0}, n_ghost_q[27] = {0};
   int64_t ubb_off[28] = {0}, ghost_off[28] = {0};
+  int64_t n_out = 0, n_out_q[27] = {0}, out_off[28] = {0};
 
   // device memory
   double* pdf = nullptr;   // active buffer
@@ -31,6 +32,12 @@ struct SlbmEngine {
   uint32_t* ubb_slot = nullptr;
   uint32_t* ubb_partner = nullptr;
   double* ubb_corr = nullptr;
+  uint32_t* out_slot = nullptr;     // fixed-density outlet program
+  uint32_t* out_partner = nullptr;
+  uint32_t* out_cell = nullptr;
+  uint8_t* out_dir = nullptr;
+  double* out_rho = nullptr;
+  double* out_u = nullptr;          // 3 x n_out, velocity kept EVEN -> ODD
   uint64_t* ghost_key = nullptr;  // per q sorted (sigma_key << 32 | pflat)
   std::vector<uint64_t> ghost_key_host;
   uint32_t* interior_cids = nullptr;

@@ -31,7 +31,7 @@ from . import _abi, errors
 from .collision import Parity, params_code
 from .counters import Counters
 from .lattice import stencil_code
-from .tags import UBB, rev_shape
+from .tags import OUTLET, UBB, rev_shape
 
 PATTERNS = ("pull", "aa")
 _PHASE_CODE = {"all": 0, "interior": 1, "frame": 2}
@@ -90,7 +90,7 @@ class SparseEngine:
         if tags.shape != want:
             raise errors.make("ConfigurationError", f"tag box shape {tags.shape} != {want}")
         ubb = None
-        if np.any(tags == UBB):
+        if np.any((tags == UBB) | (tags == OUTLET)):
             ubb = np.ascontiguousarray(flags.ubb_u, dtype=np.float64)
             if ubb.shape != want + (dim,):
                 raise errors.make("ConfigurationError", f"ubb_u shape {ubb.shape} != {want + (dim,)}")
@@ -122,6 +122,7 @@ class SparseEngine:
         self.total_slots = int(info.total_slots)
         self.n_ubb_slots = int(info.n_ubb_slots)
         self.n_ghost_slots = int(info.n_ghost_slots)
+        self.n_outlet_slots = int(info.n_outlet_slots)
         self.base = np.array(info.base[: q + 1], dtype=np.int64)
         self._has_split = bool(info.has_split)
         self._n_interior = int(info.n_interior)

@@ -26,7 +26,10 @@ FLUID = 0
 NOSLIP = 1
 UBB = 2
 EXCHANGE = 3
-TAG_NAMES = {FLUID: "fluid", NOSLIP: "noslip", UBB: "ubb", EXCHANGE: "exchange"}
+# extension beyond the reference (no outlet there): fixed-density
+# outlet cell; its prescribed density is stored in ubb_u[..., 0]
+OUTLET = 4
+TAG_NAMES = {FLUID: "fluid", NOSLIP: "noslip", UBB: "ubb", EXCHANGE: "exchange", OUTLET: "outlet"}
 
 
 class FaceKind(Enum):
@@ -37,8 +40,12 @@ class FaceKind(Enum):
 
 @dataclass(frozen=True)
 class FaceSpec:
+    """A face: WALL (resting, or moving with ``velocity`` -> UBB inlet, or
+    with ``density`` -> fixed-density OUTLET) or PERIODIC."""
+
     kind: FaceKind
     velocity: tuple[float, ...] | None = None
+    density: float | None = None
 
 
 WALL = FaceSpec(FaceKind.WALL)
@@ -116,9 +123,19 @@ class FlagField:
 
 
 def _wall_tag(spec: FaceSpec) -> int:
+    if spec.density is not None:
+        return OUTLET
     if spec.velocity is not None and any(float(v) != 0.0 for v in spec.velocity):
         return UBB
     return NOSLIP
+
+
+def _face_value(spec: FaceSpec, nd: int):
+    """per-cell payload painted with a wall face: UBB velocity, or the
+    OUTLET density in component 0"""
+    if spec.density is not None:
+        return np.array([float(spec.density)] + [0.0] * (nd - 1))
+    return 0.0 if spec.velocity is None else np.asarray(spec.velocity, np.float64)
 
 
 def _check_faces(dims, faces):
@@ -131,6 +148,8 @@ def _check_faces(dims, faces):
         for spec in (lo, hi):
             if spec.kind is FaceKind.EXCHANGE:
                 raise errors.make("ConfigurationError", "exchange faces only arise from partitioning")
+            if spec.density is not None and (spec.kind is not FaceKind.WALL or spec.velocity is not None):
+                raise errors.make("ConfigurationError", "density is only valid on resting wall faces")
             if spec.velocity is not None:
                 if spec.kind is not FaceKind.WALL:
                     raise errors.make("ConfigurationError", "velocity is only valid on wall faces")
@@ -161,7 +180,7 @@ def make_flags(dims, faces, solid: np.ndarray | None = None) -> FlagField:
 
     padded = tuple(n + 2 for n in shape)
     tags = np.zeros(padded, dtype=np.uint8)
-    moving = any(_wall_tag(s) == UBB for pair in faces for s in pair)
+    moving = any(_wall_tag(s) in (UBB, OUTLET) for pair in faces for s in pair)
     if moving:
         vel = np.zeros(padded + (nd,), dtype=np.float64)
     else:
@@ -198,11 +217,11 @@ def make_flags(dims, faces, solid: np.ndarray | None = None) -> FlagField:
             tags[tuple(dst_lo)] = _wall_tag(lo)
             tags[tuple(dst_hi)] = _wall_tag(hi)
             if moving:
-                vel[tuple(dst_lo)] = 0.0 if lo.velocity is None else np.asarray(lo.velocity, np.float64)
-                vel[tuple(dst_hi)] = 0.0 if hi.velocity is None else np.asarray(hi.velocity, np.float64)
+                vel[tuple(dst_lo)] = _face_value(lo, nd)
+                vel[tuple(dst_hi)] = _face_value(hi, nd)
         lo_idx[arr_axis] = 0
         hi_idx[arr_axis] = n + 2
     if moving:
-        vel[tags != UBB] = 0.0
+        vel[(tags != UBB) & (tags != OUTLET)] = 0.0
     periodic = tuple(faces[a][0].kind is FaceKind.PERIODIC for a in range(nd))
     return FlagField(dims=dims, tags=tags, ubb_u=vel, periodic=periodic)
