@@ -491,7 +491,7 @@ int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
   SLBM_TRY(dalloc(e, &e->out_dir, e->n_out));
   SLBM_TRY(dalloc(e, &e->out_rho, e->n_out));
   SLBM_TRY(dalloc(e, &e->out_u, 3 * e->n_out));
-  SLBM_CUDA_TRY(cudaMemsetAsync(e->out_u, 0, 3 * std::max<int64_t>(e->n_out, 1) * sizeof(double), s));
+  if (e->n_out) SLBM_CUDA_TRY(cudaMemsetAsync(e->out_u, 0, 3 * e->n_out * sizeof(double), s));
   for (int q = 1; q < d.q; ++q) {
     if (!e->n_out_q[q]) continue;
     int64_t cnt = 0;
