@@ -203,6 +203,14 @@ int slbm_nccl_comm_destroy(void* comm);
 int slbm_voxelize_spheres(const int32_t* dims, const double* centers, int64_t n,
                           double diameter, int device, uint8_t* solid);
 
+/* CUDA graph capture of arbitrary engine / halo work issued on `stream`
+ * (e.g. one AA step pair of a whole multi-block domain incl. NCCL): begin,
+ * issue the work through the other entry points, end -> executable graph. */
+int slbm_capture_begin(void* stream);
+int slbm_capture_end(void* stream, void** graph_exec);
+int slbm_graph_launch(void* graph_exec, void* stream);
+int slbm_graph_destroy(void* graph_exec);
+
 /* kernel-variant knobs for tuning experiments: knob 0 = index-list sweep
  * variant, knob 1 = cell-local sweep variant (0 = default)                 */
 int slbm_set_tuning(int knob, int value);

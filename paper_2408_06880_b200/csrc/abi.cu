@@ -126,6 +126,36 @@ const char* slbm_version(void) { return "slbm_b200 0.1 sm_100a"; }
 
 int slbm_set_tuning(int knob, int value) { return set_tuning(knob, value); }
 
+int slbm_capture_begin(void* stream) {
+  if (!stream) return fail(SLBM_ECONFIG, "capture needs a non-default stream");
+  SLBM_CUDA_TRY(cudaStreamBeginCapture((cudaStream_t)stream, cudaStreamCaptureModeThreadLocal));
+  return SLBM_OK;
+}
+
+int slbm_capture_end(void* stream, void** graph_exec) {
+  if (!stream || !graph_exec) return fail(SLBM_ECONFIG, "null argument");
+  cudaGraph_t graph = nullptr;
+  SLBM_CUDA_TRY(cudaStreamEndCapture((cudaStream_t)stream, &graph));
+  cudaGraphExec_t exec = nullptr;
+  cudaError_t err = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (err != cudaSuccess)
+    return fail(SLBM_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(err));
+  *graph_exec = (void*)exec;
+  return SLBM_OK;
+}
+
+int slbm_graph_launch(void* graph_exec, void* stream) {
+  if (!graph_exec) return fail(SLBM_ECONFIG, "null graph");
+  SLBM_CUDA_TRY(cudaGraphLaunch((cudaGraphExec_t)graph_exec, (cudaStream_t)stream));
+  return SLBM_OK;
+}
+
+int slbm_graph_destroy(void* graph_exec) {
+  if (graph_exec) cudaGraphExecDestroy((cudaGraphExec_t)graph_exec);
+  return SLBM_OK;
+}
+
 int slbm_engine_create(const uint8_t* tags_pad, const double* ubb_u_pad, int dim,
                        const int32_t* dims, const uint8_t* periodic, int q, int model,
                        double omega, double lambda_odd, int pattern,

@@ -398,13 +398,57 @@ class Domain:
         for e in self.local_engines():
             e.finish_step()
 
-    def run(self, steps: int, driver: str = "sequential") -> None:
+    def run(self, steps: int, driver: str = "sequential", use_graph: bool = False) -> None:
+        """``steps`` time steps.  ``use_graph`` (check="deferred" only) captures
+        one step pair of the whole domain — halo program on the comm stream,
+        every block's refresh and sweeps, NCCL included — into a CUDA graph
+        and replays it, so many-block domains are not host-launch bound."""
         fn = self._driver(driver)
-        for _ in range(int(steps)):
+        steps = int(steps)
+        if use_graph and self.check == "deferred" and self._graph_capable():
+            while steps >= 2:
+                self._replay_pair(driver, fn)
+                steps -= 2
+        for _ in range(steps):
             fn()
             if self.check == "step":
                 self._poll_or_raise()
             self.steps_done += 1
+
+    def _graph_capable(self) -> bool:
+        return bool(self._stream) and isinstance(self._halo, DeviceHalo)
+
+    def _replay_pair(self, driver, fn):
+        from . import _abi
+        import ctypes as C
+
+        key = (driver, getattr(self.parity, "value", self.parity))
+        graphs = self.__dict__.setdefault("_graphs", {})
+        if key not in graphs:
+            engines = self.local_engines()
+            snap = [(e.counters.copy(), e.parity) for e in engines]
+            _abi.call("slbm_capture_begin", C.c_void_p(self._stream))
+            try:
+                fn()
+                fn()
+            finally:
+                exec_ = C.c_void_p()
+                _abi.call("slbm_capture_end", C.c_void_p(self._stream), C.byref(exec_))
+            deltas = []
+            for e, (c0, p0) in zip(engines, snap):
+                d = {k: v - getattr(c0, k) for k, v in e.counters.as_dict().items()}
+                deltas.append(d)
+                e.counters = c0
+                e.parity = p0
+            graphs[key] = (exec_, deltas)
+        exec_, deltas = graphs[key]
+        from . import _abi as abi
+
+        abi.call("slbm_graph_launch", exec_, C.c_void_p(self._stream))
+        for e, d in zip(self.local_engines(), deltas):
+            for k, v in d.items():
+                setattr(e.counters, k, getattr(e.counters, k) + v)
+        self.steps_done += 2
 
     def _driver(self, name: str):
         if name == "sequential":
@@ -626,8 +670,8 @@ class DistributedDomain(Domain):
         return cls(fl, (bx, by, bz), stencil, params, pattern="aa", frame_width=1, rank=rank,
                    world=world, device=device, assignment=assignment, transport=transport)
 
-    def run(self, steps: int, driver: str = "overlapped") -> None:
-        super().run(steps, driver)
+    def run(self, steps: int, driver: str = "overlapped", use_graph: bool = False) -> None:
+        super().run(steps, driver, use_graph)
 
 
 def _balance_without_engines(gf, block_size, stencil, n_workers):

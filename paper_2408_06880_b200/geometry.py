@@ -229,27 +229,28 @@ def read_voxel_mask(path) -> VoxelMask:
 # ---------------------------------------------------------------- vessel tree
 
 
-def artery_tree(dims, seed: int = 0, r_root: float = 20.0, r_min: float = 8.0,
-                levels: int = 5, device: int | None = None) -> np.ndarray:
-    """Fluid mask (True = fluid) of a branching tube tree inside ``dims``:
-    a root capsule enters at x = 0 and bifurcates ``levels`` times with
-    Murray-law radii (r_child = r / 2^(1/3)), clamped at ``r_min``.  New
-    geometry (no reference generator), deterministic in seed."""
+def artery_segments(dims, seed: int = 0, r_root: float = 20.0, r_min: float = 8.0,
+                    levels: int = 5):
+    """Capsule segments (p0, p1, radius) of a branching tube tree in the box
+    ``dims`` (public order): a root enters through the x = 0 face at the
+    centre of the y-z face, bifurcates ``levels`` times with Murray-law radii
+    (r / 2^(1/3), clamped at ``r_min``) at 25-45 degrees in random planes,
+    and the terminal branches run on until they leave the box.  New geometry
+    (the reference has no vessel generator); deterministic in ``seed``."""
     rng = np.random.default_rng(seed)
-    dims = tuple(int(d) for d in dims)
-    ext = np.asarray(dims, dtype=np.float64)
-    segs = []  # (p0, p1, radius)
-    start = np.array([0.0, ext[1] / 2, ext[2] / 2])
-    direction = np.array([1.0, 0.0, 0.0])
-    length = ext[0] / (levels + 1) * 1.3
-    stack = [(start, direction, r_root, 0)]
+    ext = np.asarray([float(d) for d in dims])
+    seg_len = ext[0] / (levels + 1.5)
+    segs = []
+    stack = [(np.array([-1.0, ext[1] / 2, ext[2] / 2]), np.array([1.0, 0.0, 0.0]), r_root, 0)]
     while stack:
         p0, d, r, lvl = stack.pop()
-        p1 = p0 + d * length * (0.85 ** lvl)
-        p1 = np.clip(p1, r, ext - r)
-        segs.append((p0, p1, r))
-        if lvl + 1 > levels:
+        if lvl == levels:
+            # terminal branch: continue straight until it exits the box
+            p1 = p0 + d * (2.0 * float(ext.max()))
+            segs.append((p0, p1, r))
             continue
+        p1 = p0 + d * seg_len * (0.9 ** lvl)
+        segs.append((p0, p1, r))
         rc = max(r / 2.0 ** (1.0 / 3.0), r_min)
         axis = rng.normal(size=3)
         axis -= axis.dot(d) * d
@@ -257,34 +258,60 @@ def artery_tree(dims, seed: int = 0, r_root: float = 20.0, r_min: float = 8.0,
         for sgn in (1.0, -1.0):
             ang = math.radians(rng.uniform(25.0, 45.0))
             nd = math.cos(ang) * d + sgn * math.sin(ang) * axis
+            nd[0] = max(nd[0], 0.35)  # keep the tree flowing towards +x
             nd /= np.linalg.norm(nd)
-            stack.append((p1, nd, rc, lvl + 1))
+            stack.append((p1.copy(), nd, rc, lvl + 1))
+    return segs
+
+
+def artery_tree(dims, seed: int = 0, **kw) -> np.ndarray:
+    """Fluid mask (True = fluid) over rev_shape(dims) of artery_segments:
+    a cell is fluid iff its centre lies within a segment's radius."""
+    dims = tuple(int(d) for d in dims)
     fluid = np.zeros(rev_shape(dims), dtype=bool)
-    zz, yy, xx = None, None, None
-    for p0, p1, r in segs:
-        lo = np.maximum(np.floor(np.minimum(p0, p1) - r - 1).astype(int), 0)
-        hi = np.minimum(np.ceil(np.maximum(p0, p1) + r + 1).astype(int), np.asarray(dims) - 1)
-        if np.any(hi < lo):
-            continue
-        zs = np.arange(lo[2], hi[2] + 1) + 0.5
-        ys = np.arange(lo[1], hi[1] + 1) + 0.5
-        xs = np.arange(lo[0], hi[0] + 1) + 0.5
-        zz, yy, xx = np.meshgrid(zs, ys, xs, indexing="ij")
-        pts = np.stack([xx, yy, zz], axis=-1)
+    hi_box = np.asarray(dims) - 1
+    for p0, p1, r in artery_segments(dims, seed, **kw):
         seg = p1 - p0
         L2 = float(seg.dot(seg)) or 1.0
-        tpar = np.clip(((pts - p0) @ seg) / L2, 0.0, 1.0)
-        near = p0 + tpar[..., None] * seg
-        d2 = ((pts - near) ** 2).sum(-1)
-        fluid[lo[2]:hi[2] + 1, lo[1]:hi[1] + 1, lo[0]:hi[0] + 1] |= d2 < r * r
+        lo = np.maximum(np.floor(np.minimum(p0, p1) - r - 1).astype(np.int64), 0)
+        hi = np.minimum(np.ceil(np.maximum(p0, p1) + r + 1).astype(np.int64), hi_box)
+        if np.any(hi < lo):
+            continue
+        # march along x in slabs; each slab only scans the y-z box the
+        # segment (plus radius) occupies inside that slab
+        step = 16
+        for x0 in range(int(lo[0]), int(hi[0]) + 1, step):
+            x1 = min(int(hi[0]), x0 + step - 1)
+            if abs(seg[0]) > 1e-9:
+                ta = np.clip((x0 - r - 1.0 - p0[0]) / seg[0], 0.0, 1.0)
+                tb = np.clip((x1 + 1.0 + r - p0[0]) / seg[0], 0.0, 1.0)
+                pa, pb = p0 + ta * seg, p0 + tb * seg
+                ylo = max(int(np.floor(min(pa[1], pb[1]) - r - 1)), int(lo[1]))
+                yhi = min(int(np.ceil(max(pa[1], pb[1]) + r + 1)), int(hi[1]))
+                zlo = max(int(np.floor(min(pa[2], pb[2]) - r - 1)), int(lo[2]))
+                zhi = min(int(np.ceil(max(pa[2], pb[2]) + r + 1)), int(hi[2]))
+            else:
+                ylo, yhi, zlo, zhi = int(lo[1]), int(hi[1]), int(lo[2]), int(hi[2])
+            if yhi < ylo or zhi < zlo:
+                continue
+            xs = np.arange(x0, x1 + 1) + 0.5
+            ys = np.arange(ylo, yhi + 1) + 0.5
+            zs = np.arange(zlo, zhi + 1) + 0.5
+            zz, yy, xx = np.meshgrid(zs, ys, xs, indexing="ij")
+            pts = np.stack([xx, yy, zz], axis=-1)
+            tpar = np.clip(((pts - p0) @ seg) / L2, 0.0, 1.0)
+            d2 = ((pts - (p0 + tpar[..., None] * seg)) ** 2).sum(-1)
+            fluid[zlo:zhi + 1, ylo:yhi + 1, x0:x1 + 1] |= d2 < r * r
     return fluid
 
 
-def artery_flags(dims, seed: int = 0, inlet_speed: float = 0.02, **kw):
-    """Walled box, tube tree fluid, UBB inlet on the x-low face (moving
-    wall pushing +x); the x-high face is a resting wall (the outlet
-    boundary is the next row)."""
+def artery_flags(dims, seed: int = 0, inlet_speed: float = 0.02, outlet_density: float = 1.0,
+                 **kw):
+    """Vessel-like benchmark geometry: tube-tree fluid in a solid box, UBB
+    velocity inlet on the x-low face, fixed-density outlets on the other five
+    faces (wherever a branch leaves the box)."""
     fluid = artery_tree(dims, seed=seed, **kw)
     inlet = FaceSpec(FaceKind.WALL, velocity=(float(inlet_speed), 0.0, 0.0))
-    faces = [(inlet, WALL), (WALL, WALL), (WALL, WALL)]
+    out = FaceSpec(FaceKind.WALL, density=float(outlet_density))
+    faces = [(inlet, out), (out, out), (out, out)]
     return make_flags(dims, faces, solid=~fluid)

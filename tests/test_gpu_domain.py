@@ -104,3 +104,33 @@ def test_driver_validation(gpu_lib):
         dom.run(1, driver="overlapped")
     with pytest.raises(errors.ConfigurationError, match="unknown driver"):
         dom.run(1, driver="sideways")
+
+
+@pytest.mark.parametrize("loopback", [False, True])
+@pytest.mark.parametrize("pattern", ["aa", "pull"])
+def test_graph_replay_matches_python_driver(pattern, loopback, gpu_lib):
+    """Domain.run(use_graph=True) (one captured step pair of the whole
+    domain, halo + all blocks, NCCL in loopback mode) == the Python driver."""
+    from paper_2408_06880_b200 import geometry
+    from paper_2408_06880_b200.collision import CollisionParams
+    from paper_2408_06880_b200.domain import Domain, DistributedDomain
+    from paper_2408_06880_b200.lattice import make_stencil
+
+    st = make_stencil("d3q19")
+    gf = geometry.riverbed_flags((24, 16, 16), (8, 8, 8), 0.5, 7, 0.03)
+    p = CollisionParams(1.4, "trt", 0.9)
+    doms = []
+    for use_graph in (False, True):
+        if loopback:
+            d = DistributedDomain(gf, (8, 8, 8), st, p, pattern=pattern, frame_width=1, rank=0,
+                                  world=1, device=0, loopback=True)
+        else:
+            d = Domain(gf, (8, 8, 8), st, p, pattern=pattern, frame_width=1, check="deferred")
+        d.init_random(3)
+        d.run(3, driver="overlapped")
+        d.run(8, driver="overlapped", use_graph=use_graph)
+        d.run(1, driver="overlapped")
+        doms.append(d)
+    np.testing.assert_array_equal(doms[0].gather_canonical(), doms[1].gather_canonical())
+    assert doms[0].counters().as_dict() == doms[1].counters().as_dict()
+    assert doms[0].steps_done == doms[1].steps_done == 12
