@@ -89,6 +89,33 @@ __global__ void __launch_bounds__(kBlock, MINB) k_aa_even(const SweepArgs a) {
   if (bad) flag_bad(a);
 }
 
+// block-size study of the register-resident sweep (tuning variants 13-17)
+template <class L, int MODEL, int BLOCK, int MINB, bool RELOAD>
+__global__ void __launch_bounds__(BLOCK, MINB) k_aa_even_b(const SweepArgs a) {
+  const uint32_t i = blockIdx.x * BLOCK + threadIdx.x;
+  if (i >= a.n_cells) return;
+  const uint32_t c = a.cids ? a.cids[i] : i;
+  uint32_t s[L::Q];
+  double t[L::Q];
+  s[0] = c;
+  if constexpr (RELOAD) {
+    sfor<1, L::Q>([&](auto q) { s[q] = ld_idx_keep(a.idx + size_t(q - 1) * a.n_fluid + c); });
+  } else {
+    sfor<1, L::Q>([&](auto q) { s[q] = __ldcs(a.idx + size_t(q - 1) * a.n_fluid + c); });
+  }
+  sfor<0, L::Q>([&](auto q) { t[q] = a.pdf[s[q]]; });
+  double* pdf = a.pdf;
+  const bool bad = collide<L, MODEL>(t, a.omega, a.lam, [&](auto q, double v) {
+    constexpr int qb = L::INV[decltype(q)::value];
+    if constexpr (RELOAD && qb != 0) {
+      pdf[ld_idx_again(a.idx + size_t(qb - 1) * a.n_fluid + c)] = v;
+    } else {
+      pdf[s[qb]] = v;
+    }
+  });
+  if (bad) flag_bad(a);
+}
+
 // ---- asynchronous-gather variant of the index-list sweep -------------------
 // The register-resident kernel above is latency bound (ncu r01: long
 // scoreboard 9 of 14 cycles/issue at 25% occupancy, 126 registers for 19
@@ -294,9 +321,19 @@ void launch_kind(int kind, const SweepArgs& a, unsigned grid, cudaStream_t s) {
         case 8: launch_pf<L, MODEL, 2>(a, grid, s); break;
         case 9: launch_pf<L, MODEL, 1>(a, grid, s); break;
         case 10: launch_pf<L, MODEL, 3>(a, grid, s); break;
+        case 13: k_aa_even<L, MODEL, 2, true><<<grid, kBlock, 0, s>>>(a); break;
+        case 14: k_aa_even_b<L, MODEL, 320, 2, false><<<(a.n_cells + 319) / 320, 320, 0, s>>>(a); break;
+        case 15: k_aa_even_b<L, MODEL, 320, 2, true><<<(a.n_cells + 319) / 320, 320, 0, s>>>(a); break;
+        case 16: k_aa_even_b<L, MODEL, 128, 4, false><<<(a.n_cells + 127) / 128, 128, 0, s>>>(a); break;
+        case 17: k_aa_even_b<L, MODEL, 288, 2, false><<<(a.n_cells + 287) / 288, 288, 0, s>>>(a); break;
         case 11: k_probe<L, 0><<<grid, kBlock, 0, s>>>(a); break;
         case 12: k_probe<L, 1><<<grid, kBlock, 0, s>>>(a); break;
-        default: k_aa_even<L, MODEL, 2, false><<<grid, kBlock, 0, s>>>(a); break;
+        case 18: k_aa_even<L, MODEL, 2, false><<<grid, kBlock, 0, s>>>(a); break;
+        // default: 128-thread CTAs, 4 per SM (same 16 warps/SM as 256 x 2 at
+        // <= 128 registers, finer scheduling; +2% measured, profiles/)
+        default:
+          k_aa_even_b<L, MODEL, 128, 4, false><<<(a.n_cells + 127) / 128, 128, 0, s>>>(a);
+          break;
       }
     }
   } else {
