@@ -78,7 +78,7 @@ void free_engine(SlbmEngine* e) {
                   e->cid_map,     e->ubb_slot,     e->ubb_partner, e->ubb_corr,
                   e->ghost_key,   e->interior_cids, e->frame_cids, e->d_bad,
                   e->out_slot,    e->out_partner,  e->out_cell,  e->out_dir,
-                  e->out_rho,     e->out_u,
+                  e->out_rho,     e->out_u,        e->idx_aos,
                   e->d_step,      e->d_scratch};
   for (void* p : ptrs)
     if (p) cudaFree(p);

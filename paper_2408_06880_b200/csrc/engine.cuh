@@ -27,6 +27,7 @@ struct SlbmEngine {
   double* pdf = nullptr;   // active buffer
   double* tmp = nullptr;   // pull: second buffer
   uint32_t* idx = nullptr;  // (q-1) x n_fluid
+  uint32_t* idx_aos = nullptr;  // optional cell-major copy (tuning variant)
   uint32_t* x_flat = nullptr;  // cid -> padded flat
   int32_t* cid_map = nullptr;  // padded flat -> cid or -1
   uint32_t* ubb_slot = nullptr;

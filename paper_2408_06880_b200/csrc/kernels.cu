@@ -35,6 +35,7 @@ struct SweepArgs {
   double omega, lam;
   unsigned long long* bad;
   const unsigned long long* step;
+  const uint32_t* idx_aos;  // optional cell-major index list (tuning)
 };
 
 namespace {
@@ -112,6 +113,43 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_aa_even_b(const SweepArgs a) {
     } else {
       pdf[s[qb]] = v;
     }
+  });
+  if (bad) flag_bad(a);
+}
+
+// cell-major ("AoS") copy of the index list: cell c's Q-1 slot ids are
+// contiguous (padded to a multiple of 4 for 16-byte loads), so a warp reads
+// one contiguous 2.5 KB run instead of Q-1 separate 128-byte rows
+template <int QM1P>
+__global__ void k_idx_to_aos(const uint32_t* idx, uint32_t n, int qm1, uint32_t* out) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  for (int q = 0; q < QM1P; ++q) out[size_t(c) * QM1P + q] = q < qm1 ? idx[size_t(q) * n + c] : 0u;
+}
+
+template <class L, int MODEL, int BLOCK, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB) k_aa_even_aos(const SweepArgs a,
+                                                             const uint32_t* __restrict__ aos) {
+  constexpr int QP = ((L::Q - 1) + 3) / 4 * 4;
+  const uint32_t i = blockIdx.x * BLOCK + threadIdx.x;
+  if (i >= a.n_cells) return;
+  const uint32_t c = a.cids ? a.cids[i] : i;
+  uint32_t s[QP + 1];
+  s[0] = c;
+  const uint4* row = reinterpret_cast<const uint4*>(aos + size_t(c) * QP);
+  sfor<0, QP / 4>([&](auto k) {
+    const uint4 v = __ldcs(row + k);
+    s[1 + 4 * k] = v.x;
+    s[2 + 4 * k] = v.y;
+    s[3 + 4 * k] = v.z;
+    s[4 + 4 * k] = v.w;
+  });
+  double t[L::Q];
+  sfor<0, L::Q>([&](auto q) { t[q] = a.pdf[s[q]]; });
+  double* pdf = a.pdf;
+  const bool bad = collide<L, MODEL>(t, a.omega, a.lam, [&](auto q, double v) {
+    constexpr int qb = L::INV[decltype(q)::value];
+    pdf[s[qb]] = v;
   });
   if (bad) flag_bad(a);
 }
@@ -322,6 +360,9 @@ void launch_kind(int kind, const SweepArgs& a, unsigned grid, cudaStream_t s) {
         case 9: launch_pf<L, MODEL, 1>(a, grid, s); break;
         case 10: launch_pf<L, MODEL, 3>(a, grid, s); break;
         case 13: k_aa_even<L, MODEL, 2, true><<<grid, kBlock, 0, s>>>(a); break;
+        case 19:
+          k_aa_even_aos<L, MODEL, 128, 4><<<(a.n_cells + 127) / 128, 128, 0, s>>>(a, a.idx_aos);
+          break;
         case 14: k_aa_even_b<L, MODEL, 320, 2, false><<<(a.n_cells + 319) / 320, 320, 0, s>>>(a); break;
         case 15: k_aa_even_b<L, MODEL, 320, 2, true><<<(a.n_cells + 319) / 320, 320, 0, s>>>(a); break;
         case 16: k_aa_even_b<L, MODEL, 128, 4, false><<<(a.n_cells + 127) / 128, 128, 0, s>>>(a); break;
@@ -567,6 +608,19 @@ int launch_step(SlbmEngine* e, int phase) {
   if (a.n_cells == 0) return SLBM_OK;
   const int kind = e->pattern == SLBM_PULL ? kPull : (e->parity == SLBM_EVEN ? kEven : kOdd);
   const unsigned grid = grid_for(a.n_cells, kBlock);
+  if (kind == kEven && g_even_variant == 19 && e->q != 9) {
+    if (!e->idx_aos) {  // lazily built cell-major copy of the index list
+      const int qp = ((e->q - 1) + 3) / 4 * 4;
+      SLBM_CUDA_TRY(cudaMalloc(&e->idx_aos, size_t(e->n_fluid) * qp * sizeof(uint32_t)));
+      if (e->q == 19)
+        k_idx_to_aos<20><<<grid_for(e->n_fluid, 256), 256, 0, e->stream>>>(
+            e->idx, uint32_t(e->n_fluid), e->q - 1, e->idx_aos);
+      else
+        k_idx_to_aos<28><<<grid_for(e->n_fluid, 256), 256, 0, e->stream>>>(
+            e->idx, uint32_t(e->n_fluid), e->q - 1, e->idx_aos);
+    }
+    a.idx_aos = e->idx_aos;
+  }
   by_lattice(e->q, [&](auto lat) {
     launch_model<decltype(lat)>(e->model, kind, a, grid, e->stream);
   });
