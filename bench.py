@@ -283,22 +283,42 @@ def impl_ours(args, rank, world, local_rank):
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
     clocks.mark("t0")
-    ev0.record(stream)
-    runner.run(steps, **run_kw)
-    ev1.record(stream)
-    runner.synchronize()
+    if world == 1:
+        # one CUDA event after every step on the engine's stream: the total
+        # gives `value`, consecutive pairs give each sweep kernel's duration
+        # live inside the timed region (the roofline's denominator)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+        parities = []
+        evs[0].record(stream)
+        for k in range(steps):
+            parities.append(eng.parity.value)
+            eng.refresh_boundary(eng.parity)
+            eng.step()
+            eng.finish_step()
+            evs[k + 1].record(stream)
+        evs[-1].synchronize()
+        ms = evs[0].elapsed_time(evs[-1])
+        per = [evs[k].elapsed_time(evs[k + 1]) for k in range(steps)]
+        t_even = statistics.mean(p for p, par in zip(per, parities) if par == 0)
+        t_odd = statistics.mean(p for p, par in zip(per, parities) if par == 1)
+    else:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        runner.run(steps, **run_kw)
+        ev1.record(stream)
+        runner.synchronize()
+        ms = ev0.elapsed_time(ev1)
     torch.cuda.synchronize()
     clocks.mark("t1")
-    ms = reduce(ev0.elapsed_time(ev1))
+    ms = reduce(ms)
     if dist is not None:
         dist.barrier()
     runner.poll()
-
-    # per-kernel roofline (index-list sweep = dominant kernel)
-    t_even, t_odd = time_kernels(eng, torch)
+    if world > 1:
+        # per-kernel durations from a short separate sequence of sweeps
+        t_even, t_odd = time_kernels(eng, torch)
     clocks.stop()
     csum = clocks.summary()
 
@@ -358,7 +378,10 @@ def impl_ours(args, rank, world, local_rank):
         },
         "roofline": {
             "bound": "hbm",
-            "kernel": "k_aa_even<D3Q19,TRT> (index-list AA sweep)",
+            "kernel": "k_aa_even_b<D3Q19,TRT,128,4> (index-list AA sweep)",
+            "timing": ("CUDA events after every step inside the timed region (mean over the "
+                       "index-list steps)" if world == 1 else
+                       "CUDA events around individual sweeps after the timed region"),
             "achieved": round(ach_even, 1),
             "peak": hbm,
             "unit": "GB/s",
