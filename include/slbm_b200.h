@@ -71,6 +71,7 @@ typedef struct SlbmInfo {
   int64_t n_ghost_q[27];
   int64_t device_bytes;  /* bytes of device memory held by the engine */
   int64_t n_outlet_slots; /* fixed-density outlet reads (extension, tag 4) */
+  int64_t layout;         /* 0 sparse (index list), 1 dense (direct addressing) */
 } SlbmInfo;
 
 /* ---- construction: SparseEngine.__init__ (sparse.py:51-93) ----------------
@@ -90,6 +91,13 @@ int slbm_engine_create(const uint8_t* tags_pad, const double* ubb_u_pad, int dim
                        const int32_t* dims, const uint8_t* periodic, int q, int model,
                        double omega, double lambda_odd, int pattern,
                        const int32_t* frame_width, int device, SlbmEngine** out);
+/* direct-addressing block engine, the reference's DenseEngine (dense.py:52-342):
+ * same arguments; storage q-planes over the padded box, slot = q*npad + p,
+ * no index list; outlets unsupported.  Same entry points apply to it.      */
+int slbm_engine_create_dense(const uint8_t* tags_pad, const double* ubb_u_pad, int dim,
+                             const int32_t* dims, const uint8_t* periodic, int q, int model,
+                             double omega, double lambda_odd, int pattern,
+                             const int32_t* frame_width, int device, SlbmEngine** out);
 int slbm_engine_destroy(SlbmEngine* eng);
 int slbm_engine_info(const SlbmEngine* eng, SlbmInfo* info);
 /* cudaStream_t as void*; set_stream(NULL) restores the engine's own stream */

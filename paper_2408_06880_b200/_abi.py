@@ -42,6 +42,7 @@ class SlbmInfo(C.Structure):
         ("n_ghost_q", C.c_int64 * 27),
         ("device_bytes", C.c_int64),
         ("n_outlet_slots", C.c_int64),
+        ("layout", C.c_int64),
     ]
 
 
@@ -49,6 +50,8 @@ class SlbmInfo(C.Structure):
 SIGNATURES = {
     "slbm_engine_create": [c_u8p, c_dp, C.c_int, c_i32p, c_u8p, C.c_int, C.c_int, C.c_double,
                            C.c_double, C.c_int, c_i32p, C.c_int, C.POINTER(vp)],
+    "slbm_engine_create_dense": [c_u8p, c_dp, C.c_int, c_i32p, c_u8p, C.c_int, C.c_int,
+                                 C.c_double, C.c_double, C.c_int, c_i32p, C.c_int, C.POINTER(vp)],
     "slbm_engine_destroy": [vp],
     "slbm_engine_info": [vp, C.POINTER(SlbmInfo)],
     "slbm_engine_stream": [vp, C.POINTER(vp)],

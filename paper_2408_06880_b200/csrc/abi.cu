@@ -78,7 +78,8 @@ void free_engine(SlbmEngine* e) {
                   e->cid_map,     e->ubb_slot,     e->ubb_partner, e->ubb_corr,
                   e->ghost_key,   e->interior_cids, e->frame_cids, e->d_bad,
                   e->out_slot,    e->out_partner,  e->out_cell,  e->out_dir,
-                  e->out_rho,     e->out_u,        e->idx_aos,
+                  e->out_rho,     e->out_u,        e->idx_aos,   e->dense_mask,
+                  e->dense_ubb_key, e->dense_ubb_corr,
                   e->d_step,      e->d_scratch};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -107,6 +108,19 @@ int upload_slots(SlbmEngine* e, const int64_t* slots, int64_t n, uint32_t** dev)
   SLBM_CUDA_TRY(cudaMallocAsync(dev, s32.size() * sizeof(uint32_t), e->stream));
   SLBM_CUDA_TRY(cudaMemcpyAsync(*dev, s32.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice,
                                 e->stream));
+  return SLBM_OK;
+}
+
+// dense slot of (q, padded cell): q * npad + p, halo cells included
+// (dense.py:311-322); no fluid check, like the reference
+int dense_slots(const SlbmEngine* e, const int64_t* qs, const int64_t* pflat, int64_t n,
+                int64_t* out) {
+  const int64_t npad = e->geo.n_padded();
+  for (int64_t i = 0; i < n; ++i) {
+    if (qs[i] < 0 || qs[i] >= e->q || pflat[i] < 0 || pflat[i] >= npad)
+      return fail(SLBM_EPROTOCOL, "dense slot outside the padded block");
+    out[i] = qs[i] * npad + pflat[i];
+  }
   return SLBM_OK;
 }
 
@@ -156,10 +170,10 @@ int slbm_graph_destroy(void* graph_exec) {
   return SLBM_OK;
 }
 
-int slbm_engine_create(const uint8_t* tags_pad, const double* ubb_u_pad, int dim,
-                       const int32_t* dims, const uint8_t* periodic, int q, int model,
-                       double omega, double lambda_odd, int pattern,
-                       const int32_t* frame_width, int device, SlbmEngine** out) {
+static int create_engine(int layout, const uint8_t* tags_pad, const double* ubb_u_pad, int dim,
+                         const int32_t* dims, const uint8_t* periodic, int q, int model,
+                         double omega, double lambda_odd, int pattern,
+                         const int32_t* frame_width, int device, SlbmEngine** out) {
   if (!out || !tags_pad || !dims || !periodic) return fail(SLBM_ECONFIG, "null argument");
   *out = nullptr;
   if (pattern != SLBM_PULL && pattern != SLBM_AA)
@@ -200,7 +214,14 @@ int slbm_engine_create(const uint8_t* tags_pad, const double* ubb_u_pad, int dim
     return fail(SLBM_ECUDA, std::string("stream create: ") + cudaGetErrorString(err));
   }
   e->stream = e->own_stream;
-  int st = build_lists(e, tags_pad, ubb_u_pad, frame_width);
+  e->layout = layout;
+  int st = SLBM_OK;
+  if (layout == 0) {
+    st = build_lists(e, tags_pad, ubb_u_pad, frame_width);
+  } else {
+    st = enumerate_fluid(e, tags_pad);
+    if (st == SLBM_OK) st = build_dense(e, tags_pad, ubb_u_pad, frame_width);
+  }
   if (st != SLBM_OK) {
     std::string msg = last_error();
     free_engine(e);
@@ -240,6 +261,22 @@ int slbm_engine_create(const uint8_t* tags_pad, const double* ubb_u_pad, int dim
   return SLBM_OK;
 }
 
+int slbm_engine_create(const uint8_t* tags_pad, const double* ubb_u_pad, int dim,
+                       const int32_t* dims, const uint8_t* periodic, int q, int model,
+                       double omega, double lambda_odd, int pattern,
+                       const int32_t* frame_width, int device, SlbmEngine** out) {
+  return create_engine(0, tags_pad, ubb_u_pad, dim, dims, periodic, q, model, omega, lambda_odd,
+                       pattern, frame_width, device, out);
+}
+
+int slbm_engine_create_dense(const uint8_t* tags_pad, const double* ubb_u_pad, int dim,
+                             const int32_t* dims, const uint8_t* periodic, int q, int model,
+                             double omega, double lambda_odd, int pattern,
+                             const int32_t* frame_width, int device, SlbmEngine** out) {
+  return create_engine(1, tags_pad, ubb_u_pad, dim, dims, periodic, q, model, omega, lambda_odd,
+                       pattern, frame_width, device, out);
+}
+
 int slbm_engine_destroy(SlbmEngine* e) {
   free_engine(e);
   return SLBM_OK;
@@ -260,6 +297,7 @@ int slbm_engine_info(const SlbmEngine* e, SlbmInfo* info) {
   info->n_ubb_slots = e->n_ubb;
   info->n_ghost_slots = e->n_ghost;
   info->n_outlet_slots = e->n_out;
+  info->layout = e->layout;
   info->n_interior = e->has_split ? e->n_interior : e->n_fluid;
   info->n_frame = e->has_split ? e->n_frame : 0;
   for (int q = 0; q <= e->q; ++q) info->base[q] = e->base[q];
@@ -304,6 +342,7 @@ int slbm_export_lists(const SlbmEngine* e, uint32_t* idx, int64_t* fluid_coords,
   DeviceGuard guard(e->device);
   cudaStream_t s = e->stream;
   const int64_t n = e->n_fluid;
+  if (idx && e->layout) return fail(SLBM_ECONFIG, "a dense engine has no index list");
   if (idx)
     SLBM_CUDA_TRY(cudaMemcpyAsync(idx, e->idx, size_t(e->q - 1) * n * sizeof(uint32_t),
                                   cudaMemcpyDeviceToHost, s));
@@ -369,6 +408,13 @@ int slbm_export_split(const SlbmEngine* e, int64_t* interior, int64_t* frame) {
 int slbm_init_canonical_dev(SlbmEngine* e, const double* dev_values) {
   CHECK_ENGINE(e);
   DeviceGuard guard(e->device);
+  if (e->layout) {  // dense.py:196-210
+    SLBM_TRY(e->ensure_scratch(size_t(e->q) * e->n_fluid * sizeof(double)));
+    SLBM_CUDA_TRY(cudaMemcpyAsync(e->d_scratch, dev_values,
+                                  size_t(e->q) * e->n_fluid * sizeof(double), cudaMemcpyDefault,
+                                  e->stream));
+    return dense_init(e, e->d_scratch);
+  }
   // sparse.py:205-210: poison everything, then write the Q direction groups
   SLBM_TRY(launch_fill(e->pdf, e->total_slots, NAN, e->stream));
   if (e->tmp) SLBM_TRY(launch_fill(e->tmp, e->total_slots, NAN, e->stream));
@@ -394,11 +440,19 @@ int slbm_init_equilibrium(SlbmEngine* e, const double* rho, int rho_scalar, cons
   DeviceGuard guard(e->device);
   const size_t nr = rho_scalar ? 1 : size_t(e->n_fluid);
   const size_t nu = u_scalar ? size_t(e->dim) : size_t(e->dim) * e->n_fluid;
-  SLBM_TRY(e->ensure_scratch((nr + nu) * sizeof(double)));
+  const size_t nq = e->layout ? size_t(e->q) * e->n_fluid : 0;
+  SLBM_TRY(e->ensure_scratch((nr + nu + nq) * sizeof(double)));
   double* d_rho = e->d_scratch;
   double* d_u = e->d_scratch + nr;
   SLBM_CUDA_TRY(cudaMemcpyAsync(d_rho, rho, nr * sizeof(double), cudaMemcpyHostToDevice, e->stream));
   SLBM_CUDA_TRY(cudaMemcpyAsync(d_u, u, nu * sizeof(double), cudaMemcpyHostToDevice, e->stream));
+  if (e->layout) {
+    double* d_f = e->d_scratch + nr + nu;
+    SLBM_TRY(launch_equilibrium_qn(e, d_rho, rho_scalar, d_u, u_scalar, d_f));
+    SLBM_TRY(dense_init(e, d_f));
+    SLBM_CUDA_TRY(cudaStreamSynchronize(e->stream));
+    return SLBM_OK;
+  }
   SLBM_TRY(launch_fill(e->pdf, e->total_slots, NAN, e->stream));
   if (e->tmp) SLBM_TRY(launch_fill(e->tmp, e->total_slots, NAN, e->stream));
   SLBM_TRY(launch_equilibrium(e, d_rho, rho_scalar, d_u, u_scalar, nullptr));
@@ -411,6 +465,14 @@ int slbm_canonical_state(SlbmEngine* e, double* values) {
   CHECK_ENGINE(e);
   if (!values) return fail(SLBM_ECONFIG, "null values");
   DeviceGuard guard(e->device);
+  if (e->layout) {  // dense.py:275-288
+    SLBM_TRY(e->ensure_scratch(size_t(e->q) * e->n_fluid * sizeof(double)));
+    SLBM_TRY(dense_canonical(e, e->d_scratch));
+    SLBM_CUDA_TRY(cudaMemcpyAsync(values, e->d_scratch, size_t(e->q) * e->n_fluid * sizeof(double),
+                                  cudaMemcpyDeviceToHost, e->stream));
+    SLBM_CUDA_TRY(cudaStreamSynchronize(e->stream));
+    return SLBM_OK;
+  }
   const bool odd = e->pattern == SLBM_AA && e->parity == SLBM_ODD;
   if (odd) SLBM_TRY(launch_refresh(e, SLBM_ODD));  // sparse.py:317
   for (int r = 0; r < e->q; ++r) {
@@ -429,12 +491,20 @@ int slbm_macroscopic(SlbmEngine* e, double* rho, double* u) {
   const bool odd = e->pattern == SLBM_AA && e->parity == SLBM_ODD;
   if (odd) SLBM_TRY(launch_refresh(e, SLBM_ODD));
   const int64_t cells = e->geo.n_cells();
-  SLBM_TRY(e->ensure_scratch(size_t(cells) * (1 + e->dim) * sizeof(double)));
+  const size_t nq = e->layout ? size_t(e->q) * e->n_fluid : 0;
+  SLBM_TRY(e->ensure_scratch((size_t(cells) * (1 + e->dim) + nq) * sizeof(double)));
   double* d_rho = e->d_scratch;
   double* d_u = e->d_scratch + cells;
   SLBM_CUDA_TRY(cudaMemsetAsync(e->d_scratch, 0, size_t(cells) * (1 + e->dim) * sizeof(double),
                                 e->stream));
-  int st = launch_macroscopic(e, nullptr, d_rho, d_u);
+  int st;
+  if (e->layout) {
+    double* d_f = e->d_scratch + size_t(cells) * (1 + e->dim);
+    SLBM_TRY(dense_canonical(e, d_f));
+    st = launch_macroscopic(e, d_f, d_rho, d_u);
+  } else {
+    st = launch_macroscopic(e, nullptr, d_rho, d_u);
+  }
   if (st != SLBM_OK) return st;
   SLBM_CUDA_TRY(cudaMemcpyAsync(rho, d_rho, cells * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
   SLBM_CUDA_TRY(cudaMemcpyAsync(u, d_u, cells * e->dim * sizeof(double), cudaMemcpyDeviceToHost,
@@ -448,10 +518,18 @@ int slbm_total_mass(SlbmEngine* e, double* mass) {
   DeviceGuard guard(e->device);
   const bool odd = e->pattern == SLBM_AA && e->parity == SLBM_ODD;
   if (odd) SLBM_TRY(launch_refresh(e, SLBM_ODD));
-  SLBM_TRY(e->ensure_scratch(size_t(e->q) * sizeof(double)));
-  for (int r = 0; r < e->q; ++r) {
-    const int g = odd ? e->dirs.inv[r] : r;
-    SLBM_TRY(launch_sum(e->pdf + e->base[g], e->n_fluid, e->d_scratch + r, e->stream));
+  const size_t nq = e->layout ? size_t(e->q) * e->n_fluid : 0;
+  SLBM_TRY(e->ensure_scratch((size_t(e->q) + nq) * sizeof(double)));
+  if (e->layout) {
+    double* d_f = e->d_scratch + e->q;
+    SLBM_TRY(dense_canonical(e, d_f));
+    for (int r = 0; r < e->q; ++r)
+      SLBM_TRY(launch_sum(d_f + size_t(r) * e->n_fluid, e->n_fluid, e->d_scratch + r, e->stream));
+  } else {
+    for (int r = 0; r < e->q; ++r) {
+      const int g = odd ? e->dirs.inv[r] : r;
+      SLBM_TRY(launch_sum(e->pdf + e->base[g], e->n_fluid, e->d_scratch + r, e->stream));
+    }
   }
   std::vector<double> parts(e->q);
   SLBM_CUDA_TRY(cudaMemcpyAsync(parts.data(), e->d_scratch, e->q * sizeof(double),
@@ -561,6 +639,7 @@ int slbm_slot_index(const SlbmEngine* ce, const int64_t* qs, const int64_t* pfla
                     int64_t* out) {
   CHECK_ENGINE(ce);
   if (n == 0) return SLBM_OK;
+  if (ce->layout) return dense_slots(ce, qs, pflat, n, out);
   SlbmEngine* e = const_cast<SlbmEngine*>(ce);
   DeviceGuard guard(e->device);
   int64_t* d = nullptr;
@@ -582,6 +661,7 @@ int slbm_slot_index(const SlbmEngine* ce, const int64_t* qs, const int64_t* pfla
 int slbm_ghost_slot_index(const SlbmEngine* e, const int64_t* qs, const int64_t* pflat,
                           int64_t n, int64_t* out) {
   CHECK_ENGINE(e);
+  if (e->layout) return dense_slots(e, qs, pflat, n, out);  // dense.py:319-322
   const Geometry& g = e->geo;
   for (int64_t i = 0; i < n; ++i) {
     const int64_t q = qs[i];

@@ -304,6 +304,37 @@ std::string dims_str(const Geometry& g) {
 
 }  // namespace
 
+// fluid cells in C order over (z, y, x) -> e->x_flat, e->n_fluid (dense engine)
+int enumerate_fluid(SlbmEngine* e, const uint8_t* tags_pad) {
+  const Geometry& g = e->geo;
+  cudaStream_t s = e->stream;
+  const int64_t n_pad = g.n_padded(), n_cells = g.n_cells();
+  if (n_pad >= (int64_t(1) << 32) - 1)
+    return fail(SLBM_ECONFIG, "padded block has >= 2^32 cells; use smaller blocks");
+  uint8_t* d_tags = nullptr;
+  uint32_t* sel = nullptr;
+  SLBM_CUDA_TRY(cudaMalloc(&d_tags, n_pad));
+  SLBM_CUDA_TRY(cudaMemcpyAsync(d_tags, tags_pad, n_pad, cudaMemcpyHostToDevice, s));
+  SLBM_CUDA_TRY(cudaMalloc(&sel, sizeof(uint32_t) * std::max<int64_t>(n_cells, 1)));
+  auto interior = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0),
+                                                  InteriorToPadded{g});
+  int64_t n_fluid = 0;
+  SLBM_TRY(select_if(interior, sel, n_cells, FluidAt{d_tags}, &n_fluid, s));
+  if (n_fluid == 0) {
+    cudaFree(sel);
+    cudaFree(d_tags);
+    return fail(SLBM_EEMPTY, "block " + dims_str(g) + " has no fluid cells");
+  }
+  e->n_fluid = n_fluid;
+  SLBM_TRY(dalloc(e, &e->x_flat, n_fluid));
+  SLBM_CUDA_TRY(cudaMemcpyAsync(e->x_flat, sel, n_fluid * sizeof(uint32_t),
+                                cudaMemcpyDeviceToDevice, s));
+  SLBM_CUDA_TRY(cudaStreamSynchronize(s));
+  cudaFree(sel);
+  cudaFree(d_tags);
+  return SLBM_OK;
+}
+
 int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
                 const int32_t* frame_width) {
   const Geometry& g = e->geo;

@@ -1,0 +1,420 @@
+// Direct-addressing ("dense") block engine on the GPU — SURVEY §8f1, the
+// reference's DenseEngine (pkg/src/slbm/dense.py).
+//
+// Storage is the reference's: one plane per direction over the padded block
+// box, slot(q, p) = q * npad + p for padded flat index p (dense.py:95-97,
+// :311-317), so halo plans address dense and sparse blocks alike and mixed
+// ("hybrid") decompositions exchange with the reference's wire formats.
+//
+// Instead of the reference's precomputed (Q, cells) gather table, every
+// read address is computed from the cell's coordinates: the neighbour slot
+// q*npad + p - stride(q) (periodic in-block wrap only on boundary cells), or
+// the cell's own opposite slot when the upwind cell is a wall — one 32-bit
+// fold mask per box cell (bit q) built once on the device.  Moving-wall
+// (UBB) folds add the reference's momentum term at the folded read and at
+// the folded write of the combined step (dense.py:263-279); their few
+// (cell, q) -> correction entries are found by binary search.  Solid cells
+// carry the sentinel mask and are skipped: their slots are never read by a
+// fluid cell, so fluid results are the same bits as the reference's full-box
+// sweep (and as the sparse engine's).
+//
+// Traffic per fluid cell: 2 Q x 8 B of PDFs + 4 B of mask, no index list
+// (D3Q19: 308 B vs 376 B for the sparse index-list step).
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "collide.cuh"
+#include "engine.cuh"
+
+namespace slbm {
+namespace {
+
+constexpr uint32_t kSolid = 0xffffffffu;
+constexpr uint32_t kHasUbb = 0x80000000u;
+constexpr uint8_t kFluidT = 0, kUbbT = 2, kExchT = 3, kOutT = 4;
+
+struct DenseArgs {
+  double* pdf;
+  double* dst;
+  const uint32_t* mask;     // per box cell
+  const uint64_t* ubb_key;  // sorted (box cell << 5 | q)
+  const double* ubb_corr;
+  int64_t n_ubb;
+  Geometry g;
+  int64_t npad;
+  int64_t stride[27];       // padded-flat offset of the upwind cell
+  int32_t frame_w[3];
+  int phase;                // SLBM_PHASE_*
+  double omega, lam;
+  unsigned long long* bad;
+  const unsigned long long* step;
+};
+
+__device__ __forceinline__ double ubb_corr_of(const DenseArgs& a, uint32_t cell, int q) {
+  const uint64_t key = (uint64_t(cell) << 5) | uint64_t(q);
+  int64_t lo = 0, hi = a.n_ubb;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (a.ubb_key[mid] < key)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return (lo < a.n_ubb && a.ubb_key[lo] == key) ? a.ubb_corr[lo] : 0.0;
+}
+
+// padded flat index of the cell a direction-q read of (x, y, z) comes from,
+// with in-block periodic wrap (dense.py:126-131)
+template <class L, int Q_>
+__device__ __forceinline__ int64_t upwind_p(const DenseArgs& a, int64_t p, int64_t x, int64_t y,
+                                            int64_t z) {
+  constexpr int cx = L::CX[Q_], cy = L::CY[Q_], cz = L::CZ[Q_];
+  int64_t sx = x - cx, sy = y - cy, sz = z - cz;
+  bool wrap = false;
+  if (a.g.periodic[0] && (sx < 0 || sx >= a.g.n[0])) {
+    sx = sx < 0 ? sx + a.g.n[0] : sx - a.g.n[0];
+    wrap = true;
+  }
+  if (a.g.periodic[1] && (sy < 0 || sy >= a.g.n[1])) {
+    sy = sy < 0 ? sy + a.g.n[1] : sy - a.g.n[1];
+    wrap = true;
+  }
+  if (L::DIM == 3 && a.g.periodic[2] && (sz < 0 || sz >= a.g.n[2])) {
+    sz = sz < 0 ? sz + a.g.n[2] : sz - a.g.n[2];
+    wrap = true;
+  }
+  return wrap ? a.g.padded_flat(sx, sy, sz) : p - a.stride[Q_];
+}
+
+__device__ __forceinline__ bool in_phase(const DenseArgs& a, int64_t x, int64_t y, int64_t z) {
+  if (a.phase == SLBM_PHASE_ALL) return true;
+  const int64_t v[3] = {x, y, z};
+  bool frame = false;
+  for (int k = 0; k < a.g.dim; ++k)
+    frame |= (v[k] < a.frame_w[k]) || (v[k] >= a.g.n[k] - a.frame_w[k]);
+  return (a.phase == SLBM_PHASE_FRAME) == frame;
+}
+
+// KIND 0 pull, 1 combined (AA even), 2 reversed (AA odd)
+template <class L, int MODEL, int KIND>
+__global__ void __launch_bounds__(128, 4) k_dense(const DenseArgs a) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= a.g.n_cells()) return;
+  const uint32_t m = a.mask[i];
+  if (m == kSolid) return;
+  const int64_t x = i % a.g.n[0];
+  const int64_t r = i / a.g.n[0];
+  const int64_t y = r % a.g.n[1];
+  const int64_t z = r / a.g.n[1];
+  if (!in_phase(a, x, y, z)) return;
+  const int64_t p = a.g.padded_flat(x, y, z);
+  double* pdf = a.pdf;
+  double t[L::Q];
+  bool bad;
+  if constexpr (KIND == 2) {
+    sfor<0, L::Q>([&](auto q) {
+      constexpr int qb = L::INV[q];
+      t[q] = pdf[qb * a.npad + p];
+    });
+    bad = collide<L, MODEL>(t, a.omega, a.lam,
+                            [&](auto q, double v) { pdf[decltype(q)::value * a.npad + p] = v; });
+  } else {
+    int64_t addr[L::Q];
+    addr[0] = p;
+    sfor<1, L::Q>([&](auto q) {
+      constexpr int qb = L::INV[q];
+      addr[q] = (m >> q) & 1u ? qb * a.npad + p : q * a.npad + upwind_p<L, q>(a, p, x, y, z);
+    });
+    sfor<0, L::Q>([&](auto q) { t[q] = pdf[addr[q]]; });
+    if (m & kHasUbb) {
+      sfor<1, L::Q>([&](auto q) {
+        if ((m >> q) & 1u) t[q] += ubb_corr_of(a, uint32_t(i), q);
+      });
+    }
+    if constexpr (KIND == 1) {
+      bad = collide<L, MODEL>(t, a.omega, a.lam, [&](auto q, double v) {
+        constexpr int qb = L::INV[decltype(q)::value];
+        // out[q] lands at the read location of direction inv q; a folded
+        // moving-wall read adds its term at that write too (dense.py:269-279)
+        if constexpr (qb != 0) {
+          if ((m & kHasUbb) && ((m >> qb) & 1u)) v = v + ubb_corr_of(a, uint32_t(i), qb);
+        }
+        pdf[addr[qb]] = v;
+      });
+    } else {
+      double* dst = a.dst;
+      bad = collide<L, MODEL>(t, a.omega, a.lam,
+                              [&](auto q, double v) { dst[decltype(q)::value * a.npad + p] = v; });
+    }
+  }
+  if (bad) atomicMin(a.bad, *a.step);
+}
+
+// fold mask per box cell and the number of UBB folds (for the entry list)
+__global__ void k_dense_mask(const uint8_t* tags, Geometry g, DirTable d, uint32_t* mask,
+                             unsigned long long* n_ubb, int* err) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= g.n_cells()) return;
+  const int64_t x = i % g.n[0];
+  const int64_t r = i / g.n[0];
+  const int64_t y = r % g.n[1];
+  const int64_t z = r / g.n[1];
+  const uint8_t here = tags[g.padded_flat(x, y, z)];
+  if (here != kFluidT) {
+    mask[i] = kSolid;
+    return;
+  }
+  uint32_t m = 0;
+  unsigned nu = 0;
+  for (int q = 1; q < d.q; ++q) {
+    int64_t s[3] = {x - d.c[q][0], y - d.c[q][1], z - d.c[q][2]};
+    for (int k = 0; k < 3; ++k)
+      if (g.periodic[k]) s[k] = ((s[k] % g.n[k]) + g.n[k]) % g.n[k];
+    const uint8_t tag = tags[g.padded_flat(s[0], s[1], s[2])];
+    if (tag == kFluidT || tag == kExchT) continue;
+    if (tag == kOutT) atomicOr(err, 1);
+    m |= 1u << q;
+    if (tag == kUbbT) {
+      m |= kHasUbb;
+      ++nu;
+    }
+  }
+  mask[i] = m;
+  if (nu) atomicAdd(n_ubb, (unsigned long long)nu);
+}
+
+__global__ void k_dense_ubb(const uint8_t* tags, Geometry g, DirTable d, const uint32_t* mask,
+                            const uint32_t* wall_flat, const double* wall_u, int64_t n_wall,
+                            unsigned long long* pos, uint64_t* keys, double* corr) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= g.n_cells()) return;
+  const uint32_t m = mask[i];
+  if (m == kSolid || !(m & kHasUbb)) return;
+  const int64_t x = i % g.n[0];
+  const int64_t r = i / g.n[0];
+  const int64_t y = r % g.n[1];
+  const int64_t z = r / g.n[1];
+  for (int q = 1; q < d.q; ++q) {
+    int64_t s[3] = {x - d.c[q][0], y - d.c[q][1], z - d.c[q][2]};
+    for (int k = 0; k < 3; ++k)
+      if (g.periodic[k]) s[k] = ((s[k] % g.n[k]) + g.n[k]) % g.n[k];
+    const int64_t sp = g.padded_flat(s[0], s[1], s[2]);
+    if (tags[sp] != kUbbT) continue;
+    int64_t lo = 0, hi = n_wall;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (int64_t(wall_flat[mid]) < sp)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    // core.py:173-188
+    double cu = 0.0;
+    for (int k = 0; k < g.dim; ++k) {
+      if (d.c[q][k] == 1) cu = cu + wall_u[lo * 3 + k];
+      if (d.c[q][k] == -1) cu = cu - wall_u[lo * 3 + k];
+    }
+    const unsigned long long at = atomicAdd(pos, 1ull);
+    keys[at] = (uint64_t(i) << 5) | uint64_t(q);
+    corr[at] = (((2.0 * d.w[q]) * 1.0) * cu) / (1.0 / 3.0);
+  }
+}
+
+// resting weights in every box cell's slots (dense.py:208-209)
+__global__ void k_dense_weights(double* pdf, Geometry g, int64_t npad, DirTable d) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= g.n_cells()) return;
+  const int64_t x = i % g.n[0];
+  const int64_t r = i / g.n[0];
+  const int64_t p = g.padded_flat(x, r % g.n[1], r / g.n[1]);
+  for (int q = 0; q < d.q; ++q) pdf[q * npad + p] = d.w[q];
+}
+
+// fluid-cell values <-> planes.  dir_map[q] = plane read for output row q
+__global__ void k_dense_scatter(double* pdf, const uint32_t* x_flat, int64_t n, int64_t npad,
+                                int q_count, const double* values) {
+  const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  for (int q = 0; q < q_count; ++q) pdf[q * npad + x_flat[c]] = values[q * n + c];
+}
+
+__global__ void k_dense_gather(const double* pdf, const uint32_t* x_flat, int64_t n, int64_t npad,
+                               DirTable d, int odd, double* values) {
+  const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  for (int q = 0; q < d.q; ++q) values[q * n + c] = pdf[(odd ? d.inv[q] : q) * npad + x_flat[c]];
+}
+
+inline unsigned grid_of(int64_t n, int b) { return unsigned(std::max<int64_t>((n + b - 1) / b, 1)); }
+
+template <class F>
+void with_lattice(int q, F&& f) {
+  if (q == 9)
+    f(LatD2Q9{});
+  else if (q == 19)
+    f(LatD3Q19{});
+  else
+    f(LatD3Q27{});
+}
+
+DenseArgs dense_args(SlbmEngine* e) {
+  DenseArgs a{};
+  a.pdf = e->pdf;
+  a.dst = e->tmp;
+  a.mask = e->dense_mask;
+  a.ubb_key = e->dense_ubb_key;
+  a.ubb_corr = e->dense_ubb_corr;
+  a.n_ubb = e->n_dense_ubb;
+  a.g = e->geo;
+  a.npad = e->geo.n_padded();
+  for (int q = 0; q < e->q; ++q)
+    a.stride[q] = (int64_t(e->dirs.c[q][2]) * e->geo.p[1] + e->dirs.c[q][1]) * e->geo.p[0] +
+                  e->dirs.c[q][0];
+  for (int k = 0; k < 3; ++k) a.frame_w[k] = e->dense_frame_w[k];
+  a.phase = SLBM_PHASE_ALL;
+  a.omega = e->omega;
+  a.lam = e->lambda_odd;
+  a.bad = e->d_bad;
+  a.step = e->d_step;
+  return a;
+}
+
+}  // namespace
+
+int build_dense(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
+                const int32_t* frame_width) {
+  const Geometry& g = e->geo;
+  cudaStream_t s = e->stream;
+  const int64_t n_pad = g.n_padded(), cells = g.n_cells();
+  std::vector<uint32_t> wall_flat;
+  std::vector<double> wall_u;
+  for (int64_t p = 0; p < n_pad; ++p) {
+    if (tags_pad[p] != kUbbT) continue;
+    if (!ubb_u_pad) return fail(SLBM_ECONFIG, "UBB tags present but no wall velocity array");
+    wall_flat.push_back(uint32_t(p));
+    for (int a = 0; a < 3; ++a) wall_u.push_back(a < g.dim ? ubb_u_pad[p * g.dim + a] : 0.0);
+  }
+  uint8_t* d_tags = nullptr;
+  SLBM_CUDA_TRY(cudaMalloc(&d_tags, n_pad));
+  SLBM_CUDA_TRY(cudaMemcpyAsync(d_tags, tags_pad, n_pad, cudaMemcpyHostToDevice, s));
+  SLBM_CUDA_TRY(cudaMalloc(&e->dense_mask, cells * sizeof(uint32_t)));
+  e->device_bytes += cells * 4;
+  unsigned long long* d_cnt = nullptr;
+  int* d_err = nullptr;
+  SLBM_CUDA_TRY(cudaMalloc(&d_cnt, 2 * sizeof(unsigned long long)));
+  SLBM_CUDA_TRY(cudaMalloc(&d_err, sizeof(int)));
+  SLBM_CUDA_TRY(cudaMemsetAsync(d_cnt, 0, 2 * sizeof(unsigned long long), s));
+  SLBM_CUDA_TRY(cudaMemsetAsync(d_err, 0, sizeof(int), s));
+  k_dense_mask<<<grid_of(cells, 256), 256, 0, s>>>(d_tags, g, e->dirs, e->dense_mask, d_cnt,
+                                                    d_err);
+  unsigned long long n_ubb = 0;
+  int h_err = 0;
+  SLBM_CUDA_TRY(cudaMemcpyAsync(&n_ubb, d_cnt, sizeof(n_ubb), cudaMemcpyDeviceToHost, s));
+  SLBM_CUDA_TRY(cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SLBM_CUDA_TRY(cudaStreamSynchronize(s));
+  if (h_err) {
+    cudaFree(d_tags);
+    return fail(SLBM_ECONFIG, "outlet boundaries are not supported by the dense engine");
+  }
+  e->n_dense_ubb = int64_t(n_ubb);
+  if (n_ubb) {
+    uint32_t* d_wf = nullptr;
+    double* d_wu = nullptr;
+    uint64_t* keys = nullptr;
+    double* corr = nullptr;
+    SLBM_CUDA_TRY(cudaMalloc(&d_wf, wall_flat.size() * 4));
+    SLBM_CUDA_TRY(cudaMalloc(&d_wu, wall_u.size() * 8));
+    SLBM_CUDA_TRY(cudaMemcpyAsync(d_wf, wall_flat.data(), wall_flat.size() * 4,
+                                  cudaMemcpyHostToDevice, s));
+    SLBM_CUDA_TRY(cudaMemcpyAsync(d_wu, wall_u.data(), wall_u.size() * 8, cudaMemcpyHostToDevice, s));
+    SLBM_CUDA_TRY(cudaMalloc(&keys, n_ubb * 8));
+    SLBM_CUDA_TRY(cudaMalloc(&corr, n_ubb * 8));
+    SLBM_CUDA_TRY(cudaMalloc(&e->dense_ubb_key, n_ubb * 8));
+    SLBM_CUDA_TRY(cudaMalloc(&e->dense_ubb_corr, n_ubb * 8));
+    k_dense_ubb<<<grid_of(cells, 256), 256, 0, s>>>(d_tags, g, e->dirs, e->dense_mask, d_wf, d_wu,
+                                                     int64_t(wall_flat.size()), d_cnt + 1, keys,
+                                                     corr);
+    size_t tmp_bytes = 0;
+    SLBM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, e->dense_ubb_key, corr,
+                                                  e->dense_ubb_corr, int64_t(n_ubb), 0, 64, s));
+    void* tmp = nullptr;
+    SLBM_CUDA_TRY(cudaMalloc(&tmp, tmp_bytes));
+    SLBM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, e->dense_ubb_key, corr,
+                                                  e->dense_ubb_corr, int64_t(n_ubb), 0, 64, s));
+    SLBM_CUDA_TRY(cudaStreamSynchronize(s));
+    cudaFree(tmp);
+    cudaFree(keys);
+    cudaFree(corr);
+    cudaFree(d_wf);
+    cudaFree(d_wu);
+  }
+  if (frame_width) {
+    for (int k = 0; k < 3; ++k)
+      e->dense_frame_w[k] = k < g.dim ? std::min<int32_t>(frame_width[k], g.n[k]) : 1;
+    // interior / frame sizes in box cells (dense.py:330-341)
+    int64_t inner = 1;
+    for (int k = 0; k < g.dim; ++k) inner *= std::max<int64_t>(g.n[k] - 2 * e->dense_frame_w[k], 0);
+    e->n_interior = inner;
+    e->n_frame = cells - inner;
+    e->has_split = true;
+  }
+  cudaFree(d_cnt);
+  cudaFree(d_err);
+  cudaFree(d_tags);
+  e->total_slots = int64_t(e->q) * n_pad;
+  return SLBM_OK;
+}
+
+int dense_step(SlbmEngine* e, int phase) {
+  DenseArgs a = dense_args(e);
+  a.phase = phase;
+  const int kind = e->pattern == SLBM_PULL ? 0 : (e->parity == SLBM_EVEN ? 1 : 2);
+  const unsigned grid = grid_of(e->geo.n_cells(), 128);
+  with_lattice(e->q, [&](auto lat) {
+    using L = decltype(lat);
+    auto go = [&](auto model) {
+      constexpr int M = decltype(model)::value;
+      if (kind == 0)
+        k_dense<L, M, 0><<<grid, 128, 0, e->stream>>>(a);
+      else if (kind == 1)
+        k_dense<L, M, 1><<<grid, 128, 0, e->stream>>>(a);
+      else
+        k_dense<L, M, 2><<<grid, 128, 0, e->stream>>>(a);
+    };
+    if (e->model == SLBM_SRT)
+      go(std::integral_constant<int, SLBM_SRT>{});
+    else if (e->model == SLBM_TRT)
+      go(std::integral_constant<int, SLBM_TRT>{});
+    else if constexpr (L::Q == 27)
+      go(std::integral_constant<int, SLBM_CUMULANT>{});
+  });
+  SLBM_CUDA_TRY(cudaGetLastError());
+  return SLBM_OK;
+}
+
+// init: NaN everywhere, resting weights in every box cell, values at fluid
+int dense_init(SlbmEngine* e, const double* dev_values) {
+  const int64_t npad = e->geo.n_padded();
+  SLBM_TRY(launch_fill(e->pdf, e->total_slots, NAN, e->stream));
+  if (e->tmp) SLBM_TRY(launch_fill(e->tmp, e->total_slots, NAN, e->stream));
+  k_dense_weights<<<grid_of(e->geo.n_cells(), 256), 256, 0, e->stream>>>(e->pdf, e->geo, npad,
+                                                                          e->dirs);
+  k_dense_scatter<<<grid_of(e->n_fluid, 256), 256, 0, e->stream>>>(e->pdf, e->x_flat, e->n_fluid,
+                                                                    npad, e->q, dev_values);
+  SLBM_CUDA_TRY(cudaGetLastError());
+  e->parity = SLBM_EVEN;
+  return SLBM_OK;
+}
+
+int dense_canonical(SlbmEngine* e, double* dev_values) {
+  const int odd = (e->pattern == SLBM_AA && e->parity == SLBM_ODD) ? 1 : 0;
+  k_dense_gather<<<grid_of(e->n_fluid, 256), 256, 0, e->stream>>>(
+      e->pdf, e->x_flat, e->n_fluid, e->geo.n_padded(), e->dirs, odd, dev_values);
+  SLBM_CUDA_TRY(cudaGetLastError());
+  return SLBM_OK;
+}
+
+}  // namespace slbm

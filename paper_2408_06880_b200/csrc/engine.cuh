@@ -26,6 +26,12 @@ struct SlbmEngine {
   // device memory
   double* pdf = nullptr;   // active buffer
   double* tmp = nullptr;   // pull: second buffer
+  int layout = 0;  // 0 sparse (index list), 1 dense (direct addressing)
+  uint32_t* dense_mask = nullptr;       // per box cell fold mask (dense)
+  uint64_t* dense_ubb_key = nullptr;    // sorted (box cell << 5 | q)
+  double* dense_ubb_corr = nullptr;
+  int64_t n_dense_ubb = 0;
+  int32_t dense_frame_w[3] = {1, 1, 1};
   uint32_t* idx = nullptr;  // (q-1) x n_fluid
   uint32_t* idx_aos = nullptr;  // optional cell-major copy (tuning variant)
   uint32_t* x_flat = nullptr;  // cid -> padded flat
@@ -77,6 +83,8 @@ int launch_fill(double* p, int64_t n, double v, cudaStream_t s);
 int launch_equilibrium(SlbmEngine* e, const double* rho, int rho_scalar, const double* u,
                        int u_scalar, double* dev_out);
 int launch_sum(const double* p, int64_t n, double* dev_out, cudaStream_t s);
+int launch_equilibrium_qn(SlbmEngine* e, const double* rho, int rho_scalar, const double* u,
+                          int u_scalar, double* out);
 int launch_slot_lookup(SlbmEngine* e, const int64_t* d_qs, const int64_t* d_pflat, int64_t n,
                        int64_t* d_out, int* d_err);
 
@@ -85,5 +93,13 @@ int set_tuning(int knob, int value);
 // builder.cu
 int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
                 const int32_t* frame_width);
+int enumerate_fluid(SlbmEngine* e, const uint8_t* tags_pad);
+
+// dense.cu (direct-addressing engine)
+int build_dense(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
+                const int32_t* frame_width);
+int dense_step(SlbmEngine* e, int phase);
+int dense_init(SlbmEngine* e, const double* dev_values);
+int dense_canonical(SlbmEngine* e, double* dev_values);
 
 }  // namespace slbm

@@ -597,6 +597,7 @@ int launch_slot_lookup(SlbmEngine* e, const int64_t* d_qs, const int64_t* d_pfla
 }
 
 int launch_step(SlbmEngine* e, int phase) {
+  if (e->layout) return dense_step(e, phase);
   SweepArgs a = sweep_args(e);
   if (phase == SLBM_PHASE_INTERIOR) {
     a.cids = e->interior_cids;
@@ -653,15 +654,23 @@ int launch_advance(SlbmEngine* e) {
   return SLBM_OK;
 }
 
-int launch_macroscopic(SlbmEngine* e, const double* /*unused*/, double* dev_rho, double* dev_u) {
+// canonical: nullptr -> read the sparse groups of e->pdf at the current
+// parity; else a (q, n_fluid) canonical array (dense engine)
+int launch_macroscopic(SlbmEngine* e, const double* canonical, double* dev_rho, double* dev_u) {
   SweepArgs a = sweep_args(e);
+  const double* src = e->pdf;
+  int odd = (e->pattern == SLBM_AA && e->parity == SLBM_ODD) ? 1 : 0;
+  if (canonical) {
+    for (int q = 0; q < 28; ++q) a.base[q] = uint32_t(q) * uint32_t(e->n_fluid);
+    src = canonical;
+    odd = 0;
+  }
   int* bad = nullptr;
   SLBM_CUDA_TRY(cudaMallocAsync(&bad, sizeof(int), e->stream));
   SLBM_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int), e->stream));
-  const int odd = (e->pattern == SLBM_AA && e->parity == SLBM_ODD) ? 1 : 0;
   by_lattice(e->q, [&](auto lat) {
     using L = decltype(lat);
-    k_macro<L><<<grid_for(e->n_fluid, 256), 256, 0, e->stream>>>(e->pdf, a, odd, e->geo,
+    k_macro<L><<<grid_for(e->n_fluid, 256), 256, 0, e->stream>>>(src, a, odd, e->geo,
                                                                    e->x_flat, dev_rho, dev_u, bad);
   });
   int h_bad = 0;
@@ -679,6 +688,20 @@ int launch_equilibrium(SlbmEngine* e, const double* rho, int rho_scalar, const d
     using L = decltype(lat);
     k_equilibrium<L><<<grid_for(e->n_fluid, 256), 256, 0, e->stream>>>(e->pdf, a, rho,
                                                                          rho_scalar, u, u_scalar);
+  });
+  SLBM_CUDA_TRY(cudaGetLastError());
+  return SLBM_OK;
+}
+
+// equilibrium into a (q, n_fluid) array (dense engine init)
+int launch_equilibrium_qn(SlbmEngine* e, const double* rho, int rho_scalar, const double* u,
+                          int u_scalar, double* out) {
+  SweepArgs a = sweep_args(e);
+  for (int q = 0; q < 28; ++q) a.base[q] = uint32_t(q) * uint32_t(e->n_fluid);
+  by_lattice(e->q, [&](auto lat) {
+    using L = decltype(lat);
+    k_equilibrium<L><<<grid_for(e->n_fluid, 256), 256, 0, e->stream>>>(out, a, rho, rho_scalar,
+                                                                         u, u_scalar);
   });
   SLBM_CUDA_TRY(cudaGetLastError());
   return SLBM_OK;

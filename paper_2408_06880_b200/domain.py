@@ -16,8 +16,11 @@ blocks assigned to it, and exchanges cross-rank edges with NCCL send/recv
 (one message per peer per phase) on a comm stream that overlaps the
 interior sweep.
 
-Only the sparse layout is built in this tier (policy "sparse"); dense and
-hybrid blocks are the next row.
+Layout policies "sparse", "dense" and "hybrid" (dense at porosity >= phi_s)
+follow the reference (``domain.py:58-65``); dense blocks are
+:class:`~paper_2408_06880_b200.engine.DenseEngine` (direct addressing), and a
+dense sender ships its whole layer (reference wire format), of which the
+receiver stores the storable entries.
 """
 
 from __future__ import annotations
@@ -29,7 +32,7 @@ import numpy as np
 from . import errors
 from .collision import Parity
 from .counters import Counters
-from .engine import SparseEngine, default_device
+from .engine import DenseEngine, SparseEngine, default_device
 from .halo import DeviceHalo, EdgePlan, NcclComm, Phase, phase_for
 from .tags import EXCHANGE, FLUID, NOSLIP, FlagField, rev_shape
 
@@ -210,10 +213,6 @@ class Domain:
                  _assignment=None, _comm=None, engine_factory=None, halo_factory=None):
         if policy not in POLICIES:
             raise errors.make("ConfigurationError", f"unknown layout policy {policy!r}")
-        if policy != "sparse":
-            raise errors.make("ConfigurationError",
-                              f"layout policy {policy!r}: dense blocks are not built on the GPU "
-                              "in this tier (sparse only)")
         self.stencil, self.params, self.pattern = stencil, params, pattern
         self.policy, self.phi_s, self.frame_width = policy, phi_s, frame_width
         self.device = default_device() if device is None else int(device)
@@ -248,9 +247,11 @@ class Domain:
         make_engine = engine_factory or _cuda_engine
         for bid, blk in self.blocks.items():
             blk.rank = self.assignment.get(bid, 0)
+            # hybrid picks dense at or above phi_s (domain.py:58-65, :109-114)
+            blk.kind = classify_kind(blk.porosity, policy, phi_s)
             if blk.rank == self.rank:
                 blk.engine = make_engine(blk.flags, stencil, params, pattern, frame_width,
-                                         self.device)
+                                         self.device, blk.kind)
         engines = self.local_engines()
         self._stream = engines[0].stream() if engines and hasattr(engines[0], "stream") else 0
         for e in engines[1:]:
@@ -265,7 +266,7 @@ class Domain:
             if ba.rank != self.rank and bb.rank != self.rank:
                 continue
             self.edge_plans.append(EdgePlan(a, b, sigma, stencil, ba.flags, bb.flags, pattern,
-                                            ba.engine, bb.engine))
+                                            ba.engine, bb.engine, src_layout=ba.kind))
         self._comm = _comm
         self._halo = self._build_halo()
         self.overlap_samples: list[tuple[float, float]] = []
@@ -509,8 +510,12 @@ class Domain:
     # -- balancing --------------------------------------------------------------------
 
     def workload(self, bid: int) -> int:
-        """model.workload_sparse: Q x fluid cells"""
-        return self.stencil.q * self.blocks[bid].n_fluid
+        """model.workload_sparse / workload_dense: Q x fluid cells, or Q x box
+        cells for a dense block (domain.py:281-285)"""
+        blk = self.blocks[bid]
+        if blk.kind == "dense":
+            return self.stencil.q * blk.flags.cell_count()
+        return self.stencil.q * blk.n_fluid
 
     def curve_order(self) -> list[int]:
         return sorted(self.blocks, key=lambda b: (curve_key(self.blocks[b].grid_pos, self.grid), b))
@@ -523,9 +528,19 @@ class Domain:
         return {b: int(w) for b, w in zip(order, seats)}
 
 
-def _cuda_engine(flags, stencil, params, pattern, frame_width, device):
-    return SparseEngine(flags, stencil, params, pattern=pattern, frame_width=frame_width,
-                        device=device, check="deferred")
+def _cuda_engine(flags, stencil, params, pattern, frame_width, device, kind="sparse"):
+    cls = DenseEngine if kind == "dense" else SparseEngine
+    return cls(flags, stencil, params, pattern=pattern, frame_width=frame_width, device=device,
+               check="deferred")
+
+
+def classify_kind(porosity: float, policy: str, phi_s: float = DEFAULT_PHI_S) -> str:
+    """domain.py:58-65: hybrid is dense at or above phi_s (ties dense)."""
+    if policy == "hybrid":
+        return "dense" if porosity >= phi_s else "sparse"
+    if policy in ("sparse", "dense"):
+        return policy
+    raise errors.make("ConfigurationError", f"unknown layout policy {policy!r}")
 
 
 class HostStagedHalo:

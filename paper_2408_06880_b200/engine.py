@@ -62,6 +62,7 @@ def _widths(frame_width, dim):
 
 class SparseEngine:
     layout = "sparse"
+    _CREATE = "slbm_engine_create"
 
     def __init__(self, flags, stencil, params, pattern: str = "pull", frame_width=None,
                  device: int | None = None, check: str = "step"):
@@ -100,7 +101,7 @@ class SparseEngine:
         model, omega, lam = params_code(params)
         handle = C.c_void_p()
         _abi.call(
-            "slbm_engine_create",
+            self._CREATE,
             _abi.ptr(tags, C.c_uint8),
             _abi.ptr(ubb, C.c_double),
             dim,
@@ -389,3 +390,68 @@ class SparseEngine:
     @property
     def device_bytes(self) -> int:
         return int(self.info().device_bytes)
+
+
+class DenseEngine(SparseEngine):
+    """GPU direct-addressing engine: the reference's ``DenseEngine``
+    (``pkg/src/slbm/dense.py:52-342``), same protocol.  Storage is one
+    plane per direction over the padded box (slot = q * npad + p), reads are
+    computed from coordinates plus a per-cell wall-fold mask (no index list),
+    and the counters count box cells like the reference (dense.py:290-297).
+    Fluid results are bit-identical to :class:`SparseEngine`'s."""
+
+    layout = "dense"
+    _CREATE = "slbm_engine_create_dense"
+
+    @property
+    def idx(self):
+        raise AttributeError("a dense engine has no index list")
+
+    def _box_cells(self) -> int:
+        return int(np.prod(self.dims))
+
+    def _phase_cells(self, phase: str) -> int:
+        if phase == "all":
+            return self._box_cells()
+        if self._has_split and phase in ("interior", "frame"):
+            return self._n_interior if phase == "interior" else self._n_frame
+        raise errors.make(
+            "ConfigurationError", f"{phase!r} sweep needs split lists; build with frame_width"
+        )
+
+    def step(self, phase: str = "all") -> None:
+        cells = self._phase_cells(phase)
+        _abi.call("slbm_step", self._h, _PHASE_CODE[phase])
+        self.counters.record_sweep(phase, cells, self.stencil.q, False)
+        if self.check == "step":
+            self.poll()
+
+    def run(self, steps: int, use_graph: bool = True) -> None:
+        steps = int(steps)
+        if steps <= 0:
+            return
+        for _ in range(steps):
+            self.counters.record_sweep("all", self._box_cells(), self.stencil.q, False)
+            if self.pattern == "aa":
+                self.parity = self.parity.flipped()
+            self.counters.steps += 1
+        _abi.call("slbm_run", self._h, steps, 1 if use_graph else 0)
+        if self.check == "step":
+            self.poll()
+
+    def export_boundary_lists(self) -> dict:
+        raise errors.make("ConfigurationError", "a dense engine resolves walls in its fold mask")
+
+    def pdf_element_count(self) -> int:
+        return (2 if self.pattern == "pull" else 1) * self.stencil.q * self._box_cells()
+
+    def idx_element_count(self) -> int:
+        return 0
+
+    @property
+    def n_interior(self) -> int:
+        return self._n_interior if self._has_split else self._box_cells()
+
+    @property
+    def n_frame(self) -> int:
+        return self._n_frame if self._has_split else 0

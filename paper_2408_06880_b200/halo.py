@@ -89,14 +89,17 @@ def _tags_at(flags, coords) -> np.ndarray:
 class PhasePlan:
     __slots__ = ("subset", "n_full", "n_wire", "send_sel", "tgt_sel", "pos_from_full",
                  "pos_from_sparse", "sparse_in_full", "_send_cells", "_send_qs", "_tgt_cells",
-                 "_tgt_qs")
+                 "_tgt_qs", "n_msg", "take")
+    # n_msg / take: message length and stored positions for THIS edge's
+    # sender layout (whole layer for a dense sender, existing slots for a
+    # sparse one; exchange.py:203-207, :242-247)
 
 
 class EdgePlan:
     """exchange.py:125-219; engines may be None for the remote end."""
 
     def __init__(self, src_bid, dst_bid, sigma, stencil, src_flags, dst_flags, pattern,
-                 src_engine=None, dst_engine=None):
+                 src_engine=None, dst_engine=None, src_layout=None):
         for axis, t in enumerate(sigma):
             if t == 0 and src_flags.dims[axis] != dst_flags.dims[axis]:
                 raise errors.make("ConfigurationError", "adjacent blocks must share extents on in-face axes")
@@ -109,6 +112,9 @@ class EdgePlan:
         self.src_flags, self.dst_flags = src_flags, dst_flags
         self.src_engine, self.dst_engine = src_engine, dst_engine
         self.pattern = pattern
+        if src_layout is None:
+            src_layout = getattr(src_engine, "layout", "sparse")
+        self.src_layout = src_layout
         self.phases = {Phase.CANONICAL: self._build(Phase.CANONICAL)}
         if pattern == "aa":
             self.phases[Phase.REVERSED] = self._build(Phase.REVERSED)
@@ -154,15 +160,21 @@ class EdgePlan:
         pp.pos_from_full = np.nonzero(storable)[0]
         pp.pos_from_sparse = np.nonzero(storable[wire])[0]
         pp.sparse_in_full = np.nonzero(wire)[0]
-        pp._send_cells = ecells[wire] if canonical else eimg[wire]
-        pp._send_qs = eqs[wire]
+        if self.src_layout == "dense":
+            pp._send_cells = ecells if canonical else eimg
+            pp._send_qs = eqs
+            pp.n_msg, pp.take = n_full, pp.pos_from_full
+        else:
+            pp._send_cells = ecells[wire] if canonical else eimg[wire]
+            pp._send_qs = eqs[wire]
+            pp.n_msg, pp.take = pp.n_wire, pp.pos_from_sparse
         pp._tgt_cells = eimg[storable] if canonical else ecells[storable]
         pp._tgt_qs = eqs[storable]
         pp.send_sel = None
         pp.tgt_sel = None
         if self.src_engine is not None:
             lookup = self.src_engine.slot_index if canonical else self.src_engine.ghost_slot_index
-            pp.send_sel = lookup(pp._send_cells, pp._send_qs) if pp.n_wire else np.empty(0, np.int64)
+            pp.send_sel = lookup(pp._send_cells, pp._send_qs) if pp.n_msg else np.empty(0, np.int64)
         if self.dst_engine is not None:
             lookup = self.dst_engine.ghost_slot_index if canonical else self.dst_engine.slot_index
             pp.tgt_sel = (lookup(pp._tgt_cells, pp._tgt_qs) if pp._tgt_qs.size
@@ -197,7 +209,7 @@ class DeviceHalo:
             pass
 
     def add_local(self, phase: Phase, src, dst, pp: PhasePlan):
-        send, take, tgt = _i64(pp.send_sel), _i64(pp.pos_from_sparse), _i64(pp.tgt_sel)
+        send, take, tgt = _i64(pp.send_sel), _i64(pp.take), _i64(pp.tgt_sel)
         _abi.call("slbm_halo_add_local", self._h, phase.value, src.handle, dst.handle,
                   _abi.ptr(send, C.c_int64), send.size, _abi.ptr(take, C.c_int64),
                   _abi.ptr(tgt, C.c_int64), tgt.size)
@@ -209,9 +221,9 @@ class DeviceHalo:
                   _abi.ptr(send, C.c_int64), send.size)
 
     def add_recv(self, phase: Phase, dst, peer: int, pp: PhasePlan):
-        take, tgt = _i64(pp.pos_from_sparse), _i64(pp.tgt_sel)
+        take, tgt = _i64(pp.take), _i64(pp.tgt_sel)
         self.has_remote = True
-        _abi.call("slbm_halo_add_recv", self._h, phase.value, dst.handle, int(peer), pp.n_wire,
+        _abi.call("slbm_halo_add_recv", self._h, phase.value, dst.handle, int(peer), pp.n_msg,
                   _abi.ptr(take, C.c_int64), _abi.ptr(tgt, C.c_int64), tgt.size)
 
     def commit(self, nccl_comm: int | None = None):

@@ -30,14 +30,14 @@ class ProtocolHalo:
         self.recvs = {0: {}, 1: {}}
 
     def add_local(self, phase, src, dst, pp):
-        self.local[phase.value].append((src, dst, pp.send_sel, pp.pos_from_sparse, pp.tgt_sel))
+        self.local[phase.value].append((src, dst, pp.send_sel, pp.take, pp.tgt_sel))
 
     def add_send(self, phase, src, peer, pp):
         self.sends[phase.value].setdefault(peer, []).append((src, pp.send_sel))
 
     def add_recv(self, phase, dst, peer, pp):
         self.recvs[phase.value].setdefault(peer, []).append(
-            (dst, pp.n_wire, pp.pos_from_sparse, pp.tgt_sel))
+            (dst, pp.n_msg, pp.take, pp.tgt_sel))
 
     def commit(self, comm=None):
         pass
@@ -71,7 +71,7 @@ class ProtocolHalo:
         pass
 
 
-def _oracle_engine(flags, stencil, params, pattern, frame_width, device):
+def _oracle_engine(flags, stencil, params, pattern, frame_width, device, kind="sparse"):
     from oracle.sparse_ref import OracleSparseEngine
 
     return OracleSparseEngine(flags, stencil, params, pattern, frame_width=frame_width)
