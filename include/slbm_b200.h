@@ -211,6 +211,17 @@ int slbm_nccl_comm_destroy(void* comm);
 int slbm_voxelize_spheres(const int32_t* dims, const double* centers, int64_t n,
                           double diameter, int device, uint8_t* solid);
 
+/* ---- block groups: all sparse engines of one rank swept by
+ * one launch per phase (block table + CTA prefix), batched UBB refresh and
+ * step counters.  Engines must share stencil, collision, pattern, device
+ * and parity.  While grouped, drive the engines only through the group.   */
+typedef struct SlbmGroup SlbmGroup;
+int slbm_group_create(SlbmEngine** engines, int n, SlbmGroup** out);
+int slbm_group_destroy(SlbmGroup* group);
+int slbm_group_refresh(SlbmGroup* group, int parity, void* stream);
+int slbm_group_step(SlbmGroup* group, int phase, void* stream);
+int slbm_group_finish(SlbmGroup* group, void* stream);
+
 /* CUDA graph capture of arbitrary engine / halo work issued on `stream`
  * (e.g. one AA step pair of a whole multi-block domain incl. NCCL): begin,
  * issue the work through the other entry points, end -> executable graph. */

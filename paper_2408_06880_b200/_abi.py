@@ -95,6 +95,11 @@ SIGNATURES = {
     "slbm_nccl_comm_destroy": [vp],
     "slbm_voxelize_spheres": [c_i32p, c_dp, C.c_int64, C.c_double, C.c_int, c_u8p],
     "slbm_set_tuning": [C.c_int, C.c_int],
+    "slbm_group_create": [C.POINTER(vp), C.c_int, C.POINTER(vp)],
+    "slbm_group_destroy": [vp],
+    "slbm_group_refresh": [vp, C.c_int, vp],
+    "slbm_group_step": [vp, C.c_int, vp],
+    "slbm_group_finish": [vp, vp],
     "slbm_capture_begin": [vp],
     "slbm_capture_end": [vp, C.POINTER(vp)],
     "slbm_graph_launch": [vp, vp],

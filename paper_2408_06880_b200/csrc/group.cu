@@ -1,0 +1,325 @@
+// Batched block-table execution: every sparse engine a rank
+// owns is swept by ONE launch per phase instead of one per block.  The
+// reference only computes a block -> worker assignment (domain.py:302-325);
+// here the blocks of a worker actually execute together.
+//
+// A group holds, per engine and phase, the engine's SweepArgs in a device
+// table, and per phase the prefix sum of its CTA counts.  A CTA finds its
+// engine by binary search over that prefix, stages the engine's SweepArgs in
+// shared memory, and runs the same per-cell code as the single-engine sweep
+// (identical arithmetic -> identical bits).  UBB refresh, outlet refresh and
+// the step counters are batched the same way.  With the halo program this
+// makes one domain step O(1) launches, which a CUDA graph then replays.
+#include <algorithm>
+#include <vector>
+
+#include "collide.cuh"
+#include "engine.cuh"
+
+// per-engine sweep arguments of one phase, staged in shared memory by a CTA
+namespace slbm {
+struct GroupArgs {
+  double* pdf;
+  double* dst;
+  const uint32_t* idx;
+  const uint32_t* cids;
+  uint32_t n_cells;
+  uint32_t n_fluid;
+  uint32_t base[28];
+  unsigned long long* bad;
+  const unsigned long long* step;
+};
+}  // namespace slbm
+
+using namespace slbm;
+
+struct SlbmGroup {
+  int device = 0;
+  int q = 19, model = SLBM_SRT, pattern = SLBM_AA;
+  double omega = 1.0, lam = 1.0;
+  std::vector<SlbmEngine*> engines;
+  // tables[phase][flip] -> device array of GroupArgs (one per engine)
+  GroupArgs* table[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
+  uint32_t* cta_start[3] = {nullptr, nullptr, nullptr};
+  uint32_t n_cta[3] = {0, 0, 0};
+  // batched UBB program
+  uint16_t* ubb_eng = nullptr;
+  uint32_t *ubb_slot = nullptr, *ubb_partner = nullptr;
+  double* ubb_corr = nullptr;
+  int64_t n_ubb = 0;
+  unsigned long long** steps = nullptr;  // per engine d_step
+  int flip = 0;  // pull: which buffer of each engine is current
+  bool has_outlets = false;
+};
+
+namespace {
+
+constexpr int kGB = 128;
+
+__device__ __forceinline__ int find_engine(const uint32_t* start, int n, uint32_t cta) {
+  int lo = 0, hi = n;  // last e with start[e] <= cta
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (start[mid] <= cta)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+template <class L, int MODEL, int KIND>
+__global__ void __launch_bounds__(kGB, 4) k_group(const GroupArgs* table, const uint32_t* start,
+                                                  int n_eng, double omega, double lam) {
+  __shared__ GroupArgs a;
+  if (threadIdx.x == 0) a = table[find_engine(start, n_eng, blockIdx.x)];
+  __shared__ uint32_t first;
+  if (threadIdx.x == 0) first = start[find_engine(start, n_eng, blockIdx.x)];
+  __syncthreads();
+  const uint32_t i = (blockIdx.x - first) * kGB + threadIdx.x;
+  if (i >= a.n_cells) return;
+  const uint32_t c = a.cids ? a.cids[i] : i;
+  double t[L::Q];
+  double* pdf = a.pdf;
+  bool bad;
+  if constexpr (KIND == 2) {  // AA odd (sparse.py:273-282)
+    sfor<0, L::Q>([&](auto q) {
+      constexpr int qb = L::INV[q];
+      t[q] = pdf[a.base[qb] + c];
+    });
+    bad = collide<L, MODEL>(t, omega, lam,
+                            [&](auto q, double v) { pdf[a.base[decltype(q)::value] + c] = v; });
+  } else {
+    uint32_t s[L::Q];
+    s[0] = c;
+    sfor<1, L::Q>([&](auto q) { s[q] = __ldcs(a.idx + size_t(q - 1) * a.n_fluid + c); });
+    sfor<0, L::Q>([&](auto q) { t[q] = pdf[s[q]]; });
+    if constexpr (KIND == 1) {  // AA even (sparse.py:264-271)
+      bad = collide<L, MODEL>(t, omega, lam, [&](auto q, double v) {
+        constexpr int qb = L::INV[decltype(q)::value];
+        pdf[s[qb]] = v;
+      });
+    } else {  // pull (sparse.py:257-262)
+      double* dst = a.dst;
+      bad = collide<L, MODEL>(t, omega, lam,
+                              [&](auto q, double v) { dst[a.base[decltype(q)::value] + c] = v; });
+    }
+  }
+  if (bad) atomicMin(a.bad, *a.step);
+}
+
+__global__ void k_group_refresh(const GroupArgs* table, const uint16_t* eng, const uint32_t* slot,
+                                const uint32_t* partner, const double* corr, int64_t n,
+                                int parity) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double* pdf = table[eng[i]].pdf;
+  if (parity == SLBM_EVEN)
+    pdf[slot[i]] = pdf[partner[i]] + corr[i];
+  else
+    pdf[partner[i]] = pdf[slot[i]] + corr[i];
+}
+
+__global__ void k_group_advance(unsigned long long** steps, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) *steps[i] += 1;
+}
+
+template <class F>
+void on_lattice(int q, F&& f) {
+  if (q == 9)
+    f(LatD2Q9{});
+  else if (q == 19)
+    f(LatD3Q19{});
+  else
+    f(LatD3Q27{});
+}
+
+GroupArgs args_of(SlbmEngine* e, int phase, int flip) {
+  GroupArgs a{};
+  double* bufs[2] = {e->pdf, e->tmp};
+  a.pdf = e->pattern == SLBM_PULL ? bufs[flip] : e->pdf;
+  a.dst = e->pattern == SLBM_PULL ? bufs[1 - flip] : nullptr;
+  a.idx = e->idx;
+  a.n_fluid = uint32_t(e->n_fluid);
+  a.cids = phase == SLBM_PHASE_INTERIOR ? e->interior_cids
+                                        : (phase == SLBM_PHASE_FRAME ? e->frame_cids : nullptr);
+  a.n_cells = uint32_t(phase == SLBM_PHASE_INTERIOR ? e->n_interior
+                                                    : (phase == SLBM_PHASE_FRAME ? e->n_frame
+                                                                                 : e->n_fluid));
+  for (int q = 0; q <= e->q && q < 28; ++q) a.base[q] = uint32_t(e->base[q]);
+  a.bad = e->d_bad;
+  a.step = e->d_step;
+  return a;
+}
+
+}  // namespace
+
+extern "C" {
+
+int slbm_group_create(SlbmEngine** engines, int n, SlbmGroup** out) {
+  if (!engines || n < 1 || !out) return fail(SLBM_ECONFIG, "group needs engines");
+  SlbmEngine* e0 = engines[0];
+  for (int i = 0; i < n; ++i) {
+    SlbmEngine* e = engines[i];
+    if (!e) return fail(SLBM_ECONFIG, "null engine in group");
+    if (e->layout != 0) return fail(SLBM_ECONFIG, "block groups hold sparse engines only");
+    if (e->q != e0->q || e->model != e0->model || e->pattern != e0->pattern ||
+        e->omega != e0->omega || e->lambda_odd != e0->lambda_odd || e->device != e0->device ||
+        e->parity != e0->parity || e->has_split != e0->has_split)
+      return fail(SLBM_ECONFIG, "group engines must share stencil, collision, pattern, device "
+                                "and parity");
+  }
+  cudaSetDevice(e0->device);
+  SlbmGroup* g = new SlbmGroup();
+  g->device = e0->device;
+  g->q = e0->q;
+  g->model = e0->model;
+  g->pattern = e0->pattern;
+  g->omega = e0->omega;
+  g->lam = e0->lambda_odd;
+  g->engines.assign(engines, engines + n);
+  // pull: each engine's e->pdf is "current"; record the flip as 0
+  for (int phase = 0; phase < 3; ++phase) {
+    if (phase && !e0->has_split) continue;
+    std::vector<uint32_t> start(n + 1, 0);
+    for (int i = 0; i < n; ++i) {
+      const GroupArgs a = args_of(engines[i], phase, 0);
+      start[i + 1] = start[i] + (a.n_cells + kGB - 1) / kGB;
+    }
+    g->n_cta[phase] = start[n];
+    SLBM_CUDA_TRY(cudaMalloc(&g->cta_start[phase], (n + 1) * sizeof(uint32_t)));
+    SLBM_CUDA_TRY(cudaMemcpy(g->cta_start[phase], start.data(), (n + 1) * sizeof(uint32_t),
+                             cudaMemcpyHostToDevice));
+    for (int flip = 0; flip < 2; ++flip) {
+      std::vector<GroupArgs> tab(n);
+      for (int i = 0; i < n; ++i) tab[i] = args_of(engines[i], phase, flip);
+      SLBM_CUDA_TRY(cudaMalloc(&g->table[phase][flip], n * sizeof(GroupArgs)));
+      SLBM_CUDA_TRY(cudaMemcpy(g->table[phase][flip], tab.data(), n * sizeof(GroupArgs),
+                               cudaMemcpyHostToDevice));
+    }
+  }
+  // concatenated UBB program with engine ids
+  for (int i = 0; i < n; ++i) g->n_ubb += engines[i]->n_ubb;
+  for (int i = 0; i < n; ++i) g->has_outlets |= engines[i]->n_out > 0;
+  if (g->n_ubb) {
+    SLBM_CUDA_TRY(cudaMalloc(&g->ubb_eng, g->n_ubb * sizeof(uint16_t)));
+    SLBM_CUDA_TRY(cudaMalloc(&g->ubb_slot, g->n_ubb * sizeof(uint32_t)));
+    SLBM_CUDA_TRY(cudaMalloc(&g->ubb_partner, g->n_ubb * sizeof(uint32_t)));
+    SLBM_CUDA_TRY(cudaMalloc(&g->ubb_corr, g->n_ubb * sizeof(double)));
+    int64_t off = 0;
+    for (int i = 0; i < n; ++i) {
+      SlbmEngine* e = engines[i];
+      if (!e->n_ubb) continue;
+      std::vector<uint16_t> ids(e->n_ubb, uint16_t(i));
+      SLBM_CUDA_TRY(cudaMemcpy(g->ubb_eng + off, ids.data(), e->n_ubb * 2, cudaMemcpyHostToDevice));
+      SLBM_CUDA_TRY(cudaMemcpy(g->ubb_slot + off, e->ubb_slot, e->n_ubb * 4, cudaMemcpyDeviceToDevice));
+      SLBM_CUDA_TRY(
+          cudaMemcpy(g->ubb_partner + off, e->ubb_partner, e->n_ubb * 4, cudaMemcpyDeviceToDevice));
+      SLBM_CUDA_TRY(cudaMemcpy(g->ubb_corr + off, e->ubb_corr, e->n_ubb * 8, cudaMemcpyDeviceToDevice));
+      off += e->n_ubb;
+    }
+  }
+  std::vector<unsigned long long*> st(n);
+  for (int i = 0; i < n; ++i) st[i] = engines[i]->d_step;
+  SLBM_CUDA_TRY(cudaMalloc(&g->steps, n * sizeof(unsigned long long*)));
+  SLBM_CUDA_TRY(cudaMemcpy(g->steps, st.data(), n * sizeof(unsigned long long*),
+                           cudaMemcpyHostToDevice));
+  *out = g;
+  return SLBM_OK;
+}
+
+int slbm_group_destroy(SlbmGroup* g) {
+  if (!g) return SLBM_OK;
+  cudaSetDevice(g->device);
+  for (int p = 0; p < 3; ++p) {
+    for (int f = 0; f < 2; ++f)
+      if (g->table[p][f]) cudaFree(g->table[p][f]);
+    if (g->cta_start[p]) cudaFree(g->cta_start[p]);
+  }
+  void* ptrs[] = {g->ubb_eng, g->ubb_slot, g->ubb_partner, g->ubb_corr, g->steps};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete g;
+  return SLBM_OK;
+}
+
+// refresh_boundary of every engine (sparse.py:295-304), on `stream`
+int slbm_group_refresh(SlbmGroup* g, int parity, void* stream) {
+  if (!g) return fail(SLBM_ECONFIG, "null group");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (g->n_ubb) {
+    const int flip = g->pattern == SLBM_PULL ? g->flip : 0;
+    k_group_refresh<<<unsigned((g->n_ubb + 255) / 256), 256, 0, s>>>(
+        g->table[0][flip], g->ubb_eng, g->ubb_slot, g->ubb_partner, g->ubb_corr, g->n_ubb, parity);
+    SLBM_CUDA_TRY(cudaGetLastError());
+  }
+  if (g->has_outlets) {  // few outlet blocks: per-engine launches
+    for (SlbmEngine* e : g->engines) {
+      if (!e->n_out) continue;
+      cudaStream_t keep = e->stream;
+      e->stream = s;
+      const int n_ubb = int(e->n_ubb);
+      e->n_ubb = 0;  // UBB already done above
+      int st = launch_refresh(e, parity);
+      e->n_ubb = n_ubb;
+      e->stream = keep;
+      if (st != SLBM_OK) return st;
+    }
+  }
+  return SLBM_OK;
+}
+
+// one sweep of `phase` over every engine of the group, one launch
+int slbm_group_step(SlbmGroup* g, int phase, void* stream) {
+  if (!g) return fail(SLBM_ECONFIG, "null group");
+  if (phase < 0 || phase > 2 || !g->cta_start[phase])
+    return fail(SLBM_ECONFIG, "sweep needs split lists; build with frame_width");
+  if (!g->n_cta[phase]) return SLBM_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int parity = g->engines[0]->parity;
+  const int kind = g->pattern == SLBM_PULL ? 0 : (parity == SLBM_EVEN ? 1 : 2);
+  const int flip = g->pattern == SLBM_PULL ? g->flip : 0;
+  const GroupArgs* tab = g->table[phase][flip];
+  const int n = int(g->engines.size());
+  on_lattice(g->q, [&](auto lat) {
+    using L = decltype(lat);
+    auto go = [&](auto mc) {
+      constexpr int M = decltype(mc)::value;
+      if (kind == 0)
+        k_group<L, M, 0><<<g->n_cta[phase], kGB, 0, s>>>(tab, g->cta_start[phase], n, g->omega, g->lam);
+      else if (kind == 1)
+        k_group<L, M, 1><<<g->n_cta[phase], kGB, 0, s>>>(tab, g->cta_start[phase], n, g->omega, g->lam);
+      else
+        k_group<L, M, 2><<<g->n_cta[phase], kGB, 0, s>>>(tab, g->cta_start[phase], n, g->omega, g->lam);
+    };
+    if (g->model == SLBM_SRT)
+      go(std::integral_constant<int, SLBM_SRT>{});
+    else if (g->model == SLBM_TRT)
+      go(std::integral_constant<int, SLBM_TRT>{});
+    else if constexpr (L::Q == 27)
+      go(std::integral_constant<int, SLBM_CUMULANT>{});
+  });
+  SLBM_CUDA_TRY(cudaGetLastError());
+  return SLBM_OK;
+}
+
+// finish_step of every engine (sparse.py:243-249): host state flips, one
+// device kernel advances all step counters
+int slbm_group_finish(SlbmGroup* g, void* stream) {
+  if (!g) return fail(SLBM_ECONFIG, "null group");
+  for (SlbmEngine* e : g->engines) {
+    if (e->pattern == SLBM_PULL)
+      std::swap(e->pdf, e->tmp);
+    else
+      e->parity = 1 - e->parity;
+    e->steps_done += 1;
+  }
+  if (g->pattern == SLBM_PULL) g->flip ^= 1;
+  const int n = int(g->engines.size());
+  k_group_advance<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(g->steps, n);
+  SLBM_CUDA_TRY(cudaGetLastError());
+  return SLBM_OK;
+}
+
+}  // extern "C"

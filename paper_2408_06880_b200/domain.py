@@ -269,8 +269,17 @@ class Domain:
                                             ba.engine, bb.engine, src_layout=ba.kind))
         self._comm = _comm
         self._halo = self._build_halo()
+        self._group = self._build_group() if engine_factory is None else None
         self.overlap_samples: list[tuple[float, float]] = []
         self.steps_done = 0
+
+    def _build_group(self):
+        """Batched block-table execution when this rank owns
+        several sparse blocks: one launch per phase for all of them."""
+        engines = self.local_engines()
+        if len(engines) < 2 or any(getattr(e, "layout", "") != "sparse" for e in engines):
+            return None
+        return BlockGroup(engines)
 
     # -- construction ------------------------------------------------------------
 
@@ -370,8 +379,25 @@ class Domain:
                 src.engine.counters.messages += 1
 
     def _sweep(self, phase: str):
+        if self._group is not None:
+            self._group.step(phase, self._stream)
+            return
         for e in self.local_engines():
             e.step(phase)
+
+    def _refresh_all(self):
+        if self._group is not None:
+            self._group.refresh(self.parity, self._stream)
+            return
+        for e in self.local_engines():
+            e.refresh_boundary(e.parity)
+
+    def _finish_all(self):
+        if self._group is not None:
+            self._group.finish(self._stream)
+            return
+        for e in self.local_engines():
+            e.finish_step()
 
     def step_sequential(self) -> None:
         """exchange.py:330-346 on the device: exchange, then whole-block sweeps."""
@@ -379,11 +405,9 @@ class Domain:
         self._halo.start(phase, self._stream)
         self._halo.wait(self._stream)
         self._count_exchange(phase)
-        for e in self.local_engines():
-            e.refresh_boundary(e.parity)
+        self._refresh_all()
         self._sweep("all")
-        for e in self.local_engines():
-            e.finish_step()
+        self._finish_all()
 
     def step_overlapped(self) -> None:
         """exchange.py:349-374: pack/send/recv/unpack on the comm stream while
@@ -391,13 +415,11 @@ class Domain:
         phase = phase_for(self.pattern, self.parity)
         self._halo.start(phase, self._stream)
         self._count_exchange(phase)
-        for e in self.local_engines():
-            e.refresh_boundary(e.parity)
+        self._refresh_all()
         self._sweep("interior")
         self._halo.wait(self._stream)
         self._sweep("frame")
-        for e in self.local_engines():
-            e.finish_step()
+        self._finish_all()
 
     def run(self, steps: int, driver: str = "sequential", use_graph: bool = False) -> None:
         """``steps`` time steps.  ``use_graph`` (check="deferred" only) captures
@@ -526,6 +548,68 @@ class Domain:
         order = self.curve_order()
         seats = greedy_segments([self.workload(b) for b in order], n_workers)
         return {b: int(w) for b, w in zip(order, seats)}
+
+
+class BlockGroup:
+    """All sparse CUDA engines of one rank driven as one block table
+    (slbm_group_*): refresh, each sweep phase and finish are single
+    launches; the Python-side engine state (parity, counters) is advanced
+    exactly as the per-engine calls would."""
+
+    def __init__(self, engines):
+        import ctypes as C
+
+        from . import _abi
+
+        self.engines = list(engines)
+        arr = (C.c_void_p * len(self.engines))(*[e.handle.value for e in self.engines])
+        h = C.c_void_p()
+        _abi.call("slbm_group_create", arr, len(self.engines), C.byref(h))
+        self._h = h
+
+    def close(self):
+        from . import _abi
+
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _abi.load().slbm_group_destroy(self._h)
+        self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def refresh(self, parity, stream):
+        import ctypes as C
+
+        from . import _abi
+
+        _abi.call("slbm_group_refresh", self._h, int(getattr(parity, "value", parity)),
+                  C.c_void_p(stream or 0))
+
+    def step(self, phase: str, stream):
+        import ctypes as C
+
+        from . import _abi
+        from .engine import _PHASE_CODE
+
+        cells = [e._phase_cells(phase) for e in self.engines]  # validates the phase
+        _abi.call("slbm_group_step", self._h, _PHASE_CODE[phase], C.c_void_p(stream or 0))
+        for e, n in zip(self.engines, cells):
+            table = e.pattern == "pull" or e.parity is Parity.EVEN
+            e.counters.record_sweep(phase, n, e.stencil.q, table)
+
+    def finish(self, stream):
+        import ctypes as C
+
+        from . import _abi
+
+        _abi.call("slbm_group_finish", self._h, C.c_void_p(stream or 0))
+        for e in self.engines:
+            if e.pattern == "aa":
+                e.parity = e.parity.flipped()
+            e.counters.steps += 1
 
 
 def _cuda_engine(flags, stencil, params, pattern, frame_width, device, kind="sparse"):
