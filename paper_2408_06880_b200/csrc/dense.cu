@@ -98,40 +98,51 @@ __device__ __forceinline__ bool in_phase(const DenseArgs& a, int64_t x, int64_t 
   return (a.phase == SLBM_PHASE_FRAME) == frame;
 }
 
-// KIND 0 pull, 1 combined (AA even), 2 reversed (AA odd)
+// KIND 0 pull, 1 combined (AA even), 2 reversed (AA odd).
+// Grid: x along the CTA, one grid row per (y, z) row of the box, so the
+// coordinates cost no integer division; slots are 32-bit (q * npad < 2^32
+// is checked at build).  Cells away from the block faces take the neighbour
+// slot p - stride(q) directly; only face cells check the periodic wrap.
 template <class L, int MODEL, int KIND>
 __global__ void __launch_bounds__(128, 4) k_dense(const DenseArgs a) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= a.g.n_cells()) return;
+  const int32_t X = a.g.n[0], Y = a.g.n[1], Z = a.g.n[2];
+  const int32_t x = blockIdx.x * 128 + threadIdx.x;
+  if (x >= X) return;
+  const int32_t row = blockIdx.y;  // z * Y + y
+  const int32_t y = row % Y, z = row / Y;
+  const uint32_t i = uint32_t(row) * uint32_t(X) + uint32_t(x);
   const uint32_t m = a.mask[i];
   if (m == kSolid) return;
-  const int64_t x = i % a.g.n[0];
-  const int64_t r = i / a.g.n[0];
-  const int64_t y = r % a.g.n[1];
-  const int64_t z = r / a.g.n[1];
   if (!in_phase(a, x, y, z)) return;
-  const int64_t p = a.g.padded_flat(x, y, z);
+  const uint32_t PX = uint32_t(a.g.p[0]), PY = uint32_t(a.g.p[1]);
+  const uint32_t p = ((uint32_t(z + a.g.off[2]) * PY) + uint32_t(y + 1)) * PX + uint32_t(x + 1);
+  const uint32_t np = uint32_t(a.npad);
   double* pdf = a.pdf;
   double t[L::Q];
   bool bad;
   if constexpr (KIND == 2) {
     sfor<0, L::Q>([&](auto q) {
       constexpr int qb = L::INV[q];
-      t[q] = pdf[qb * a.npad + p];
+      t[q] = pdf[uint32_t(qb) * np + p];
     });
-    bad = collide<L, MODEL>(t, a.omega, a.lam,
-                            [&](auto q, double v) { pdf[decltype(q)::value * a.npad + p] = v; });
+    bad = collide<L, MODEL>(t, a.omega, a.lam, [&](auto q, double v) {
+      pdf[uint32_t(decltype(q)::value) * np + p] = v;
+    });
   } else {
-    int64_t addr[L::Q];
+    const bool face = x == 0 || x == X - 1 || y == 0 || y == Y - 1 ||
+                      (L::DIM == 3 && (z == 0 || z == Z - 1));
+    uint32_t addr[L::Q];
     addr[0] = p;
     sfor<1, L::Q>([&](auto q) {
       constexpr int qb = L::INV[q];
-      addr[q] = (m >> q) & 1u ? qb * a.npad + p : q * a.npad + upwind_p<L, q>(a, p, x, y, z);
+      uint32_t src = p - uint32_t(a.stride[q]);
+      if (face) src = uint32_t(upwind_p<L, q>(a, p, x, y, z));
+      addr[q] = ((m >> q) & 1u) ? uint32_t(qb) * np + p : uint32_t(int(q)) * np + src;
     });
     sfor<0, L::Q>([&](auto q) { t[q] = pdf[addr[q]]; });
     if (m & kHasUbb) {
       sfor<1, L::Q>([&](auto q) {
-        if ((m >> q) & 1u) t[q] += ubb_corr_of(a, uint32_t(i), q);
+        if ((m >> q) & 1u) t[q] += ubb_corr_of(a, i, q);
       });
     }
     if constexpr (KIND == 1) {
@@ -140,14 +151,15 @@ __global__ void __launch_bounds__(128, 4) k_dense(const DenseArgs a) {
         // out[q] lands at the read location of direction inv q; a folded
         // moving-wall read adds its term at that write too (dense.py:269-279)
         if constexpr (qb != 0) {
-          if ((m & kHasUbb) && ((m >> qb) & 1u)) v = v + ubb_corr_of(a, uint32_t(i), qb);
+          if ((m & kHasUbb) && ((m >> qb) & 1u)) v = v + ubb_corr_of(a, i, qb);
         }
         pdf[addr[qb]] = v;
       });
     } else {
       double* dst = a.dst;
-      bad = collide<L, MODEL>(t, a.omega, a.lam,
-                              [&](auto q, double v) { dst[decltype(q)::value * a.npad + p] = v; });
+      bad = collide<L, MODEL>(t, a.omega, a.lam, [&](auto q, double v) {
+        dst[uint32_t(decltype(q)::value) * np + p] = v;
+      });
     }
   }
   if (bad) atomicMin(a.bad, *a.step);
@@ -365,6 +377,8 @@ int build_dense(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
   cudaFree(d_err);
   cudaFree(d_tags);
   e->total_slots = int64_t(e->q) * n_pad;
+  if (e->total_slots >= (int64_t(1) << 32))
+    return fail(SLBM_ECONFIG, "dense block too large: q * padded cells must be < 2^32");
   return SLBM_OK;
 }
 
@@ -372,7 +386,7 @@ int dense_step(SlbmEngine* e, int phase) {
   DenseArgs a = dense_args(e);
   a.phase = phase;
   const int kind = e->pattern == SLBM_PULL ? 0 : (e->parity == SLBM_EVEN ? 1 : 2);
-  const unsigned grid = grid_of(e->geo.n_cells(), 128);
+  const dim3 grid(unsigned((e->geo.n[0] + 127) / 128), unsigned(e->geo.n[1] * e->geo.n[2]));
   with_lattice(e->q, [&](auto lat) {
     using L = decltype(lat);
     auto go = [&](auto model) {

@@ -181,7 +181,8 @@ def c5(steps):
     st = make_stencil("d3q19")
     p = CollisionParams(1.2, "trt", trt_magic_lambda(1.2))
     dense_bpc = 304.0  # D3Q19 dense AA, GPU (reference model.py, test_acceptance.py:89-98)
-    for phi in (0.05, 0.1, 0.2, 0.3, 0.4, 0.5, 0.6, 0.7, 0.8, 0.9, 1.0):
+    phis = os.environ.get("C5_PHIS", "0.05,0.1,0.2,0.3,0.4,0.5,0.6,0.7,0.8,0.9,1.0")
+    for phi in (float(v) for v in phis.split(",")):
         fl = geometry.obstacle_flags((edge,) * 3, phi, 1)
         eng = SparseEngine(fl, st, p, "aa", device=0, check="deferred")
         eng.init_equilibrium(1.0, np.array([0.005, 0.0, 0.0]))
