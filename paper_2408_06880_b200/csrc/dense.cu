@@ -99,16 +99,16 @@ __device__ __forceinline__ bool in_phase(const DenseArgs& a, int64_t x, int64_t 
 }
 
 // KIND 0 pull, 1 combined (AA even), 2 reversed (AA odd).
-// Grid: x along the CTA, one grid row per (y, z) row of the box, so the
+// Grid: x along the CTA (grid.y chunks), one grid.x index per (y, z) row, so the
 // coordinates cost no integer division; slots are 32-bit (q * npad < 2^32
 // is checked at build).  Cells away from the block faces take the neighbour
 // slot p - stride(q) directly; only face cells check the periodic wrap.
 template <class L, int MODEL, int KIND>
 __global__ void __launch_bounds__(128, 4) k_dense(const DenseArgs a) {
   const int32_t X = a.g.n[0], Y = a.g.n[1], Z = a.g.n[2];
-  const int32_t x = blockIdx.x * 128 + threadIdx.x;
+  const int32_t x = blockIdx.y * 128 + threadIdx.x;
   if (x >= X) return;
-  const int32_t row = blockIdx.y;  // z * Y + y
+  const int32_t row = blockIdx.x;  // z * Y + y (grid.x: up to 2^31 rows)
   const int32_t y = row % Y, z = row / Y;
   const uint32_t i = uint32_t(row) * uint32_t(X) + uint32_t(x);
   const uint32_t m = a.mask[i];
@@ -386,7 +386,7 @@ int dense_step(SlbmEngine* e, int phase) {
   DenseArgs a = dense_args(e);
   a.phase = phase;
   const int kind = e->pattern == SLBM_PULL ? 0 : (e->parity == SLBM_EVEN ? 1 : 2);
-  const dim3 grid(unsigned((e->geo.n[0] + 127) / 128), unsigned(e->geo.n[1] * e->geo.n[2]));
+  const dim3 grid(unsigned(e->geo.n[1] * e->geo.n[2]), unsigned((e->geo.n[0] + 127) / 128));
   with_lattice(e->q, [&](auto lat) {
     using L = decltype(lat);
     auto go = [&](auto model) {
