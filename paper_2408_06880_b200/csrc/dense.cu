@@ -104,7 +104,7 @@ __device__ __forceinline__ bool in_phase(const DenseArgs& a, int64_t x, int64_t 
 // is checked at build).  Cells away from the block faces take the neighbour
 // slot p - stride(q) directly; only face cells check the periodic wrap.
 template <class L, int MODEL, int KIND>
-__global__ void __launch_bounds__(128, 4) k_dense(const DenseArgs a) {
+__global__ void __launch_bounds__(128, KIND == 2 ? 5 : 4) k_dense(const DenseArgs a) {
   const int32_t X = a.g.n[0], Y = a.g.n[1], Z = a.g.n[2];
   const int32_t x = blockIdx.y * 128 + threadIdx.x;
   if (x >= X) return;

@@ -535,9 +535,10 @@ class Domain:
         """model.workload_sparse / workload_dense: Q x fluid cells, or Q x box
         cells for a dense block (domain.py:281-285)"""
         blk = self.blocks[bid]
+        q = self.stencil.q
         if blk.kind == "dense":
-            return self.stencil.q * blk.flags.cell_count()
-        return self.stencil.q * blk.n_fluid
+            return 2 * q * 8 * blk.flags.cell_count()  # model.py workload_dense
+        return (2 * q * 8 + (q - 1) * 4) * blk.n_fluid  # model.py workload_sparse
 
     def curve_order(self) -> list[int]:
         return sorted(self.blocks, key=lambda b: (curve_key(self.blocks[b].grid_pos, self.grid), b))
