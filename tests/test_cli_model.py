@@ -68,7 +68,7 @@ def test_cli_run_and_sweep_on_gpu(tmp_path, gpu_lib):
     row = list(csv.DictReader(open(tmp_path / "t.csv")))[0]
     assert row["steps"] == "6" and int(row["messages"]) > 0
     rho = output.read_vtk_scalars(tmp_path / "t.block0000.vtk", "density")
-    assert rho.shape == (8, 8) and rho.max() > 0.9
+    assert rho.shape == (1, 8, 8) and rho.max() > 0.9  # 2-D block: DIMENSIONS 8 8 1
     rc = cli.main(["sweep-porosity", "--dims", "24,24,24", "--stencil", "D3Q19", "--steps", "4",
                    "--phis", "0.5,1.0", "--pattern", "aa", "--out", str(tmp_path)])
     assert rc == 0
