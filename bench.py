@@ -378,7 +378,7 @@ def impl_ours(args, rank, world, local_rank):
         },
         "roofline": {
             "bound": "hbm",
-            "kernel": "k_aa_even_b<D3Q19,TRT,128,4> (index-list AA sweep)",
+            "kernel": "k_index_sweep<D3Q19,TRT,even> (index-list AA sweep, 128x4 CTAs, L2 idx prefetch)",
             "timing": ("CUDA events after every step inside the timed region (mean over the "
                        "index-list steps)" if world == 1 else
                        "CUDA events around individual sweeps after the timed region"),

@@ -78,7 +78,7 @@ void free_engine(SlbmEngine* e) {
                   e->cid_map,     e->ubb_slot,     e->ubb_partner, e->ubb_corr,
                   e->ghost_key,   e->interior_cids, e->frame_cids, e->d_bad,
                   e->out_slot,    e->out_partner,  e->out_cell,  e->out_dir,
-                  e->out_rho,     e->out_u,        e->idx_aos,   e->dense_mask,
+                  e->out_rho,     e->out_u,        e->dense_mask,
                   e->dense_ubb_key, e->dense_ubb_corr,
                   e->d_step,      e->d_scratch};
   for (void* p : ptrs)
@@ -428,8 +428,23 @@ int slbm_init_canonical_dev(SlbmEngine* e, const double* dev_values) {
 int slbm_init_canonical(SlbmEngine* e, const double* values) {
   CHECK_ENGINE(e);
   if (!values) return fail(SLBM_ECONFIG, "null values");
-  SLBM_TRY(slbm_init_canonical_dev(e, values));  // cudaMemcpyDefault handles host memory
+  DeviceGuard guard(e->device);
+  if (e->layout) {
+    SLBM_TRY(e->ensure_scratch(size_t(e->q) * e->n_fluid * sizeof(double)));
+    SLBM_TRY(copy_h2d(e->d_scratch, values, size_t(e->q) * e->n_fluid * sizeof(double), e->device,
+                      e->stream));
+    SLBM_TRY(dense_init(e, e->d_scratch));
+    SLBM_CUDA_TRY(cudaStreamSynchronize(e->stream));
+    return SLBM_OK;
+  }
+  // sparse.py:205-210: poison everything, then write the Q direction groups
+  SLBM_TRY(launch_fill(e->pdf, e->total_slots, NAN, e->stream));
+  if (e->tmp) SLBM_TRY(launch_fill(e->tmp, e->total_slots, NAN, e->stream));
+  for (int r = 0; r < e->q; ++r)
+    SLBM_TRY(copy_h2d(e->pdf + e->base[r], values + size_t(r) * e->n_fluid,
+                      e->n_fluid * sizeof(double), e->device, e->stream));
   SLBM_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  e->parity = SLBM_EVEN;
   return SLBM_OK;
 }
 
@@ -468,19 +483,16 @@ int slbm_canonical_state(SlbmEngine* e, double* values) {
   if (e->layout) {  // dense.py:275-288
     SLBM_TRY(e->ensure_scratch(size_t(e->q) * e->n_fluid * sizeof(double)));
     SLBM_TRY(dense_canonical(e, e->d_scratch));
-    SLBM_CUDA_TRY(cudaMemcpyAsync(values, e->d_scratch, size_t(e->q) * e->n_fluid * sizeof(double),
-                                  cudaMemcpyDeviceToHost, e->stream));
-    SLBM_CUDA_TRY(cudaStreamSynchronize(e->stream));
-    return SLBM_OK;
+    return copy_d2h(values, e->d_scratch, size_t(e->q) * e->n_fluid * sizeof(double), e->device,
+                    e->stream);
   }
   const bool odd = e->pattern == SLBM_AA && e->parity == SLBM_ODD;
   if (odd) SLBM_TRY(launch_refresh(e, SLBM_ODD));  // sparse.py:317
   for (int r = 0; r < e->q; ++r) {
     const int g = odd ? e->dirs.inv[r] : r;
-    SLBM_CUDA_TRY(cudaMemcpyAsync(values + size_t(r) * e->n_fluid, e->pdf + e->base[g],
-                                  e->n_fluid * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+    SLBM_TRY(copy_d2h(values + size_t(r) * e->n_fluid, e->pdf + e->base[g],
+                      e->n_fluid * sizeof(double), e->device, e->stream));
   }
-  SLBM_CUDA_TRY(cudaStreamSynchronize(e->stream));
   return SLBM_OK;
 }
 
@@ -506,11 +518,8 @@ int slbm_macroscopic(SlbmEngine* e, double* rho, double* u) {
     st = launch_macroscopic(e, nullptr, d_rho, d_u);
   }
   if (st != SLBM_OK) return st;
-  SLBM_CUDA_TRY(cudaMemcpyAsync(rho, d_rho, cells * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
-  SLBM_CUDA_TRY(cudaMemcpyAsync(u, d_u, cells * e->dim * sizeof(double), cudaMemcpyDeviceToHost,
-                                e->stream));
-  SLBM_CUDA_TRY(cudaStreamSynchronize(e->stream));
-  return SLBM_OK;
+  SLBM_TRY(copy_d2h(rho, d_rho, cells * sizeof(double), e->device, e->stream));
+  return copy_d2h(u, d_u, cells * e->dim * sizeof(double), e->device, e->stream);
 }
 
 int slbm_total_mass(SlbmEngine* e, double* mass) {

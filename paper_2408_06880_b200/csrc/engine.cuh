@@ -33,7 +33,6 @@ struct SlbmEngine {
   int64_t n_dense_ubb = 0;
   int32_t dense_frame_w[3] = {1, 1, 1};
   uint32_t* idx = nullptr;  // (q-1) x n_fluid
-  uint32_t* idx_aos = nullptr;  // optional cell-major copy (tuning variant)
   uint32_t* x_flat = nullptr;  // cid -> padded flat
   int32_t* cid_map = nullptr;  // padded flat -> cid or -1
   uint32_t* ubb_slot = nullptr;
@@ -89,6 +88,11 @@ int launch_slot_lookup(SlbmEngine* e, const int64_t* d_qs, const int64_t* d_pfla
                        int64_t* d_out, int* d_err);
 
 int set_tuning(int knob, int value);
+
+// hostcopy.cu: staged multi-threaded copies for pageable host arrays
+// (synchronous; ordered after the work already queued on `s`)
+int copy_d2h(void* host, const void* dev, size_t bytes, int device, cudaStream_t s);
+int copy_h2d(void* dev, const void* host, size_t bytes, int device, cudaStream_t s);
 
 // builder.cu
 int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,

@@ -15,6 +15,7 @@
 
 #include "collide.cuh"
 #include "engine.cuh"
+#include "sweep.cuh"
 
 // per-engine sweep arguments of one phase, staged in shared memory by a CTA
 namespace slbm {
@@ -70,7 +71,8 @@ __device__ __forceinline__ int find_engine(const uint32_t* start, int n, uint32_
 
 template <class L, int MODEL, int KIND>
 __global__ void __launch_bounds__(kGB, 4) k_group(const GroupArgs* table, const uint32_t* start,
-                                                  int n_eng, double omega, double lam) {
+                                                  int n_eng, double omega, double lam,
+                                                  uint32_t ahead) {
   __shared__ GroupArgs a;
   if (threadIdx.x == 0) a = table[find_engine(start, n_eng, blockIdx.x)];
   __shared__ uint32_t first;
@@ -94,6 +96,9 @@ __global__ void __launch_bounds__(kGB, 4) k_group(const GroupArgs* table, const 
     s[0] = c;
     sfor<1, L::Q>([&](auto q) { s[q] = __ldcs(a.idx + size_t(q - 1) * a.n_fluid + c); });
     sfor<0, L::Q>([&](auto q) { t[q] = pdf[s[q]]; });
+    // index-list rows of this engine's CTA `ahead` positions later (sweep.cuh)
+    prefetch_idx_ahead<L::Q - 1, kGB>(a.idx, a.n_fluid, a.cids, a.n_cells,
+                                      (blockIdx.x - first) * kGB, ahead);
     if constexpr (KIND == 1) {  // AA even (sparse.py:264-271)
       bad = collide<L, MODEL>(t, omega, lam, [&](auto q, double v) {
         constexpr int qb = L::INV[decltype(q)::value];
@@ -284,14 +289,21 @@ int slbm_group_step(SlbmGroup* g, int phase, void* stream) {
   const int n = int(g->engines.size());
   on_lattice(g->q, [&](auto lat) {
     using L = decltype(lat);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint32_t ahead = uint32_t(sms);  // one quarter wave at 4 CTAs/SM
     auto go = [&](auto mc) {
       constexpr int M = decltype(mc)::value;
       if (kind == 0)
-        k_group<L, M, 0><<<g->n_cta[phase], kGB, 0, s>>>(tab, g->cta_start[phase], n, g->omega, g->lam);
+        k_group<L, M, 0><<<g->n_cta[phase], kGB, 0, s>>>(tab, g->cta_start[phase], n, g->omega, g->lam,
+                                                           ahead);
       else if (kind == 1)
-        k_group<L, M, 1><<<g->n_cta[phase], kGB, 0, s>>>(tab, g->cta_start[phase], n, g->omega, g->lam);
+        k_group<L, M, 1><<<g->n_cta[phase], kGB, 0, s>>>(tab, g->cta_start[phase], n, g->omega, g->lam,
+                                                           ahead);
       else
-        k_group<L, M, 2><<<g->n_cta[phase], kGB, 0, s>>>(tab, g->cta_start[phase], n, g->omega, g->lam);
+        k_group<L, M, 2><<<g->n_cta[phase], kGB, 0, s>>>(tab, g->cta_start[phase], n, g->omega, g->lam,
+                                                           ahead);
     };
     if (g->model == SLBM_SRT)
       go(std::integral_constant<int, SLBM_SRT>{});

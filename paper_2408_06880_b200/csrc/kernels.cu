@@ -21,6 +21,7 @@
 
 #include "collide.cuh"
 #include "engine.cuh"
+#include "sweep.cuh"
 
 namespace slbm {
 
@@ -35,224 +36,79 @@ struct SweepArgs {
   double omega, lam;
   unsigned long long* bad;
   const unsigned long long* step;
-  const uint32_t* idx_aos;  // optional cell-major index list (tuning)
 };
 
 namespace {
 
-constexpr int kBlock = 256;
+constexpr int kBlock = 256;  // small kernels and the odd sweep
+constexpr int kIB = 128;     // index-list sweeps: 128-thread CTAs, 4 per SM
 
 __device__ __forceinline__ void flag_bad(const SweepArgs& a) {
   atomicMin(a.bad, *a.step);
 }
 
-// idx loads: the first read keeps the row in L1 (evict_last) so the RELOAD
-// variant can re-read the slot right before its store instead of holding
-// all Q-1 slot ids in registers through the collision.
-__device__ __forceinline__ uint32_t ld_idx_keep(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.global.nc.L1::evict_last.u32 %0, [%1];" : "=r"(v) : "l"(p));
-  return v;
-}
-__device__ __forceinline__ uint32_t ld_idx_again(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.global.nc.L1::evict_first.u32 %0, [%1];" : "=r"(v) : "l"(p));
-  return v;
-}
+// tuning knobs (slbm_set_tuning), kept for tools/variants.py
+int g_even_variant = 0;     // knob 0: 0 = production, 1 = no idx prefetch, 2 = probe
+int g_odd_variant = 0;      // knob 1: odd-sweep CTAs per SM (0: 3)
+int g_ahead_quarters = 1;   // knob 2: idx prefetch distance in quarter waves
+int g_ahead_ctas = 0;       // knob 3: ... or in CTAs when > 0
+int g_num_sms = 0;
 
-// tuning knobs (slbm_set_tuning): even-sweep variant
-int g_even_variant = 0;
-int g_odd_variant = 0;
+enum Kind { kPull = 0, kEven = 1, kOdd = 2 };
 
-template <class L, int MODEL, int MINB, bool RELOAD>
-__global__ void __launch_bounds__(kBlock, MINB) k_aa_even(const SweepArgs a) {
-  const uint32_t i = blockIdx.x * kBlock + threadIdx.x;
-  if (i >= a.n_cells) return;
-  const uint32_t c = a.cids ? a.cids[i] : i;
-  uint32_t s[L::Q];
-  double t[L::Q];
-  s[0] = c;
-  if constexpr (RELOAD) {
-    sfor<1, L::Q>([&](auto q) { s[q] = ld_idx_keep(a.idx + size_t(q - 1) * a.n_fluid + c); });
-  } else {
-    sfor<1, L::Q>([&](auto q) { s[q] = __ldcs(a.idx + size_t(q - 1) * a.n_fluid + c); });
+// Index-list sweep: AA even (combined pull-collide-push, sparse.py:264-271)
+// or pull (sparse.py:257-262).  One thread per cell; the Q-1 slot ids stay
+// in registers through the collision so the even step scatters through the
+// same slots it gathered from (opposite directions).
+//
+// Kernel-variant study (tools/variants.py, profiles/r01_variants_*.log):
+// 256x2 vs 128x4 CTAs (+2% for 128x4); register caps 80/64 (spills, -10..-40%);
+// re-reading idx before each store (RELOAD); cp.async gather into shared
+// memory; persistent CTAs with a cp.async idx double buffer; a cell-major
+// idx copy; ld.global.nc / L1::no_allocate PDF gathers (-40%: the gathers
+// want L1 sector merging); st.global.cs stores (-4%) — all slower than the
+// plain gather.  What pays is the L2 prefetch of the index list one quarter
+// wave ahead (sweep.cuh): +7-9%.
+template <class L, int MODEL, int KIND, int MINB, bool PF>
+__global__ void __launch_bounds__(kIB, MINB) k_index_sweep(const SweepArgs a, uint32_t ahead) {
+  const uint32_t first = blockIdx.x * kIB;
+  if constexpr (PF) {
+    if (a.cids == nullptr)
+      prefetch_idx_ahead<L::Q - 1, kIB>(a.idx, a.n_fluid, nullptr, a.n_cells, first, ahead);
   }
-  sfor<0, L::Q>([&](auto q) { t[q] = a.pdf[s[q]]; });
-  double* pdf = a.pdf;
-  const bool bad = collide<L, MODEL>(t, a.omega, a.lam, [&](auto q, double v) {
-    constexpr int qb = L::INV[decltype(q)::value];
-    if constexpr (RELOAD && qb != 0) {
-      pdf[ld_idx_again(a.idx + size_t(qb - 1) * a.n_fluid + c)] = v;
-    } else {
-      pdf[s[qb]] = v;
-    }
-  });
-  if (bad) flag_bad(a);
-}
-
-// block-size study of the register-resident sweep (tuning variants 13-17)
-template <class L, int MODEL, int BLOCK, int MINB, bool RELOAD>
-__global__ void __launch_bounds__(BLOCK, MINB) k_aa_even_b(const SweepArgs a) {
-  const uint32_t i = blockIdx.x * BLOCK + threadIdx.x;
+  const uint32_t i = first + threadIdx.x;
   if (i >= a.n_cells) return;
   const uint32_t c = a.cids ? a.cids[i] : i;
   uint32_t s[L::Q];
   double t[L::Q];
-  s[0] = c;
-  if constexpr (RELOAD) {
-    sfor<1, L::Q>([&](auto q) { s[q] = ld_idx_keep(a.idx + size_t(q - 1) * a.n_fluid + c); });
-  } else {
-    sfor<1, L::Q>([&](auto q) { s[q] = __ldcs(a.idx + size_t(q - 1) * a.n_fluid + c); });
-  }
-  sfor<0, L::Q>([&](auto q) { t[q] = a.pdf[s[q]]; });
-  double* pdf = a.pdf;
-  const bool bad = collide<L, MODEL>(t, a.omega, a.lam, [&](auto q, double v) {
-    constexpr int qb = L::INV[decltype(q)::value];
-    if constexpr (RELOAD && qb != 0) {
-      pdf[ld_idx_again(a.idx + size_t(qb - 1) * a.n_fluid + c)] = v;
-    } else {
-      pdf[s[qb]] = v;
-    }
-  });
-  if (bad) flag_bad(a);
-}
-
-// cell-major ("AoS") copy of the index list: cell c's Q-1 slot ids are
-// contiguous (padded to a multiple of 4 for 16-byte loads), so a warp reads
-// one contiguous 2.5 KB run instead of Q-1 separate 128-byte rows
-template <int QM1P>
-__global__ void k_idx_to_aos(const uint32_t* idx, uint32_t n, int qm1, uint32_t* out) {
-  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n) return;
-  for (int q = 0; q < QM1P; ++q) out[size_t(c) * QM1P + q] = q < qm1 ? idx[size_t(q) * n + c] : 0u;
-}
-
-template <class L, int MODEL, int BLOCK, int MINB>
-__global__ void __launch_bounds__(BLOCK, MINB) k_aa_even_aos(const SweepArgs a,
-                                                             const uint32_t* __restrict__ aos) {
-  constexpr int QP = ((L::Q - 1) + 3) / 4 * 4;
-  const uint32_t i = blockIdx.x * BLOCK + threadIdx.x;
-  if (i >= a.n_cells) return;
-  const uint32_t c = a.cids ? a.cids[i] : i;
-  uint32_t s[QP + 1];
-  s[0] = c;
-  const uint4* row = reinterpret_cast<const uint4*>(aos + size_t(c) * QP);
-  sfor<0, QP / 4>([&](auto k) {
-    const uint4 v = __ldcs(row + k);
-    s[1 + 4 * k] = v.x;
-    s[2 + 4 * k] = v.y;
-    s[3 + 4 * k] = v.z;
-    s[4 + 4 * k] = v.w;
-  });
-  double t[L::Q];
-  sfor<0, L::Q>([&](auto q) { t[q] = a.pdf[s[q]]; });
-  double* pdf = a.pdf;
-  const bool bad = collide<L, MODEL>(t, a.omega, a.lam, [&](auto q, double v) {
-    constexpr int qb = L::INV[decltype(q)::value];
-    pdf[s[qb]] = v;
-  });
-  if (bad) flag_bad(a);
-}
-
-// ---- asynchronous-gather variant of the index-list sweep -------------------
-// The register-resident kernel above is latency bound (ncu r01: long
-// scoreboard 9 of 14 cycles/issue at 25% occupancy, 126 registers for 19
-// PDFs + 18 slot ids).  Here each thread gathers its 19 PDFs straight into
-// shared memory with cp.async (LDGSTS: no destination registers), so the
-// collision can run at 4 CTAs/SM with 2x the bytes in flight; values are
-// read back from shared memory as the collision consumes them.
-__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem_src));
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_all;" ::: "memory");
-}
-
-struct SmemColumn {
-  const double* p;  // this thread's column: p[q * kBlock]
-  __device__ __forceinline__ double operator[](int q) const { return p[q * kBlock]; }
-};
-
-template <class L, int MODEL, int MINB>
-__global__ void __launch_bounds__(kBlock, MINB) k_aa_even_async(const SweepArgs a) {
-  extern __shared__ double stage[];  // [Q][kBlock]
-  const uint32_t i = blockIdx.x * kBlock + threadIdx.x;
-  if (i >= a.n_cells) return;
-  const uint32_t c = a.cids ? a.cids[i] : i;
-  uint32_t s[L::Q];
   s[0] = c;
   sfor<1, L::Q>([&](auto q) { s[q] = __ldcs(a.idx + size_t(q - 1) * a.n_fluid + c); });
-  double* col = stage + threadIdx.x;
-  sfor<0, L::Q>([&](auto q) { cp_async8(col + q * kBlock, a.pdf + s[q]); });
-  cp_async_wait_all();
-  double* pdf = a.pdf;
-  const bool bad = collide<L, MODEL>(SmemColumn{col}, a.omega, a.lam, [&](auto q, double v) {
-    constexpr int qb = L::INV[decltype(q)::value];
-    pdf[s[qb]] = v;
-  });
-  if (bad) flag_bad(a);
-}
-
-// ---- persistent variant with the index list prefetched one cell ahead ------
-// Each thread walks cells i, i + stride, ...; while it gathers and collides
-// cell k, the Q-1 slot ids of cell k+1 are already travelling into its own
-// shared-memory column (cp.async, double buffered), so the idx -> pdf
-// dependent DRAM round trip is paid once per thread, not once per cell.
-__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gmem_src) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem_src));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-template <class L, int MODEL, int MINB>
-__global__ void __launch_bounds__(kBlock, MINB) k_aa_even_pf(const SweepArgs a) {
-  extern __shared__ uint32_t pf_raw[];  // [2][Q-1][kBlock]
-  auto pf = reinterpret_cast<uint32_t(*)[L::Q - 1][kBlock]>(pf_raw);
-  const uint32_t stride = gridDim.x * kBlock;
-  uint32_t i = blockIdx.x * kBlock + threadIdx.x;
-  auto prefetch = [&](uint32_t cell, int buf) {
-    const uint32_t c = a.cids ? a.cids[cell] : cell;
-    sfor<1, L::Q>([&](auto q) {
-      cp_async4(&pf[buf][q - 1][threadIdx.x], a.idx + size_t(q - 1) * a.n_fluid + c);
-    });
-  };
-  if (i < a.n_cells) prefetch(i, 0);
-  cp_async_commit();
-  int buf = 0;
-  bool bad = false;
-  double* pdf = a.pdf;
-  for (; i < a.n_cells; i += stride) {
-    const uint32_t nxt = i + stride;
-    if (nxt < a.n_cells) prefetch(nxt, buf ^ 1);
-    cp_async_commit();
-    cp_async_wait<1>();
-    const uint32_t c = a.cids ? a.cids[i] : i;
-    uint32_t s[L::Q];
-    double t[L::Q];
-    s[0] = c;
-    sfor<1, L::Q>([&](auto q) { s[q] = pf[buf][q - 1][threadIdx.x]; });
-    sfor<0, L::Q>([&](auto q) { t[q] = pdf[s[q]]; });
-    bad |= collide<L, MODEL>(t, a.omega, a.lam, [&](auto q, double v) {
+  sfor<0, L::Q>([&](auto q) { t[q] = a.pdf[s[q]]; });
+  if constexpr (PF) {
+    if (a.cids != nullptr)
+      prefetch_idx_ahead<L::Q - 1, kIB>(a.idx, a.n_fluid, a.cids, a.n_cells, first, ahead);
+  }
+  bool bad;
+  if constexpr (KIND == kEven) {
+    double* pdf = a.pdf;
+    bad = collide<L, MODEL>(t, a.omega, a.lam, [&](auto q, double v) {
       constexpr int qb = L::INV[decltype(q)::value];
       pdf[s[qb]] = v;
     });
-    buf ^= 1;
+  } else {
+    double* dst = a.dst;
+    bad = collide<L, MODEL>(t, a.omega, a.lam,
+                            [&](auto q, double v) { dst[a.base[decltype(q)::value] + c] = v; });
   }
-  cp_async_wait<0>();
   if (bad) flag_bad(a);
 }
 
-// ---- memory-pattern probes (tuning only; they do NOT compute LBM) ----------
-// MODE 0: index-list gather + scatter back through the same slots, no math
-// MODE 1: index-list gather, coalesced writes to the cell's own groups
-template <class L, int MODE>
-__global__ void __launch_bounds__(kBlock) k_probe(const SweepArgs a) {
-  const uint32_t i = blockIdx.x * kBlock + threadIdx.x;
+// Memory-pattern probe (tuning only; does NOT compute LBM): the even sweep's
+// gather + scatter through the same slots without the collision — the
+// bandwidth ceiling of the access pattern itself.
+template <class L>
+__global__ void __launch_bounds__(kIB) k_probe(const SweepArgs a) {
+  const uint32_t i = blockIdx.x * kIB + threadIdx.x;
   if (i >= a.n_cells) return;
   const uint32_t c = i;
   uint32_t s[L::Q];
@@ -260,18 +116,13 @@ __global__ void __launch_bounds__(kBlock) k_probe(const SweepArgs a) {
   s[0] = c;
   sfor<1, L::Q>([&](auto q) { s[q] = __ldcs(a.idx + size_t(q - 1) * a.n_fluid + c); });
   sfor<0, L::Q>([&](auto q) { t[q] = a.pdf[s[q]]; });
-  sfor<0, L::Q>([&](auto q) {
-    constexpr int qb = L::INV[q];
-    if constexpr (MODE == 0)
-      a.pdf[s[qb]] = t[q];
-    else
-      a.pdf[a.base[qb] + c] = t[q];
-  });
+  sfor<0, L::Q>([&](auto q) { a.pdf[s[L::INV[q]]] = t[q]; });
 }
 
+// AA odd (cell-local reversed step, sparse.py:273-282): every access is a
+// coalesced row of a direction group, no index list.
 template <class L, int MODEL, int MINB>
 __global__ void __launch_bounds__(kBlock, MINB) k_aa_odd(const SweepArgs a) {
-
   const uint32_t i = blockIdx.x * kBlock + threadIdx.x;
   if (i >= a.n_cells) return;
   const uint32_t c = a.cids ? a.cids[i] : i;
@@ -287,106 +138,46 @@ __global__ void __launch_bounds__(kBlock, MINB) k_aa_odd(const SweepArgs a) {
   if (bad) flag_bad(a);
 }
 
-template <class L, int MODEL>
-__global__ void __launch_bounds__(kBlock) k_pull(const SweepArgs a) {
-  const uint32_t i = blockIdx.x * kBlock + threadIdx.x;
-  if (i >= a.n_cells) return;
-  const uint32_t c = a.cids ? a.cids[i] : i;
-  double t[L::Q];
-  t[0] = a.pdf[c];
-  sfor<1, L::Q>([&](auto q) {
-    t[q] = a.pdf[__ldcs(a.idx + size_t(q - 1) * a.n_fluid + c)];
-  });
-  double* dst = a.dst;
-  const bool bad = collide<L, MODEL>(t, a.omega, a.lam, [&](auto q, double v) {
-    dst[a.base[decltype(q)::value] + c] = v;
-  });
-  if (bad) flag_bad(a);
-}
-
-enum Kind { kPull = 0, kEven = 1, kOdd = 2 };
-
-template <class L, int MODEL, int MINB>
-void launch_async(const SweepArgs& a, unsigned grid, cudaStream_t s) {
-  constexpr int bytes = L::Q * kBlock * sizeof(double);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_aa_even_async<L, MODEL, MINB>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    configured = true;
-  }
-  k_aa_even_async<L, MODEL, MINB><<<grid, kBlock, bytes, s>>>(a);
-}
-
-int g_num_sms = 0;
-
-template <class L, int MODEL, int MINB>
-void launch_pf(const SweepArgs& a, unsigned grid, cudaStream_t s) {
+int num_sms() {
   if (!g_num_sms) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  constexpr int bytes = 2 * (L::Q - 1) * kBlock * sizeof(uint32_t);
-  static int per_sm = 0;
-  if (!per_sm) {
-    cudaFuncSetAttribute(k_aa_even_pf<L, MODEL, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         bytes);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_aa_even_pf<L, MODEL, MINB>, kBlock,
-                                                  bytes);
-    per_sm = std::max(per_sm, 1);
+  return g_num_sms;
+}
+
+template <class L, int MODEL, int KIND, int MINB, bool PF>
+void launch_index(const SweepArgs& a, cudaStream_t s) {
+  static int resident = 0;  // CTAs per SM this instantiation actually gets
+  if (!resident) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_index_sweep<L, MODEL, KIND, MINB, PF>,
+                                                  kIB, 0);
+    resident = std::max(resident, 1);
   }
-  const unsigned persistent = unsigned(per_sm * g_num_sms);
-  k_aa_even_pf<L, MODEL, MINB><<<std::min(grid, persistent), kBlock, bytes, s>>>(a);
+  const uint32_t ahead = g_ahead_ctas > 0 ? uint32_t(g_ahead_ctas)
+                                          : uint32_t(num_sms() * resident * g_ahead_quarters / 4);
+  k_index_sweep<L, MODEL, KIND, MINB, PF>
+      <<<(a.n_cells + kIB - 1) / kIB, kIB, 0, s>>>(a, std::max(ahead, 1u));
 }
 
 template <class L, int MODEL>
 void launch_kind(int kind, const SweepArgs& a, unsigned grid, cudaStream_t s) {
+  constexpr int MINB = L::Q == 9 ? 8 : 4;
   if (kind == kPull) {
-    k_pull<L, MODEL><<<grid, kBlock, 0, s>>>(a);
+    launch_index<L, MODEL, kPull, MINB, true>(a, s);
   } else if (kind == kEven) {
-    if constexpr (L::Q == 9) {
-      k_aa_even<L, MODEL, 1, false><<<grid, kBlock, 0, s>>>(a);
-    } else {
-      switch (g_even_variant) {
-        case 1: k_aa_even<L, MODEL, 3, false><<<grid, kBlock, 0, s>>>(a); break;
-        case 2: k_aa_even<L, MODEL, 4, false><<<grid, kBlock, 0, s>>>(a); break;
-        case 3: k_aa_even<L, MODEL, 3, true><<<grid, kBlock, 0, s>>>(a); break;
-        case 4: k_aa_even<L, MODEL, 4, true><<<grid, kBlock, 0, s>>>(a); break;
-        case 5: launch_async<L, MODEL, 4>(a, grid, s); break;
-        case 6: launch_async<L, MODEL, 3>(a, grid, s); break;
-        case 7: launch_async<L, MODEL, 2>(a, grid, s); break;
-        case 8: launch_pf<L, MODEL, 2>(a, grid, s); break;
-        case 9: launch_pf<L, MODEL, 1>(a, grid, s); break;
-        case 10: launch_pf<L, MODEL, 3>(a, grid, s); break;
-        case 13: k_aa_even<L, MODEL, 2, true><<<grid, kBlock, 0, s>>>(a); break;
-        case 19:
-          k_aa_even_aos<L, MODEL, 128, 4><<<(a.n_cells + 127) / 128, 128, 0, s>>>(a, a.idx_aos);
-          break;
-        case 14: k_aa_even_b<L, MODEL, 320, 2, false><<<(a.n_cells + 319) / 320, 320, 0, s>>>(a); break;
-        case 15: k_aa_even_b<L, MODEL, 320, 2, true><<<(a.n_cells + 319) / 320, 320, 0, s>>>(a); break;
-        case 16: k_aa_even_b<L, MODEL, 128, 4, false><<<(a.n_cells + 127) / 128, 128, 0, s>>>(a); break;
-        case 17: k_aa_even_b<L, MODEL, 288, 2, false><<<(a.n_cells + 287) / 288, 288, 0, s>>>(a); break;
-        case 11: k_probe<L, 0><<<grid, kBlock, 0, s>>>(a); break;
-        case 12: k_probe<L, 1><<<grid, kBlock, 0, s>>>(a); break;
-        case 18: k_aa_even<L, MODEL, 2, false><<<grid, kBlock, 0, s>>>(a); break;
-        // default: 128-thread CTAs, 4 per SM (same 16 warps/SM as 256 x 2 at
-        // <= 128 registers, finer scheduling; +2% measured, profiles/)
-        default:
-          k_aa_even_b<L, MODEL, 128, 4, false><<<(a.n_cells + 127) / 128, 128, 0, s>>>(a);
-          break;
-      }
-    }
+    if (g_even_variant == 1)
+      launch_index<L, MODEL, kEven, MINB, false>(a, s);
+    else if (g_even_variant == 2)
+      k_probe<L><<<(a.n_cells + kIB - 1) / kIB, kIB, 0, s>>>(a);
+    else
+      launch_index<L, MODEL, kEven, MINB, true>(a, s);
   } else {
-    if constexpr (L::Q == 9) {
-      k_aa_odd<L, MODEL, 1><<<grid, kBlock, 0, s>>>(a);
-    } else {
-      switch (g_odd_variant) {
-        case 1: k_aa_odd<L, MODEL, 3><<<grid, kBlock, 0, s>>>(a); break;
-        case 2: k_aa_odd<L, MODEL, 4><<<grid, kBlock, 0, s>>>(a); break;
-        default: k_aa_odd<L, MODEL, 3><<<grid, kBlock, 0, s>>>(a); break;
-      }
-    }
+    if (L::Q != 9 && g_odd_variant == 2)
+      k_aa_odd<L, MODEL, 4><<<grid, kBlock, 0, s>>>(a);
+    else
+      k_aa_odd<L, MODEL, L::Q == 9 ? 1 : 3><<<grid, kBlock, 0, s>>>(a);
   }
 }
 
@@ -582,6 +373,8 @@ void by_lattice(int q, F&& f) {
 int set_tuning(int knob, int value) {
   if (knob == 0) g_even_variant = value;
   else if (knob == 1) g_odd_variant = value;
+  else if (knob == 2) g_ahead_quarters = value;
+  else if (knob == 3) g_ahead_ctas = value;
   else return fail(SLBM_ECONFIG, "unknown tuning knob");
   return SLBM_OK;
 }
@@ -609,19 +402,6 @@ int launch_step(SlbmEngine* e, int phase) {
   if (a.n_cells == 0) return SLBM_OK;
   const int kind = e->pattern == SLBM_PULL ? kPull : (e->parity == SLBM_EVEN ? kEven : kOdd);
   const unsigned grid = grid_for(a.n_cells, kBlock);
-  if (kind == kEven && g_even_variant == 19 && e->q != 9) {
-    if (!e->idx_aos) {  // lazily built cell-major copy of the index list
-      const int qp = ((e->q - 1) + 3) / 4 * 4;
-      SLBM_CUDA_TRY(cudaMalloc(&e->idx_aos, size_t(e->n_fluid) * qp * sizeof(uint32_t)));
-      if (e->q == 19)
-        k_idx_to_aos<20><<<grid_for(e->n_fluid, 256), 256, 0, e->stream>>>(
-            e->idx, uint32_t(e->n_fluid), e->q - 1, e->idx_aos);
-      else
-        k_idx_to_aos<28><<<grid_for(e->n_fluid, 256), 256, 0, e->stream>>>(
-            e->idx, uint32_t(e->n_fluid), e->q - 1, e->idx_aos);
-    }
-    a.idx_aos = e->idx_aos;
-  }
   by_lattice(e->q, [&](auto lat) {
     launch_model<decltype(lat)>(e->model, kind, a, grid, e->stream);
   });

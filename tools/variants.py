@@ -43,8 +43,8 @@ def main():
     q = int(os.environ.get("Q", 19))
     model = os.environ.get("MODEL", "trt")
     edge = int(os.environ.get("EDGE", 512))
-    variants = [int(v) for v in os.environ.get("VARIANTS", "0,1,2,3,4").split(",")]
-    odd_variants = [int(v) for v in os.environ.get("ODD_VARIANTS", "0,1,2").split(",")]
+    variants = [int(v) for v in os.environ.get("VARIANTS", "0,1,2").split(",")]
+    odd_variants = [int(v) for v in os.environ.get("ODD_VARIANTS", "0,2").split(",")]
     st = make_stencil("d3q19" if q == 19 else "d3q27")
     p = CollisionParams(bench.OMEGA, model, bench.magic_lambda(bench.OMEGA))
     fl = bench.make_flags(edge, 0)
@@ -57,11 +57,29 @@ def main():
     be = 2 * q * 8 + (q - 1) * 4
     bo = 2 * q * 8
     hbm = bench.peaks()[0]
-    for v in variants:
-        lib.slbm_set_tuning(0, v)
-        te, _ = time_pair(eng)
-        res["even"][v] = {"ms": te, "gbs": n * be / te / 1e6, "frac": n * be / te / 1e6 / hbm}
-        print(f"even variant {v}: {te:.4f} ms  {n * be / te / 1e6:.0f} GB/s  {n * be / te / 1e6 / hbm:.3f}")
+    aheads = [int(v) for v in os.environ.get("AHEADS", "1").split(",")]
+    reps = int(os.environ.get("REPS", 1))
+    samples = {}
+    # round-robin over (distance, variant) so clock/thermal drift spreads evenly
+    for _ in range(reps):
+        for ah in aheads:
+            if ah < 0:
+                lib.slbm_set_tuning(3, -ah)  # negative: distance in CTAs
+            else:
+                lib.slbm_set_tuning(3, 0)
+                lib.slbm_set_tuning(2, ah)
+            for v in variants:
+                lib.slbm_set_tuning(0, v)
+                te, _ = time_pair(eng, reps=3 if reps > 1 else 6)
+                key = f"{v}" if len(aheads) == 1 else f"{v}@{ah}"
+                samples.setdefault(key, []).append(te)
+    for key, ts in samples.items():
+        te = statistics.median(ts)
+        res["even"][key] = {"ms": te, "gbs": n * be / te / 1e6, "frac": n * be / te / 1e6 / hbm}
+        print(f"even variant {key}: {te:.4f} ms  {n * be / te / 1e6:.0f} GB/s  "
+              f"{n * be / te / 1e6 / hbm:.3f}")
+    lib.slbm_set_tuning(2, 1)
+    lib.slbm_set_tuning(3, 0)
     lib.slbm_set_tuning(0, 0)
     for v in odd_variants:
         lib.slbm_set_tuning(1, v)
@@ -73,7 +91,7 @@ def main():
     # bitwise agreement of all variants on a small bed
     small = bench.make_flags(48, 0)
     ref = None
-    for v in variants:
+    for v in [v for v in variants if v != 2]:  # 2 = memory probe, not LBM
         for ov in odd_variants:
             lib.slbm_set_tuning(0, v)
             lib.slbm_set_tuning(1, ov)
