@@ -251,6 +251,10 @@ static int create_engine(int layout, const uint8_t* tags_pad, const double* ubb_
     if (cudaStreamSynchronize(e->stream) != cudaSuccess)
       st = fail(SLBM_ECUDA, "engine init sync failed");
   }
+  // large blocks will move GBs through init_canonical / canonical_state /
+  // macroscopic_fields: set up the pinned staging lanes now, not in the
+  // first transfer (hostcopy.cu)
+  if (st == SLBM_OK && e->total_slots * 8 >= (int64_t(256) << 20)) st = hostcopy_reserve(e->device);
   if (st != SLBM_OK) {
     std::string msg = last_error();
     free_engine(e);

@@ -93,6 +93,8 @@ int set_tuning(int knob, int value);
 // (synchronous; ordered after the work already queued on `s`)
 int copy_d2h(void* host, const void* dev, size_t bytes, int device, cudaStream_t s);
 int copy_h2d(void* dev, const void* host, size_t bytes, int device, cudaStream_t s);
+int hostcopy_reserve(int device);
+int hostcopy_tune(int knob, int value);  // 10: chunk MiB, 11: max threads
 
 // builder.cu
 int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,

@@ -23,9 +23,10 @@
 namespace slbm {
 namespace {
 
-constexpr size_t kChunk = size_t(8) << 20;  // bytes per pinned chunk
-constexpr int kMaxThreads = 8;
+constexpr int kMaxLanes = 16;
 constexpr size_t kMinStaged = size_t(4) << 20;  // below this: plain copy
+size_t g_chunk = size_t(4) << 20;  // bytes per pinned chunk (tuning knob 10, MiB)
+int g_max_threads = 8;             // lanes used per transfer (tuning knob 11)
 
 struct Lane {
   int device = -1;
@@ -35,10 +36,9 @@ struct Lane {
 };
 
 std::mutex g_mu;            // one staged transfer at a time per process
-std::vector<Lane> g_lanes;  // kMaxThreads lanes, created for the current device
+std::vector<Lane> g_lanes;  // kMaxLanes lanes, created for the current device
 
-int lanes_for(int device) {
-  if (!g_lanes.empty() && g_lanes[0].device == device) return SLBM_OK;
+void drop_lanes() {
   for (Lane& l : g_lanes) {
     cudaSetDevice(l.device);
     for (int k = 0; k < 2; ++k) {
@@ -47,14 +47,20 @@ int lanes_for(int device) {
     }
     cudaStreamDestroy(l.stream);
   }
-  g_lanes.assign(kMaxThreads, Lane{});
+  g_lanes.clear();
+}
+
+int lanes_for(int device) {
+  if (!g_lanes.empty() && g_lanes[0].device == device) return SLBM_OK;
+  drop_lanes();
+  g_lanes.assign(kMaxLanes, Lane{});
   cudaSetDevice(device);
   for (Lane& l : g_lanes) {
     l.device = device;
     SLBM_CUDA_TRY(cudaStreamCreateWithFlags(&l.stream, cudaStreamNonBlocking));
     for (int k = 0; k < 2; ++k) {
       SLBM_CUDA_TRY(cudaEventCreateWithFlags(&l.done[k], cudaEventDisableTiming));
-      SLBM_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&l.buf[k]), kChunk, 0));
+      SLBM_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&l.buf[k]), g_chunk, 0));
     }
   }
   return SLBM_OK;
@@ -79,8 +85,8 @@ void advise_huge(void* p, size_t bytes) {
 
 int threads_for(size_t bytes) {
   const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-  const size_t by_size = (bytes + 4 * kChunk - 1) / (4 * kChunk);
-  return int(std::max<size_t>(1, std::min<size_t>({size_t(kMaxThreads), size_t(hw), by_size})));
+  const size_t by_size = (bytes + 4 * g_chunk - 1) / (4 * g_chunk);
+  return int(std::max<size_t>(1, std::min<size_t>({size_t(g_max_threads), size_t(hw), by_size})));
 }
 
 // dir 0: device -> host, 1: host -> device.  `after` orders the lanes after
@@ -106,15 +112,15 @@ int staged(int dir, void* host, void* dev, size_t bytes, int device, cudaStream_
       size_t off = lo;
       int k = 0;
       if (off < hi) {
-        const size_t n = std::min(kChunk, hi - off);
+        const size_t n = std::min(g_chunk, hi - off);
         e = e ? e : cudaMemcpyAsync(l.buf[0], d + off, n, cudaMemcpyDeviceToHost, l.stream);
         e = e ? e : cudaEventRecord(l.done[0], l.stream);
       }
       while (off < hi && !e) {
-        const size_t n = std::min(kChunk, hi - off);
+        const size_t n = std::min(g_chunk, hi - off);
         const size_t nxt = off + n;
         if (nxt < hi) {
-          const size_t m = std::min(kChunk, hi - nxt);
+          const size_t m = std::min(g_chunk, hi - nxt);
           e = cudaMemcpyAsync(l.buf[k ^ 1], d + nxt, m, cudaMemcpyDeviceToHost, l.stream);
           e = e ? e : cudaEventRecord(l.done[k ^ 1], l.stream);
         }
@@ -127,8 +133,8 @@ int staged(int dir, void* host, void* dev, size_t bytes, int device, cudaStream_
       // host copies chunk k into a buffer while chunk k-1 is in flight
       int k = 0;
       bool used[2] = {false, false};
-      for (size_t off = lo; off < hi && !e; off += kChunk, k ^= 1) {
-        const size_t n = std::min(kChunk, hi - off);
+      for (size_t off = lo; off < hi && !e; off += g_chunk, k ^= 1) {
+        const size_t n = std::min(g_chunk, hi - off);
         if (used[k]) e = cudaEventSynchronize(l.done[k]);
         if (e) break;
         std::memcpy(l.buf[k], h + off, n);
@@ -151,6 +157,25 @@ int staged(int dir, void* host, void* dev, size_t bytes, int device, cudaStream_
 }
 
 }  // namespace
+
+// allocate the pinned lanes ahead of the first large transfer (engine
+// creation does this for blocks whose state is large)
+int hostcopy_reserve(int device) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  return lanes_for(device);
+}
+
+int hostcopy_tune(int knob, int value) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  if (value <= 0) return fail(SLBM_ECONFIG, "host copy tuning value must be positive");
+  if (knob == 10) {
+    drop_lanes();
+    g_chunk = size_t(value) << 20;
+  } else {
+    g_max_threads = std::min(value, kMaxLanes);
+  }
+  return SLBM_OK;
+}
 
 int copy_d2h(void* host, const void* dev, size_t bytes, int device, cudaStream_t s) {
   if (!bytes) return SLBM_OK;

@@ -53,7 +53,7 @@ def algorithmic_bytes(name, n_cells):
     q = 27 if "D3Q27" in name else (9 if "D2Q9" in name else 19)
     if "aa_odd" in name:
         return 2 * q * 8 * n_cells
-    if "aa_even" in name or "pull" in name:
+    if "aa_even" in name or "pull" in name or "index_sweep" in name:
         return (2 * q * 8 + (q - 1) * 4) * n_cells
     return None
 
@@ -84,7 +84,8 @@ def main():
             f"{m['sm__warps_active.avg.pct_of_peak_sustained_active']:.1f}/"
             f"{m['sm__maximum_warps_per_active_cycle_pct']:.1f} | {m['lts__t_sector_hit_rate.pct']:.1f} | "
             f"{m['sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active']:.1f} |")
-        key = "k_aa_even" if "aa_even" in name else ("k_aa_odd" if "aa_odd" in name else short)
+        idx_sweep = "aa_even" in name or "index_sweep" in name
+        key = "k_aa_even" if idx_sweep else ("k_aa_odd" if "aa_odd" in name else short)
         traffic.setdefault(key, []).append(tot)
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     with open(os.path.join(ROOT, "profiles", f"{tag}_kernels.md"), "w") as fh:
