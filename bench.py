@@ -370,7 +370,7 @@ def impl_ours(args, rank, world, local_rank):
                         f"seed {SEED})",
             "n_fluid_per_gpu": eng.n_fluid,
             "porosity": round(eng.n_fluid / EDGE**3, 4),
-            "decomposition": f"{world}x1x1 blocks of {EDGE}^3",
+            "decomposition": f"1x1x{world} z slabs of {EDGE}^3" if world > 1 else f"1 block of {EDGE}^3",
             "l2": "inputs larger than L2 (PDF + index list ~9 GB per GPU)",
             "build_s": round(build_s, 2),
             "omega": OMEGA,

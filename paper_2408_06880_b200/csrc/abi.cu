@@ -76,7 +76,7 @@ void free_engine(SlbmEngine* e) {
     if (gx) cudaGraphExecDestroy(gx);
   void* ptrs[] = {e->pdf,         e->tmp,          e->idx,       e->x_flat,
                   e->cid_map,     e->ubb_slot,     e->ubb_partner, e->ubb_corr,
-                  e->ghost_key,   e->interior_cids, e->frame_cids, e->d_bad,
+                  e->ghost_key,   e->frame_cids,   e->frame_bits, e->d_bad,
                   e->out_slot,    e->out_partner,  e->out_cell,  e->out_dir,
                   e->out_rho,     e->out_u,        e->dense_mask,
                   e->dense_ubb_key, e->dense_ubb_corr,
@@ -187,7 +187,9 @@ static int create_engine(int layout, const uint8_t* tags_pad, const double* ubb_
     if (dims[a] < 1) return fail(SLBM_ECONFIG, "all extents must be positive");
   if (frame_width)
     for (int a = 0; a < dim; ++a)
-      if (frame_width[a] < 1) return fail(SLBM_ECONFIG, "frame widths must be >= 1");
+      // 0 = no frame on that axis (used for axes without halo exchange;
+      // the reference's frame_mask requires >= 1, enforced by the host layer)
+      if (frame_width[a] < 0) return fail(SLBM_ECONFIG, "frame widths must be >= 0");
 
   DeviceGuard guard(device);
   SlbmEngine* e = new SlbmEngine();
@@ -396,16 +398,20 @@ int slbm_export_split(const SlbmEngine* e, int64_t* interior, int64_t* frame) {
   CHECK_ENGINE(e);
   if (!e->has_split) return fail(SLBM_ECONFIG, "engine has no split lists; build with frame_width");
   DeviceGuard guard(e->device);
-  std::vector<uint32_t> a(size_t(std::max<int64_t>(e->n_interior, 1))),
-      b(size_t(std::max<int64_t>(e->n_frame, 1)));
-  if (e->n_interior)
-    SLBM_CUDA_TRY(cudaMemcpy(a.data(), e->interior_cids, e->n_interior * 4, cudaMemcpyDeviceToHost));
+  std::vector<uint32_t> b(size_t(std::max<int64_t>(e->n_frame, 1)));
   if (e->n_frame)
     SLBM_CUDA_TRY(cudaMemcpy(b.data(), e->frame_cids, e->n_frame * 4, cudaMemcpyDeviceToHost));
-  if (interior)
-    for (int64_t i = 0; i < e->n_interior; ++i) interior[i] = a[i];
   if (frame)
     for (int64_t i = 0; i < e->n_frame; ++i) frame[i] = b[i];
+  if (interior) {  // the complement of the (sorted) frame list
+    int64_t k = 0, j = 0;
+    for (int64_t c = 0; c < e->n_fluid; ++c) {
+      if (j < e->n_frame && int64_t(b[j]) == c)
+        ++j;
+      else
+        interior[k++] = c;
+    }
+  }
   return SLBM_OK;
 }
 

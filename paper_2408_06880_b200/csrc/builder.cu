@@ -94,6 +94,17 @@ struct InFrame {
   }
 };
 
+// one bit per cell, set for frame cells: the interior sweep runs over all
+// cells in cid order and skips the set bits (one broadcast word per warp)
+// instead of reading an explicit interior cell list (4 B/cell + a dependent
+// load in front of the index list)
+__global__ void k_frame_bits(InFrame fr, int64_t n, uint32_t* bits) {
+  const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool in = c < n && fr(uint32_t(c));
+  const unsigned word = __ballot_sync(0xffffffffu, in);
+  if ((threadIdx.x & 31) == 0 && c < n) bits[c >> 5] = word;
+}
+
 __global__ void k_cid_map(const uint32_t* x_flat, int64_t n, int32_t* cid_map) {
   int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) cid_map[x_flat[i]] = int32_t(i);
@@ -567,19 +578,35 @@ int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
       int32_t w = a < g.dim ? frame_width[a] : 1;
       fr.w[a] = std::min<int32_t>(w, g.n[a]);
     }
-    int64_t nf = 0, ni = 0;
+    // frame: explicit cell list; interior: the complement, as a bitmask
+    int64_t nf = 0;
     SLBM_TRY(select_if(thrust::counting_iterator<uint32_t>(0), sel_buf, n, fr, &nf, s));
     SLBM_TRY(dalloc(e, &e->frame_cids, nf));
     SLBM_CUDA_TRY(cudaMemcpyAsync(e->frame_cids, sel_buf, nf * sizeof(uint32_t),
                                   cudaMemcpyDeviceToDevice, s));
-    fr.want = false;
-    SLBM_TRY(select_if(thrust::counting_iterator<uint32_t>(0), sel_buf, n, fr, &ni, s));
-    SLBM_TRY(dalloc(e, &e->interior_cids, ni));
-    SLBM_CUDA_TRY(cudaMemcpyAsync(e->interior_cids, sel_buf, ni * sizeof(uint32_t),
-                                  cudaMemcpyDeviceToDevice, s));
     e->n_frame = nf;
-    e->n_interior = ni;
+    e->n_interior = n - nf;
     e->has_split = true;
+    // frame = a cid prefix + a cid suffix (faces only across z, e.g. slab
+    // decompositions): the interior is one contiguous cid range and needs
+    // no mask at all
+    std::vector<uint32_t> h(size_t(std::max<int64_t>(nf, 1)));
+    if (nf)
+      SLBM_CUDA_TRY(cudaMemcpyAsync(h.data(), e->frame_cids, nf * 4, cudaMemcpyDeviceToHost, s));
+    SLBM_CUDA_TRY(cudaStreamSynchronize(s));
+    int64_t lo = 0;
+    while (lo < nf && int64_t(h[lo]) == lo) ++lo;
+    const int64_t hi = n - (nf - lo);
+    bool ranged = true;
+    for (int64_t k = lo; k < nf && ranged; ++k) ranged = int64_t(h[k]) == hi + (k - lo);
+    if (ranged) {
+      e->interior_lo = lo;
+    } else {
+      e->interior_lo = -1;
+      SLBM_TRY(dalloc(e, &e->frame_bits, (n + 31) / 32));
+      k_frame_bits<<<grid_for(n, 256), 256, 0, s>>>(fr, n, e->frame_bits);
+      SLBM_CUDA_TRY(cudaGetLastError());
+    }
   }
   SLBM_CUDA_TRY(cudaStreamSynchronize(s));
   cleanup();

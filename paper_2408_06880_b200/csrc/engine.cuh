@@ -46,8 +46,9 @@ struct SlbmEngine {
   double* out_u = nullptr;          // 3 x n_out, velocity kept EVEN -> ODD
   uint64_t* ghost_key = nullptr;  // per q sorted (sigma_key << 32 | pflat)
   std::vector<uint64_t> ghost_key_host;
-  uint32_t* interior_cids = nullptr;
   uint32_t* frame_cids = nullptr;
+  uint32_t* frame_bits = nullptr;  // bit c set <=> cell c is a frame cell
+  int64_t interior_lo = -1;        // >= 0: interior = cids [lo, lo + n_interior), no mask
   unsigned long long* d_bad = nullptr;   // first unstable step (ULLONG_MAX = none)
   unsigned long long* d_step = nullptr;  // step counter read by the sweeps
   double* d_scratch = nullptr;           // staging for host transfers

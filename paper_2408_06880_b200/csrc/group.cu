@@ -24,6 +24,8 @@ struct GroupArgs {
   double* dst;
   const uint32_t* idx;
   const uint32_t* cids;
+  const uint32_t* skip;  // interior: identity order minus the frame bits
+  uint32_t offset;       // identity sweeps: first cell (contiguous interior)
   uint32_t n_cells;
   uint32_t n_fluid;
   uint32_t base[28];
@@ -80,7 +82,8 @@ __global__ void __launch_bounds__(kGB, 4) k_group(const GroupArgs* table, const 
   __syncthreads();
   const uint32_t i = (blockIdx.x - first) * kGB + threadIdx.x;
   if (i >= a.n_cells) return;
-  const uint32_t c = a.cids ? a.cids[i] : i;
+  const uint32_t c = a.cids ? a.cids[i] : a.offset + i;
+  if (a.skip && ((__ldg(a.skip + (c >> 5)) >> (c & 31)) & 1u)) return;
   double t[L::Q];
   double* pdf = a.pdf;
   bool bad;
@@ -97,8 +100,12 @@ __global__ void __launch_bounds__(kGB, 4) k_group(const GroupArgs* table, const 
     sfor<1, L::Q>([&](auto q) { s[q] = __ldcs(a.idx + size_t(q - 1) * a.n_fluid + c); });
     sfor<0, L::Q>([&](auto q) { t[q] = pdf[s[q]]; });
     // index-list rows of this engine's CTA `ahead` positions later (sweep.cuh)
-    prefetch_idx_ahead<L::Q - 1, kGB>(a.idx, a.n_fluid, a.cids, a.n_cells,
-                                      (blockIdx.x - first) * kGB, ahead);
+    if (a.cids)
+      prefetch_idx_ahead<L::Q - 1, kGB>(a.idx, a.n_fluid, a.cids, a.n_cells,
+                                        (blockIdx.x - first) * kGB, ahead);
+    else
+      prefetch_idx_ahead<L::Q - 1, kGB>(a.idx, a.n_fluid, nullptr, a.offset + a.n_cells,
+                                        a.offset + (blockIdx.x - first) * kGB, ahead);
     if constexpr (KIND == 1) {  // AA even (sparse.py:264-271)
       bad = collide<L, MODEL>(t, omega, lam, [&](auto q, double v) {
         constexpr int qb = L::INV[decltype(q)::value];
@@ -147,11 +154,19 @@ GroupArgs args_of(SlbmEngine* e, int phase, int flip) {
   a.dst = e->pattern == SLBM_PULL ? bufs[1 - flip] : nullptr;
   a.idx = e->idx;
   a.n_fluid = uint32_t(e->n_fluid);
-  a.cids = phase == SLBM_PHASE_INTERIOR ? e->interior_cids
-                                        : (phase == SLBM_PHASE_FRAME ? e->frame_cids : nullptr);
-  a.n_cells = uint32_t(phase == SLBM_PHASE_INTERIOR ? e->n_interior
-                                                    : (phase == SLBM_PHASE_FRAME ? e->n_frame
-                                                                                 : e->n_fluid));
+  a.cids = phase == SLBM_PHASE_FRAME ? e->frame_cids : nullptr;
+  a.skip = nullptr;
+  a.offset = 0;
+  a.n_cells = uint32_t(phase == SLBM_PHASE_FRAME ? e->n_frame : e->n_fluid);
+  if (phase == SLBM_PHASE_INTERIOR) {
+    if (e->interior_lo >= 0) {
+      a.offset = uint32_t(e->interior_lo);
+      a.n_cells = uint32_t(e->n_interior);
+    } else {
+      a.skip = e->frame_bits;
+      if (e->n_interior == 0) a.n_cells = 0;
+    }
+  }
   for (int q = 0; q <= e->q && q < 28; ++q) a.base[q] = uint32_t(e->base[q]);
   a.bad = e->d_bad;
   a.step = e->d_step;

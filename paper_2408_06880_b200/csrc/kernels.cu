@@ -29,7 +29,9 @@ struct SweepArgs {
   double* pdf;
   double* dst;
   const uint32_t* idx;
-  const uint32_t* cids;  // nullptr: identity (whole block)
+  const uint32_t* cids;  // nullptr: cell = offset + position
+  const uint32_t* skip;  // identity sweep minus the cells whose bit is set (interior)
+  uint32_t offset;       // first cell of an identity sweep (contiguous interior)
   uint32_t n_cells;
   uint32_t n_fluid;
   uint32_t base[28];
@@ -46,6 +48,7 @@ constexpr int kIB = 128;     // index-list sweeps: 128-thread CTAs, 4 per SM
 __device__ __forceinline__ void flag_bad(const SweepArgs& a) {
   atomicMin(a.bad, *a.step);
 }
+
 
 // tuning knobs (slbm_set_tuning), kept for tools/variants.py
 int g_even_variant = 0;     // knob 0: 0 = production, 1 = no idx prefetch, 2 = probe
@@ -74,15 +77,21 @@ __global__ void __launch_bounds__(kIB, MINB) k_index_sweep(const SweepArgs a, ui
   const uint32_t first = blockIdx.x * kIB;
   if constexpr (PF) {
     if (a.cids == nullptr)
-      prefetch_idx_ahead<L::Q - 1, kIB>(a.idx, a.n_fluid, nullptr, a.n_cells, first, ahead);
+      prefetch_idx_ahead<L::Q - 1, kIB>(a.idx, a.n_fluid, nullptr, a.offset + a.n_cells,
+                                        a.offset + first, ahead);
   }
   const uint32_t i = first + threadIdx.x;
   if (i >= a.n_cells) return;
-  const uint32_t c = a.cids ? a.cids[i] : i;
+  const uint32_t c = a.cids ? a.cids[i] : a.offset + i;
   uint32_t s[L::Q];
   double t[L::Q];
   s[0] = c;
+  // the skip word (interior sweep) is loaded alongside the index list, not
+  // in front of it: a frame cell reads its idx row for nothing (~1% extra)
+  // but no cell waits for the mask before its own loads start
+  const uint32_t skip_word = a.skip ? __ldg(a.skip + (c >> 5)) : 0u;
   sfor<1, L::Q>([&](auto q) { s[q] = __ldcs(a.idx + size_t(q - 1) * a.n_fluid + c); });
+  if ((skip_word >> (c & 31)) & 1u) return;
   sfor<0, L::Q>([&](auto q) { t[q] = a.pdf[s[q]]; });
   if constexpr (PF) {
     if (a.cids != nullptr)
@@ -125,7 +134,8 @@ template <class L, int MODEL, int MINB>
 __global__ void __launch_bounds__(kBlock, MINB) k_aa_odd(const SweepArgs a) {
   const uint32_t i = blockIdx.x * kBlock + threadIdx.x;
   if (i >= a.n_cells) return;
-  const uint32_t c = a.cids ? a.cids[i] : i;
+  const uint32_t c = a.cids ? a.cids[i] : a.offset + i;
+  if (a.skip && ((__ldg(a.skip + (c >> 5)) >> (c & 31)) & 1u)) return;
   double t[L::Q];
   sfor<0, L::Q>([&](auto q) {
     constexpr int qb = L::INV[q];
@@ -394,8 +404,13 @@ int launch_step(SlbmEngine* e, int phase) {
   if (e->layout) return dense_step(e, phase);
   SweepArgs a = sweep_args(e);
   if (phase == SLBM_PHASE_INTERIOR) {
-    a.cids = e->interior_cids;
-    a.n_cells = uint32_t(e->n_interior);
+    if (e->interior_lo >= 0) {  // one contiguous cid range
+      a.offset = uint32_t(e->interior_lo);
+      a.n_cells = uint32_t(e->n_interior);
+    } else {  // all cells minus the frame (identity order)
+      a.skip = e->frame_bits;
+      if (e->n_interior == 0) a.n_cells = 0;
+    }
   } else if (phase == SLBM_PHASE_FRAME) {
     a.cids = e->frame_cids;
     a.n_cells = uint32_t(e->n_frame);

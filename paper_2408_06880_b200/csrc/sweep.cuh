@@ -20,19 +20,20 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 // and only the gather goes to DRAM.  Same DRAM bytes (the rows are read
 // once either way), ~+7-9% sweep bandwidth measured (profiles/r01_*).
 //
-// `first` is the sweep position of this CTA's first cell; with a cell list
-// (interior / frame sweeps) the future CTA's first cell id of each 32-cell
-// run is read from `cids` (call after the own gathers are issued, so that
-// dependent load overlaps them).
+// Positions are sweep positions: with a cell list (frame sweeps) they index
+// `cids` (the future CTA's first cell id of each 32-cell run is read from
+// it; call after the own gathers are issued, so that dependent load overlaps
+// them), without one they are cell ids.  `first` is this CTA's first
+// position, `end` one past the sweep's last.
 template <int QM1, int BLOCK>
 __device__ __forceinline__ void prefetch_idx_ahead(const uint32_t* idx, uint32_t n_fluid,
-                                                   const uint32_t* cids, uint32_t n_cells,
+                                                   const uint32_t* cids, uint32_t end,
                                                    uint32_t first, uint32_t ahead) {
   constexpr int kLines = BLOCK * 4 / 128;
   if (threadIdx.x >= QM1 * kLines) return;
   const uint32_t row = threadIdx.x / kLines, line = threadIdx.x % kLines;
   const uint32_t pos = first + ahead * BLOCK + line * 32;
-  if (pos >= n_cells) return;
+  if (pos >= end) return;
   const uint32_t cell = cids ? __ldcs(cids + pos) : pos;
   prefetch_l2(idx + size_t(row) * n_fluid + cell);
 }

@@ -250,8 +250,8 @@ class Domain:
             # hybrid picks dense at or above phi_s (domain.py:58-65, :109-114)
             blk.kind = classify_kind(blk.porosity, policy, phi_s)
             if blk.rank == self.rank:
-                blk.engine = make_engine(blk.flags, stencil, params, pattern, frame_width,
-                                         self.device, blk.kind)
+                blk.engine = make_engine(blk.flags, stencil, params, pattern,
+                                         self._block_frame(frame_width), self.device, blk.kind)
         engines = self.local_engines()
         self._stream = engines[0].stream() if engines and hasattr(engines[0], "stream") else 0
         for e in engines[1:]:
@@ -272,6 +272,16 @@ class Domain:
         self._group = self._build_group() if engine_factory is None else None
         self.overlap_samples: list[tuple[float, float]] = []
         self.steps_done = 0
+
+    def _block_frame(self, frame_width):
+        """``frame_width="halo"`` (extension): width 1 only on axes with more
+        than one block, 0 on axes every block wraps or spans alone (no halo
+        there).  Anything else is passed through with the reference's rules."""
+        if not (isinstance(frame_width, str) and frame_width == "halo"):
+            return frame_width
+        from .engine import HaloWidths
+
+        return HaloWidths(1 if g > 1 else 0 for g in self.grid)
 
     def _build_group(self):
         """Batched block-table execution when this rank owns
@@ -716,7 +726,7 @@ class DistributedDomain(Domain):
     through the library's own communicator (``transport="nccl"``), or host
     staging over a gloo group (``transport="host"``)."""
 
-    def __init__(self, global_flags, block_size, stencil, params, pattern="aa", frame_width=1,
+    def __init__(self, global_flags, block_size, stencil, params, pattern="aa", frame_width="halo",
                  rank: int | None = None, world: int | None = None, device: int | None = None,
                  assignment=None, check: str = "deferred", comm=None, transport: str = "nccl",
                  engine_factory=None, halo_factory=None, loopback: bool = False):
@@ -758,17 +768,24 @@ class DistributedDomain(Domain):
     @classmethod
     def weak_scaling_bed(cls, block_edge, world, rank, stencil, params, porosity, diameter, seed,
                          device=None, transport="nccl"):
-        """world blocks of ``block_edge`` along x, fully periodic
-        overlapping-sphere bed over the whole box, block i on rank i."""
+        """world slabs of ``block_edge`` stacked along z, fully periodic
+        overlapping-sphere bed over the whole box, slab i on rank i.
+
+        Slabs along z: each block exchanges with its two z neighbours only
+        (one message per peer per phase over NVSwitch), x and y wrap inside
+        the block, and with ``frame_width="halo"`` the frame is two whole z
+        planes — a contiguous cid prefix and suffix — so the interior sweep
+        is one cid range and the frame sweep stays coalesced."""
         from .geometry import packed_bed_flags
 
         bx, by, bz = block_edge
-        dims = (bx * world, by, bz)
+        dims = (bx, by, bz * world)
         fl = packed_bed_flags(dims, porosity, diameter, seed, periodic=True,
                               device=default_device() if device is None else device)
         assignment = {i: i for i in range(world)}
-        return cls(fl, (bx, by, bz), stencil, params, pattern="aa", frame_width=1, rank=rank,
-                   world=world, device=device, assignment=assignment, transport=transport)
+        return cls(fl, (bx, by, bz), stencil, params, pattern="aa", frame_width="halo",
+                   rank=rank, world=world, device=device, assignment=assignment,
+                   transport=transport)
 
     def run(self, steps: int, driver: str = "overlapped", use_graph: bool = False) -> None:
         super().run(steps, driver, use_graph)

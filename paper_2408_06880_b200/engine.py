@@ -44,9 +44,26 @@ def default_device() -> int:
     return 0
 
 
+class HaloWidths(tuple):
+    """Per-axis frame widths that may contain 0 = no frame on that axis.
+
+    The reference's ``frame_mask`` requires every width >= 1 (flags.py:83-108)
+    and so does this layer for plain ints/tuples.  The domain drivers use
+    this type for blocks whose axes have no halo exchange (in-block periodic
+    wrap or a single block along the axis): those faces need no frame, and
+    dropping them leaves a frame of whole z planes whose cells are
+    contiguous in cid order (profiles: x faces make the frame sweep a
+    scattered gather)."""
+
+
 def _widths(frame_width, dim):
     if frame_width is None:
         return None
+    if isinstance(frame_width, HaloWidths):
+        widths = tuple(int(w) for w in frame_width)
+        if len(widths) != dim or min(widths) < 0:
+            raise errors.make("ConfigurationError", f"bad halo frame widths {widths}")
+        return widths
     if isinstance(frame_width, (int, np.integer)):
         widths = (int(frame_width),) * dim
     else:

@@ -134,3 +134,32 @@ def test_graph_replay_matches_python_driver(pattern, loopback, gpu_lib):
     np.testing.assert_array_equal(doms[0].gather_canonical(), doms[1].gather_canonical())
     assert doms[0].counters().as_dict() == doms[1].counters().as_dict()
     assert doms[0].steps_done == doms[1].steps_done == 12
+
+
+@pytest.mark.parametrize("pattern", ["aa", "pull"])
+def test_halo_frame_slabs_match_sequential(pattern, gpu_lib):
+    """frame_width="halo" on a z-slab decomposition (the weak-scaling
+    layout): x/y wrap in-block, the frame is whole z planes, and the
+    overlapped driver (loopback NCCL) equals the sequential single-block run."""
+    from paper_2408_06880_b200 import geometry
+    from paper_2408_06880_b200.collision import CollisionParams
+    from paper_2408_06880_b200.domain import Domain, DistributedDomain
+    from paper_2408_06880_b200.lattice import make_stencil
+
+    st = make_stencil("d3q19")
+    gf = geometry.packed_bed_flags((16, 12, 24), 0.5, 5.0, 3, periodic=True)
+    p = CollisionParams(1.2, "trt", 0.94)
+    ref = Domain(gf, (16, 12, 24), st, p, pattern=pattern)
+    ref.init_random(2)
+    ref.run(6)
+    d = DistributedDomain(gf, (16, 12, 8), st, p, pattern=pattern, rank=0, world=1, device=0,
+                          loopback=True)
+    assert d.frame_width == "halo"
+    for e in d.local_engines():
+        interior, frame = e.split_lists()
+        z = e.fluid_coords[frame, 2]
+        assert np.all((z == 0) | (z == 7))
+        assert np.array_equal(interior, np.arange(interior[0], interior[-1] + 1))
+    d.init_random(2)
+    d.run(6, driver="overlapped")
+    np.testing.assert_array_equal(d.gather_canonical(), ref.gather_canonical())

@@ -242,6 +242,47 @@ def test_interior_plus_frame_composes_bitwise(pattern, gpu_lib):
     assert split.n_interior + split.n_frame == split.n_fluid
 
 
+@pytest.mark.parametrize("widths", [(0, 0, 1), (0, 0, 2), (1, 0, 0), (0, 2, 1), (0, 0, 0)])
+@pytest.mark.parametrize("pattern", ["pull", "aa"])
+def test_halo_frame_widths(widths, pattern, gpu_lib):
+    """HaloWidths (0 = no frame on that axis, domain-driver extension):
+    frame = cells within the width of the faces of the non-zero axes;
+    z-only frames are a cid prefix + suffix (contiguous interior range),
+    others use the frame bitmask; either way interior + frame == whole."""
+    from paper_2408_06880_b200 import errors, geometry
+    from paper_2408_06880_b200.collision import CollisionParams
+    from paper_2408_06880_b200.engine import HaloWidths
+    from paper_2408_06880_b200.lattice import make_stencil
+
+    st = make_stencil("d3q19")
+    fl = geometry.packed_bed_flags((20, 16, 12), 0.6, 5.0, 2, periodic=True)
+    p = CollisionParams(1.3, "trt", 0.8)
+    v = seed_values(fl, st, 5)
+    whole = _engine(fl, st, p, pattern)
+    split = _engine(fl, st, p, pattern, frame_width=HaloWidths(widths))
+    coords = split.fluid_coords
+    want = np.zeros(split.n_fluid, bool)
+    for a, w in enumerate(widths):
+        if w:
+            want |= (coords[:, a] < w) | (coords[:, a] >= fl.dims[a] - w)
+    interior, frame = split.split_lists()
+    np.testing.assert_array_equal(frame, np.flatnonzero(want))
+    np.testing.assert_array_equal(interior, np.flatnonzero(~want))
+    whole.init_canonical(v)
+    split.init_canonical(v)
+    for _ in range(4):
+        whole.refresh_boundary(whole.parity)
+        whole.step("all")
+        whole.finish_step()
+        split.refresh_boundary(split.parity)
+        split.step("interior")
+        split.step("frame")
+        split.finish_step()
+    np.testing.assert_array_equal(whole.canonical_state(), split.canonical_state())
+    with pytest.raises(errors.ConfigurationError):
+        _engine(fl, st, p, pattern, frame_width=(0, 0, 1))  # reference rule: >= 1
+
+
 def test_errors(gpu_lib):
     from paper_2408_06880_b200 import errors, geometry
     from paper_2408_06880_b200.collision import CollisionParams
