@@ -59,7 +59,7 @@ namespace {
 
 constexpr int kGB = 128;
 
-__device__ __forceinline__ int find_engine(const uint32_t* start, int n, uint32_t cta) {
+__device__ __forceinline__ int find_engine(const uint32_t* __restrict__ start, int n, uint32_t cta) {
   int lo = 0, hi = n;  // last e with start[e] <= cta
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
@@ -72,17 +72,34 @@ __device__ __forceinline__ int find_engine(const uint32_t* start, int n, uint32_
 }
 
 template <class L, int MODEL, int KIND>
-__global__ void __launch_bounds__(kGB, 4) k_group(const GroupArgs* table, const uint32_t* start,
-                                                  int n_eng, double omega, double lam,
-                                                  uint32_t ahead) {
-  __shared__ GroupArgs a;
-  if (threadIdx.x == 0) a = table[find_engine(start, n_eng, blockIdx.x)];
-  __shared__ uint32_t first;
-  if (threadIdx.x == 0) first = start[find_engine(start, n_eng, blockIdx.x)];
-  __syncthreads();
-  const uint32_t i = (blockIdx.x - first) * kGB + threadIdx.x;
-  if (i >= a.n_cells) return;
-  const uint32_t c = a.cids ? a.cids[i] : a.offset + i;
+__global__ void __launch_bounds__(kGB, KIND == 2 ? 6 : 4) k_group(const GroupArgs* __restrict__ table,
+                                                  const uint32_t* __restrict__ start, int n_eng,
+                                                  double omega, double lam, uint32_t ahead) {
+  // every thread finds its engine and reads the (tiny, L1-resident) table
+  // row itself: no single-thread staging + __syncthreads at CTA start, which
+  // cost ~15% of the even sweep (measured, tools/slab_probe.py)
+  const int eng = find_engine(start, n_eng, blockIdx.x);
+  const uint32_t first = start[eng];
+  // the odd sweep addresses 2Q group rows through base[]: staged in shared
+  // memory those offsets stay out of registers (77 vs 128 + spills)
+  __shared__ GroupArgs staged;
+  if constexpr (KIND == 2) {
+    if (threadIdx.x == 0) staged = table[eng];
+    __syncthreads();
+  }
+  const GroupArgs& a = KIND == 2 ? staged : table[eng];
+  const uint32_t pos0 = (blockIdx.x - first) * kGB;  // this CTA's first sweep position
+  const uint32_t* idx = a.idx;
+  const uint32_t* cids = a.cids;
+  const uint32_t n_fluid = a.n_fluid, n_cells = a.n_cells, offset = a.offset;
+  // index-list rows of this engine's CTA `ahead` positions later (sweep.cuh),
+  // issued first as in the single-engine sweep
+  if (KIND != 2 && cids == nullptr)
+    prefetch_idx_ahead<L::Q - 1, kGB>(idx, n_fluid, nullptr, offset + n_cells, offset + pos0,
+                                      ahead);
+  const uint32_t i = pos0 + threadIdx.x;
+  if (i >= n_cells) return;
+  const uint32_t c = cids ? cids[i] : offset + i;
   if (a.skip && ((__ldg(a.skip + (c >> 5)) >> (c & 31)) & 1u)) return;
   double t[L::Q];
   double* pdf = a.pdf;
@@ -97,15 +114,9 @@ __global__ void __launch_bounds__(kGB, 4) k_group(const GroupArgs* table, const 
   } else {
     uint32_t s[L::Q];
     s[0] = c;
-    sfor<1, L::Q>([&](auto q) { s[q] = __ldcs(a.idx + size_t(q - 1) * a.n_fluid + c); });
+    sfor<1, L::Q>([&](auto q) { s[q] = __ldcs(idx + size_t(q - 1) * n_fluid + c); });
     sfor<0, L::Q>([&](auto q) { t[q] = pdf[s[q]]; });
-    // index-list rows of this engine's CTA `ahead` positions later (sweep.cuh)
-    if (a.cids)
-      prefetch_idx_ahead<L::Q - 1, kGB>(a.idx, a.n_fluid, a.cids, a.n_cells,
-                                        (blockIdx.x - first) * kGB, ahead);
-    else
-      prefetch_idx_ahead<L::Q - 1, kGB>(a.idx, a.n_fluid, nullptr, a.offset + a.n_cells,
-                                        a.offset + (blockIdx.x - first) * kGB, ahead);
+    if (cids) prefetch_idx_ahead<L::Q - 1, kGB>(idx, n_fluid, cids, n_cells, pos0, ahead);
     if constexpr (KIND == 1) {  // AA even (sparse.py:264-271)
       bad = collide<L, MODEL>(t, omega, lam, [&](auto q, double v) {
         constexpr int qb = L::INV[decltype(q)::value];
