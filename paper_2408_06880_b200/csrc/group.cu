@@ -25,7 +25,8 @@ struct GroupArgs {
   const uint32_t* idx;
   const uint32_t* cids;
   const uint32_t* skip;  // interior: identity order minus the frame bits
-  uint32_t offset;       // identity sweeps: first cell (contiguous interior)
+  uint32_t offset;       // identity sweeps: first cell (contiguous interior), warp aligned
+  uint32_t lo;           // cells below lo are skipped
   uint32_t n_cells;
   uint32_t n_fluid;
   uint32_t base[28];
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(kGB, KIND == 2 ? 6 : 4) k_group(const GroupArg
   const uint32_t i = pos0 + threadIdx.x;
   if (i >= n_cells) return;
   const uint32_t c = cids ? cids[i] : offset + i;
-  if (a.skip && ((__ldg(a.skip + (c >> 5)) >> (c & 31)) & 1u)) return;
+  if (c < a.lo || (a.skip && ((__ldg(a.skip + (c >> 5)) >> (c & 31)) & 1u))) return;
   double t[L::Q];
   double* pdf = a.pdf;
   bool bad;
@@ -168,11 +169,13 @@ GroupArgs args_of(SlbmEngine* e, int phase, int flip) {
   a.cids = phase == SLBM_PHASE_FRAME ? e->frame_cids : nullptr;
   a.skip = nullptr;
   a.offset = 0;
+  a.lo = 0;
   a.n_cells = uint32_t(phase == SLBM_PHASE_FRAME ? e->n_frame : e->n_fluid);
   if (phase == SLBM_PHASE_INTERIOR) {
     if (e->interior_lo >= 0) {
-      a.offset = uint32_t(e->interior_lo);
-      a.n_cells = uint32_t(e->n_interior);
+      a.lo = uint32_t(e->interior_lo);
+      a.offset = a.lo & ~31u;
+      a.n_cells = uint32_t(e->interior_lo + e->n_interior) - a.offset;
     } else {
       a.skip = e->frame_bits;
       if (e->n_interior == 0) a.n_cells = 0;

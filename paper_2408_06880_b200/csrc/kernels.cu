@@ -31,7 +31,9 @@ struct SweepArgs {
   const uint32_t* idx;
   const uint32_t* cids;  // nullptr: cell = offset + position
   const uint32_t* skip;  // identity sweep minus the cells whose bit is set (interior)
-  uint32_t offset;       // first cell of an identity sweep (contiguous interior)
+  uint32_t offset;       // first cell of an identity sweep (contiguous interior),
+                         // rounded down to a warp boundary; cells below `lo` are skipped
+  uint32_t lo;
   uint32_t n_cells;
   uint32_t n_fluid;
   uint32_t base[28];
@@ -83,6 +85,7 @@ __global__ void __launch_bounds__(kIB, MINB) k_index_sweep(const SweepArgs a, ui
   const uint32_t i = first + threadIdx.x;
   if (i >= a.n_cells) return;
   const uint32_t c = a.cids ? a.cids[i] : a.offset + i;
+  if (c < a.lo) return;
   uint32_t s[L::Q];
   double t[L::Q];
   s[0] = c;
@@ -135,7 +138,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_aa_odd(const SweepArgs a) {
   const uint32_t i = blockIdx.x * kBlock + threadIdx.x;
   if (i >= a.n_cells) return;
   const uint32_t c = a.cids ? a.cids[i] : a.offset + i;
-  if (a.skip && ((__ldg(a.skip + (c >> 5)) >> (c & 31)) & 1u)) return;
+  if (c < a.lo || (a.skip && ((__ldg(a.skip + (c >> 5)) >> (c & 31)) & 1u))) return;
   double t[L::Q];
   sfor<0, L::Q>([&](auto q) {
     constexpr int qb = L::INV[q];
@@ -404,9 +407,10 @@ int launch_step(SlbmEngine* e, int phase) {
   if (e->layout) return dense_step(e, phase);
   SweepArgs a = sweep_args(e);
   if (phase == SLBM_PHASE_INTERIOR) {
-    if (e->interior_lo >= 0) {  // one contiguous cid range
-      a.offset = uint32_t(e->interior_lo);
-      a.n_cells = uint32_t(e->n_interior);
+    if (e->interior_lo >= 0) {  // one contiguous cid range, warps aligned to 32 cells
+      a.lo = uint32_t(e->interior_lo);
+      a.offset = a.lo & ~31u;
+      a.n_cells = uint32_t(e->interior_lo + e->n_interior) - a.offset;
     } else {  // all cells minus the frame (identity order)
       a.skip = e->frame_bits;
       if (e->n_interior == 0) a.n_cells = 0;
