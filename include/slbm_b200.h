@@ -82,7 +82,10 @@ typedef struct SlbmInfo {
  * dims      public extents (x, y[, z]); periodic: per public axis (0/1)
  * q         9 (d2q9, dim 2), 19 or 27 (dim 3)
  * frame_width per public axis, or NULL for no interior/frame split
- *           (flags.py:83-108; widths >= 1, clamped to the extent)
+ *           (flags.py:83-108; widths clamped to the extent).  The reference
+ *           requires widths >= 1 (enforced by the Python layer); 0 is
+ *           accepted here and means "no frame on that axis" — used by the
+ *           domain drivers for axes without halo exchange.
  * Runs the whole list build on the GPU: fluid enumeration, index list with
  * no-slip folding, UBB and ghost slot allocation, the ownership-uniqueness
  * check (sparse.py:182-185) and the split lists.  PDFs start NaN-poisoned
@@ -230,8 +233,12 @@ int slbm_capture_end(void* stream, void** graph_exec);
 int slbm_graph_launch(void* graph_exec, void* stream);
 int slbm_graph_destroy(void* graph_exec);
 
-/* kernel-variant knobs for tuning experiments: knob 0 = index-list sweep
- * variant, knob 1 = cell-local sweep variant (0 = default)                 */
+/* tuning knobs (tools/variants.py, tools/e2e_probe.py; 0 = default):
+ *   0  index-list sweep variant (0 production, 1 no idx prefetch, 2 probe)
+ *   1  cell-local sweep variant (0: 3 CTAs/SM, 2: 4 CTAs/SM)
+ *   2  idx L2 prefetch distance in quarter waves (default 1)
+ *   3  ... in CTAs, overriding knob 2 when > 0
+ *   10 host staging chunk in MiB, 11 host staging threads                   */
 int slbm_set_tuning(int knob, int value);
 
 const char* slbm_last_error(void);
