@@ -343,6 +343,23 @@ class SparseEngine:
         _abi.call("slbm_macroscopic", self._h, _abi.ptr(rho, C.c_double), _abi.ptr(u, C.c_double))
         return rho, u
 
+    def device_state(self):
+        """Zero-copy torch view (float64, ``total_slots``) of the active PDF
+        buffer on the device, slot-numbered like the reference's flat array
+        (synchronizes first).  For device-side checks at full size."""
+        import torch
+
+        ptr = C.c_void_p()
+        _abi.call("slbm_pdf_pointer", self._h, C.byref(ptr))
+        self.synchronize()
+        n = int(self.total_slots)
+
+        class _View:
+            __cuda_array_interface__ = {"shape": (n,), "typestr": "<f8",
+                                        "data": (int(ptr.value or 0), False), "version": 3}
+
+        return torch.as_tensor(_View(), device=f"cuda:{self.device}")
+
     def total_mass(self) -> float:
         m = C.c_double()
         _abi.call("slbm_total_mass", self._h, C.byref(m))
