@@ -23,10 +23,18 @@ def main():
     q = int(os.environ.get("Q", 19))
     model = os.environ.get("MODEL", "trt")
     steps = int(os.environ.get("STEPS", 6))
-    fl = bench.make_flags(edge, 0)
     st = make_stencil("d3q19" if q == 19 else "d3q27")
     p = CollisionParams(bench.OMEGA, model, bench.magic_lambda(bench.OMEGA))
-    eng = SparseEngine(fl, st, p, "aa", device=0, check="deferred")
+    if os.environ.get("DENSE"):
+        from paper_2408_06880_b200 import geometry
+        from paper_2408_06880_b200.engine import DenseEngine
+
+        phi = float(os.environ.get("PHI", 1.0))
+        fl = geometry.obstacle_flags((edge,) * 3, phi, 1)
+        eng = DenseEngine(fl, st, p, "aa", device=0, check="deferred")
+    else:
+        fl = bench.make_flags(edge, 0)
+        eng = SparseEngine(fl, st, p, "aa", device=0, check="deferred")
     eng.init_equilibrium(1.0, np.array([0.01, 0.0, 0.0]))
     for _ in range(steps):
         eng.refresh_boundary(eng.parity)
