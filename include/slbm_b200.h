@@ -161,6 +161,11 @@ int slbm_read_slots(SlbmEngine* eng, const int64_t* slots, int64_t n, double* ou
 int slbm_write_slots(SlbmEngine* eng, const int64_t* slots, int64_t n, const double* in);
 /* raw device pointer of the active PDF buffer (pull swaps it every step) */
 int slbm_pdf_pointer(const SlbmEngine* eng, double** dev_pdf);
+/* device layout of the PDF array: start of each direction group (Q + 1
+ * entries) and the element count.  Sparse engines pad every group to a
+ * multiple of 32 slots (256 B); slot ids at the C-ABI stay the reference's
+ * (sparse.py:128-137) and are translated internally.                      */
+int slbm_pdf_layout(const SlbmEngine* eng, int64_t* group_start, int64_t* n_elements);
 
 /* ---- halo exchange (exchange.py:125-374) ---------------------------------
  * A halo is the per-rank exchange program for one phase set: a list of

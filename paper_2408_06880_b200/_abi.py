@@ -78,6 +78,7 @@ SIGNATURES = {
     "slbm_read_slots": [vp, c_i64p, C.c_int64, c_dp],
     "slbm_write_slots": [vp, c_i64p, C.c_int64, c_dp],
     "slbm_pdf_pointer": [vp, C.POINTER(vp)],
+    "slbm_pdf_layout": [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
     "slbm_halo_create": [C.c_int, C.POINTER(vp)],
     "slbm_halo_destroy": [vp],
     "slbm_halo_add_local": [vp, C.c_int, vp, vp, c_i64p, C.c_int64, c_i64p, c_i64p, C.c_int64],

@@ -103,7 +103,7 @@ int upload_slots(SlbmEngine* e, const int64_t* slots, int64_t n, uint32_t** dev)
     if (slots[i] < 0 || slots[i] >= e->total_slots)
       return fail(SLBM_EPROTOCOL, "slot " + std::to_string(slots[i]) + " outside [0, " +
                                       std::to_string(e->total_slots) + ")");
-    s32[i] = uint32_t(slots[i]);
+    s32[i] = uint32_t(e->phys_slot(slots[i]));
   }
   SLBM_CUDA_TRY(cudaMallocAsync(dev, s32.size() * sizeof(uint32_t), e->stream));
   SLBM_CUDA_TRY(cudaMemcpyAsync(*dev, s32.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice,
@@ -232,12 +232,12 @@ static int create_engine(int layout, const uint8_t* tags_pad, const double* ubb_
   }
   // PDF buffers, NaN-poisoned (sparse.py:90-91)
   auto alloc = [&](double** p) -> int {
-    cudaError_t er = cudaMalloc(p, size_t(e->total_slots) * sizeof(double));
+    cudaError_t er = cudaMalloc(p, size_t(e->phys_slots) * sizeof(double));
     if (er != cudaSuccess)
-      return fail(SLBM_ECUDA, "PDF allocation of " + std::to_string(e->total_slots * 8) +
+      return fail(SLBM_ECUDA, "PDF allocation of " + std::to_string(e->phys_slots * 8) +
                                   " bytes failed: " + cudaGetErrorString(er));
-    e->device_bytes += e->total_slots * 8;
-    return launch_fill(*p, e->total_slots, NAN, e->stream);
+    e->device_bytes += e->phys_slots * 8;
+    return launch_fill(*p, e->phys_slots, NAN, e->stream);
   };
   st = alloc(&e->pdf);
   if (st == SLBM_OK && pattern == SLBM_PULL) st = alloc(&e->tmp);
@@ -349,9 +349,7 @@ int slbm_export_lists(const SlbmEngine* e, uint32_t* idx, int64_t* fluid_coords,
   cudaStream_t s = e->stream;
   const int64_t n = e->n_fluid;
   if (idx && e->layout) return fail(SLBM_ECONFIG, "a dense engine has no index list");
-  if (idx)
-    SLBM_CUDA_TRY(cudaMemcpyAsync(idx, e->idx, size_t(e->q - 1) * n * sizeof(uint32_t),
-                                  cudaMemcpyDeviceToHost, s));
+  if (idx) SLBM_TRY(export_idx_logical(const_cast<SlbmEngine*>(e), idx));
   std::vector<uint32_t> xf;
   if (fluid_coords) {
     xf.resize(n);
@@ -379,9 +377,9 @@ int slbm_export_lists(const SlbmEngine* e, uint32_t* idx, int64_t* fluid_coords,
       if (e->dim == 3) fluid_coords[c * e->dim + 2] = z;
     }
   }
-  for (int64_t i = 0; i < e->n_ubb; ++i) {
-    if (ubb_slot) ubb_slot[i] = us[i];
-    if (ubb_partner) ubb_partner[i] = up[i];
+  for (int64_t i = 0; i < e->n_ubb; ++i) {  // device addresses -> slot ids
+    if (ubb_slot) ubb_slot[i] = e->slot_of(us[i]);
+    if (ubb_partner) ubb_partner[i] = e->slot_of(up[i]);
   }
   for (int q = 1; q < e->q; ++q) {
     for (int64_t k = 0; k < e->n_ghost_q[q]; ++k) {
@@ -426,10 +424,10 @@ int slbm_init_canonical_dev(SlbmEngine* e, const double* dev_values) {
     return dense_init(e, e->d_scratch);
   }
   // sparse.py:205-210: poison everything, then write the Q direction groups
-  SLBM_TRY(launch_fill(e->pdf, e->total_slots, NAN, e->stream));
-  if (e->tmp) SLBM_TRY(launch_fill(e->tmp, e->total_slots, NAN, e->stream));
+  SLBM_TRY(launch_fill(e->pdf, e->phys_slots, NAN, e->stream));
+  if (e->tmp) SLBM_TRY(launch_fill(e->tmp, e->phys_slots, NAN, e->stream));
   for (int r = 0; r < e->q; ++r)
-    SLBM_CUDA_TRY(cudaMemcpyAsync(e->pdf + e->base[r], dev_values + size_t(r) * e->n_fluid,
+    SLBM_CUDA_TRY(cudaMemcpyAsync(e->pdf + e->pbase[r], dev_values + size_t(r) * e->n_fluid,
                                   e->n_fluid * sizeof(double), cudaMemcpyDefault, e->stream));
   e->parity = SLBM_EVEN;
   return SLBM_OK;
@@ -448,10 +446,10 @@ int slbm_init_canonical(SlbmEngine* e, const double* values) {
     return SLBM_OK;
   }
   // sparse.py:205-210: poison everything, then write the Q direction groups
-  SLBM_TRY(launch_fill(e->pdf, e->total_slots, NAN, e->stream));
-  if (e->tmp) SLBM_TRY(launch_fill(e->tmp, e->total_slots, NAN, e->stream));
+  SLBM_TRY(launch_fill(e->pdf, e->phys_slots, NAN, e->stream));
+  if (e->tmp) SLBM_TRY(launch_fill(e->tmp, e->phys_slots, NAN, e->stream));
   for (int r = 0; r < e->q; ++r)
-    SLBM_TRY(copy_h2d(e->pdf + e->base[r], values + size_t(r) * e->n_fluid,
+    SLBM_TRY(copy_h2d(e->pdf + e->pbase[r], values + size_t(r) * e->n_fluid,
                       e->n_fluid * sizeof(double), e->device, e->stream));
   SLBM_CUDA_TRY(cudaStreamSynchronize(e->stream));
   e->parity = SLBM_EVEN;
@@ -478,8 +476,8 @@ int slbm_init_equilibrium(SlbmEngine* e, const double* rho, int rho_scalar, cons
     SLBM_CUDA_TRY(cudaStreamSynchronize(e->stream));
     return SLBM_OK;
   }
-  SLBM_TRY(launch_fill(e->pdf, e->total_slots, NAN, e->stream));
-  if (e->tmp) SLBM_TRY(launch_fill(e->tmp, e->total_slots, NAN, e->stream));
+  SLBM_TRY(launch_fill(e->pdf, e->phys_slots, NAN, e->stream));
+  if (e->tmp) SLBM_TRY(launch_fill(e->tmp, e->phys_slots, NAN, e->stream));
   SLBM_TRY(launch_equilibrium(e, d_rho, rho_scalar, d_u, u_scalar, nullptr));
   SLBM_CUDA_TRY(cudaStreamSynchronize(e->stream));
   e->parity = SLBM_EVEN;
@@ -500,7 +498,7 @@ int slbm_canonical_state(SlbmEngine* e, double* values) {
   if (odd) SLBM_TRY(launch_refresh(e, SLBM_ODD));  // sparse.py:317
   for (int r = 0; r < e->q; ++r) {
     const int g = odd ? e->dirs.inv[r] : r;
-    SLBM_TRY(copy_d2h(values + size_t(r) * e->n_fluid, e->pdf + e->base[g],
+    SLBM_TRY(copy_d2h(values + size_t(r) * e->n_fluid, e->pdf + e->pbase[g],
                       e->n_fluid * sizeof(double), e->device, e->stream));
   }
   return SLBM_OK;
@@ -547,7 +545,7 @@ int slbm_total_mass(SlbmEngine* e, double* mass) {
   } else {
     for (int r = 0; r < e->q; ++r) {
       const int g = odd ? e->dirs.inv[r] : r;
-      SLBM_TRY(launch_sum(e->pdf + e->base[g], e->n_fluid, e->d_scratch + r, e->stream));
+      SLBM_TRY(launch_sum(e->pdf + e->pbase[g], e->n_fluid, e->d_scratch + r, e->stream));
     }
   }
   std::vector<double> parts(e->q);
@@ -745,6 +743,14 @@ int slbm_write_slots(SlbmEngine* e, const int64_t* slots, int64_t n, const doubl
 int slbm_pdf_pointer(const SlbmEngine* e, double** dev_pdf) {
   CHECK_ENGINE(e);
   *dev_pdf = e->pdf;
+  return SLBM_OK;
+}
+
+int slbm_pdf_layout(const SlbmEngine* e, int64_t* group_start, int64_t* n_elements) {
+  CHECK_ENGINE(e);
+  for (int q = 0; q <= e->q; ++q)
+    if (group_start) group_start[q] = e->layout ? e->base[q] : e->pbase[q];
+  if (n_elements) *n_elements = e->layout ? e->total_slots : e->phys_slots;
   return SLBM_OK;
 }
 

@@ -260,6 +260,40 @@ __global__ void k_ghost_assign(const uint32_t* sorted_cells, int64_t cnt, int q,
   idx[(q - 1) * n + sorted_cells[k]] = first_slot + uint32_t(k);
 }
 
+// reference slot ids -> device addresses (group g: pbase[g] + slot - base[g])
+struct SlotMap {
+  uint32_t base[28], pbase[28];
+  int q;
+  __device__ uint32_t operator()(uint32_t slot) const {
+    int g = 0;
+    while (g + 1 < q && base[g + 1] <= slot) ++g;
+    return pbase[g] + (slot - base[g]);
+  }
+};
+
+// logical (Q-1) x n index list -> physical addresses in rows of `pitch`
+__global__ void k_physical_idx(const uint32_t* in, int64_t n, int64_t pitch, int64_t rows,
+                               SlotMap m, uint32_t* out) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= rows * n) return;
+  const int64_t r = t / n, c = t - r * n;
+  out[r * pitch + c] = m(in[t]);
+}
+
+// physical rows of `pitch` -> the reference's contiguous (Q-1) x n slot ids
+__global__ void k_logical_idx(const uint32_t* in, int64_t n, int64_t pitch, int64_t rows,
+                              SlotMap inv, uint32_t* out) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= rows * n) return;
+  const int64_t r = t / n, c = t - r * n;
+  out[t] = inv(in[r * pitch + c]);
+}
+
+__global__ void k_physical_inplace(uint32_t* v, int64_t n, SlotMap m) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t < n) v[t] = m(v[t]);
+}
+
 __global__ void k_unique(const uint32_t* idx, int64_t n, int q, uint64_t total,
                          unsigned int* bits, int* err) {
   int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -571,6 +605,51 @@ int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
     return fail(SLBM_ECONFIG, "each slot must belong to exactly one (direction, cell) pair");
   }
 
+  // -- device layout: 256-B aligned direction groups and idx rows --
+  {
+    SlotMap m{};
+    m.q = d.q;
+    int64_t pb = 0;
+    for (int q = 0; q <= d.q; ++q) {
+      e->pbase[q] = pb;
+      if (q < d.q) pb += (e->base[q + 1] - e->base[q] + 31) / 32 * 32;
+    }
+    for (int q = 0; q <= d.q && q < 28; ++q) {
+      m.base[q] = uint32_t(e->base[q]);
+      m.pbase[q] = uint32_t(e->pbase[q]);
+    }
+    e->phys_slots = e->pbase[d.q];
+    if (e->phys_slots >= (int64_t(1) << 32)) {
+      cleanup();
+      return fail(SLBM_ECONFIG, std::to_string(e->phys_slots) +
+                                    " aligned slots exceed the 4-byte location table range");
+    }
+    e->idx_pitch = (n + 31) / 32 * 32;
+    uint32_t* logical = e->idx;
+    e->idx = nullptr;
+    if (dalloc(e, &e->idx, int64_t(d.q - 1) * e->idx_pitch) != SLBM_OK) {
+      cudaFree(logical);
+      cleanup();
+      return SLBM_ECUDA;
+    }
+    e->device_bytes -= int64_t(d.q - 1) * n * 4;  // the logical list is freed below
+    const int64_t entries = int64_t(d.q - 1) * n;
+    if (entries)
+      k_physical_idx<<<grid_for(entries, 256), 256, 0, s>>>(logical, n, e->idx_pitch, d.q - 1, m,
+                                                            e->idx);
+    if (e->n_ubb) {
+      k_physical_inplace<<<grid_for(e->n_ubb, 256), 256, 0, s>>>(e->ubb_slot, e->n_ubb, m);
+      k_physical_inplace<<<grid_for(e->n_ubb, 256), 256, 0, s>>>(e->ubb_partner, e->n_ubb, m);
+    }
+    if (e->n_out) {
+      k_physical_inplace<<<grid_for(e->n_out, 256), 256, 0, s>>>(e->out_slot, e->n_out, m);
+      k_physical_inplace<<<grid_for(e->n_out, 256), 256, 0, s>>>(e->out_partner, e->n_out, m);
+    }
+    SLBM_CUDA_TRY(cudaGetLastError());
+    SLBM_CUDA_TRY(cudaStreamSynchronize(s));
+    cudaFree(logical);
+  }
+
   // -- interior / frame split (sparse.py:80-88) --
   if (frame_width) {
     InFrame fr{e->x_flat, g, {1, 1, 1}, true};
@@ -610,6 +689,27 @@ int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
   }
   SLBM_CUDA_TRY(cudaStreamSynchronize(s));
   cleanup();
+  return SLBM_OK;
+}
+
+// the index list in the reference's layout (slot ids, contiguous rows)
+int export_idx_logical(SlbmEngine* e, uint32_t* host) {
+  const int64_t n = e->n_fluid, rows = e->q - 1;
+  if (rows * n == 0) return SLBM_OK;
+  SlotMap inv{};
+  inv.q = e->q;
+  for (int q = 0; q <= e->q && q < 28; ++q) {
+    inv.base[q] = uint32_t(e->pbase[q]);  // search the device layout ...
+    inv.pbase[q] = uint32_t(e->base[q]);  // ... map back to slot ids
+  }
+  uint32_t* tmp = nullptr;
+  SLBM_CUDA_TRY(cudaMallocAsync(&tmp, size_t(rows * n) * 4, e->stream));
+  k_logical_idx<<<grid_for(rows * n, 256), 256, 0, e->stream>>>(e->idx, n, e->idx_pitch, rows, inv,
+                                                                tmp);
+  SLBM_CUDA_TRY(cudaGetLastError());
+  SLBM_TRY(copy_d2h(host, tmp, size_t(rows * n) * 4, e->device, e->stream));
+  SLBM_CUDA_TRY(cudaFreeAsync(tmp, e->stream));
+  SLBM_CUDA_TRY(cudaStreamSynchronize(e->stream));
   return SLBM_OK;
 }
 

@@ -405,6 +405,8 @@ int build_dense(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
   cudaFree(d_err);
   cudaFree(d_tags);
   e->total_slots = int64_t(e->q) * n_pad;
+  e->phys_slots = e->total_slots;  // slot = q * npad + p is also the device address
+  for (int q = 0; q <= e->q && q < 28; ++q) e->base[q] = e->pbase[q] = int64_t(q) * n_pad;
   if (e->total_slots >= (int64_t(1) << 32))
     return fail(SLBM_ECONFIG, "dense block too large: q * padded cells must be < 2^32");
   return SLBM_OK;

@@ -18,7 +18,15 @@ struct SlbmEngine {
   int64_t n_fluid = 0, total_slots = 0, n_ubb = 0, n_ghost = 0;
   int64_t n_interior = 0, n_frame = 0;
   bool has_split = false;
-  int64_t base[28] = {0};
+  int64_t base[28] = {0};   // slot-id layout of the reference (sparse.py:128-137)
+  // Device layout: direction group q starts at pbase[q], each group padded to
+  // a multiple of 32 slots (256 B), so every group row and idx row is
+  // line-aligned (profiles: +1% index sweep, +2% cell-local sweep).  The
+  // index list and the boundary programs hold physical addresses; slot ids
+  // crossing the C-ABI are the reference's and translated (phys_slot).
+  int64_t pbase[28] = {0};
+  int64_t phys_slots = 0;   // pdf elements allocated (>= total_slots)
+  int64_t idx_pitch = 0;    // elements per idx row (n_fluid rounded up to 32)
   int64_t n_ubb_q[27] = {0}, n_ghost_q[27] = {0};
   int64_t ubb_off[28] = {0}, ghost_off[28] = {0};
   int64_t n_out = 0, n_out_q[27] = {0}, out_off[28] = {0};
@@ -65,6 +73,21 @@ struct SlbmEngine {
   int64_t steps_done = 0;
 
   int ensure_scratch(size_t bytes);
+
+  // reference slot id -> device address (identity for dense engines)
+  // inverse for a device address of a used slot
+  int64_t slot_of(int64_t phys) const {
+    if (layout) return phys;
+    int g = 0;
+    while (g + 1 < q && pbase[g + 1] <= phys) ++g;
+    return base[g] + (phys - pbase[g]);
+  }
+  int64_t phys_slot(int64_t slot) const {
+    if (layout) return slot;
+    int g = 0;
+    while (g + 1 < q && base[g + 1] <= slot) ++g;
+    return pbase[g] + (slot - base[g]);
+  }
 };
 
 namespace slbm {
@@ -101,6 +124,7 @@ int hostcopy_tune(int knob, int value);  // 10: chunk MiB, 11: max threads
 int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
                 const int32_t* frame_width);
 int enumerate_fluid(SlbmEngine* e, const uint8_t* tags_pad);
+int export_idx_logical(SlbmEngine* e, uint32_t* host);
 
 // dense.cu (direct-addressing engine)
 int build_dense(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,

@@ -29,7 +29,8 @@ struct GroupArgs {
   uint32_t lo;           // cells below lo are skipped
   uint32_t n_cells;
   uint32_t n_fluid;
-  uint32_t base[28];
+  uint32_t idx_pitch;
+  uint32_t base[28];  // device group starts (pbase)
   unsigned long long* bad;
   const unsigned long long* step;
 };
@@ -92,11 +93,11 @@ __global__ void __launch_bounds__(kGB, KIND == 2 ? 6 : 4) k_group(const GroupArg
   const uint32_t pos0 = (blockIdx.x - first) * kGB;  // this CTA's first sweep position
   const uint32_t* idx = a.idx;
   const uint32_t* cids = a.cids;
-  const uint32_t n_fluid = a.n_fluid, n_cells = a.n_cells, offset = a.offset;
+  const uint32_t pitch = a.idx_pitch, n_cells = a.n_cells, offset = a.offset;
   // index-list rows of this engine's CTA `ahead` positions later (sweep.cuh),
   // issued first as in the single-engine sweep
   if (KIND != 2 && cids == nullptr)
-    prefetch_idx_ahead<L::Q - 1, kGB>(idx, n_fluid, nullptr, offset + n_cells, offset + pos0,
+    prefetch_idx_ahead<L::Q - 1, kGB>(idx, pitch, nullptr, offset + n_cells, offset + pos0,
                                       ahead);
   const uint32_t i = pos0 + threadIdx.x;
   if (i >= n_cells) return;
@@ -115,9 +116,9 @@ __global__ void __launch_bounds__(kGB, KIND == 2 ? 6 : 4) k_group(const GroupArg
   } else {
     uint32_t s[L::Q];
     s[0] = c;
-    sfor<1, L::Q>([&](auto q) { s[q] = __ldcs(idx + size_t(q - 1) * n_fluid + c); });
+    sfor<1, L::Q>([&](auto q) { s[q] = __ldcs(idx + size_t(q - 1) * pitch + c); });
     sfor<0, L::Q>([&](auto q) { t[q] = pdf[s[q]]; });
-    if (cids) prefetch_idx_ahead<L::Q - 1, kGB>(idx, n_fluid, cids, n_cells, pos0, ahead);
+    if (cids) prefetch_idx_ahead<L::Q - 1, kGB>(idx, pitch, cids, n_cells, pos0, ahead);
     if constexpr (KIND == 1) {  // AA even (sparse.py:264-271)
       bad = collide<L, MODEL>(t, omega, lam, [&](auto q, double v) {
         constexpr int qb = L::INV[decltype(q)::value];
@@ -181,7 +182,8 @@ GroupArgs args_of(SlbmEngine* e, int phase, int flip) {
       if (e->n_interior == 0) a.n_cells = 0;
     }
   }
-  for (int q = 0; q <= e->q && q < 28; ++q) a.base[q] = uint32_t(e->base[q]);
+  a.idx_pitch = uint32_t(e->idx_pitch);
+  for (int q = 0; q <= e->q && q < 28; ++q) a.base[q] = uint32_t(e->pbase[q]);
   a.bad = e->d_bad;
   a.step = e->d_step;
   return a;

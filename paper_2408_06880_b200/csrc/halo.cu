@@ -203,9 +203,9 @@ int slbm_halo_add_local(SlbmHalo* h, int phase, SlbmEngine* src, SlbmEngine* dst
     if (take[k] < 0 || take[k] >= n_send)
       return fail(SLBM_EPROTOCOL, "take index outside the message");
     p.l_se.push_back(si);
-    p.l_ss.push_back(uint32_t(send[take[k]]));
+    p.l_ss.push_back(uint32_t(src->phys_slot(send[take[k]])));
     p.l_de.push_back(di);
-    p.l_ds.push_back(uint32_t(tgt[k]));
+    p.l_ds.push_back(uint32_t(dst->phys_slot(tgt[k])));
   }
   return SLBM_OK;
 }
@@ -220,7 +220,7 @@ int slbm_halo_add_send(SlbmHalo* h, int phase, SlbmEngine* src, int peer, const 
   PeerSend& ps = h->ph[phase].sends[peer];
   for (int64_t k = 0; k < n; ++k) {
     ps.eng.push_back(si);
-    ps.slot.push_back(uint32_t(send[k]));
+    ps.slot.push_back(uint32_t(src->phys_slot(send[k])));
   }
   return SLBM_OK;
 }
@@ -238,7 +238,7 @@ int slbm_halo_add_recv(SlbmHalo* h, int phase, SlbmEngine* dst, int peer, int64_
       return fail(SLBM_EPROTOCOL, "take index outside the message");
     pr.pos.push_back(uint64_t(pr.n_wire + take[k]));
     pr.eng.push_back(di);
-    pr.slot.push_back(uint32_t(tgt[k]));
+    pr.slot.push_back(uint32_t(dst->phys_slot(tgt[k])));
   }
   pr.n_wire += n_wire;
   return SLBM_OK;

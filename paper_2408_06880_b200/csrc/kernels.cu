@@ -36,7 +36,8 @@ struct SweepArgs {
   uint32_t lo;
   uint32_t n_cells;
   uint32_t n_fluid;
-  uint32_t base[28];
+  uint32_t idx_pitch;  // elements per index-list row (256-B aligned rows)
+  uint32_t base[28];   // device group starts (SlbmEngine::pbase)
   double omega, lam;
   unsigned long long* bad;
   const unsigned long long* step;
@@ -79,7 +80,7 @@ __global__ void __launch_bounds__(kIB, MINB) k_index_sweep(const SweepArgs a, ui
   const uint32_t first = blockIdx.x * kIB;
   if constexpr (PF) {
     if (a.cids == nullptr)
-      prefetch_idx_ahead<L::Q - 1, kIB>(a.idx, a.n_fluid, nullptr, a.offset + a.n_cells,
+      prefetch_idx_ahead<L::Q - 1, kIB>(a.idx, a.idx_pitch, nullptr, a.offset + a.n_cells,
                                         a.offset + first, ahead);
   }
   const uint32_t i = first + threadIdx.x;
@@ -93,12 +94,12 @@ __global__ void __launch_bounds__(kIB, MINB) k_index_sweep(const SweepArgs a, ui
   // in front of it: a frame cell reads its idx row for nothing (~1% extra)
   // but no cell waits for the mask before its own loads start
   const uint32_t skip_word = a.skip ? __ldg(a.skip + (c >> 5)) : 0u;
-  sfor<1, L::Q>([&](auto q) { s[q] = __ldcs(a.idx + size_t(q - 1) * a.n_fluid + c); });
+  sfor<1, L::Q>([&](auto q) { s[q] = __ldcs(a.idx + size_t(q - 1) * a.idx_pitch + c); });
   if ((skip_word >> (c & 31)) & 1u) return;
   sfor<0, L::Q>([&](auto q) { t[q] = a.pdf[s[q]]; });
   if constexpr (PF) {
     if (a.cids != nullptr)
-      prefetch_idx_ahead<L::Q - 1, kIB>(a.idx, a.n_fluid, a.cids, a.n_cells, first, ahead);
+      prefetch_idx_ahead<L::Q - 1, kIB>(a.idx, a.idx_pitch, a.cids, a.n_cells, first, ahead);
   }
   bool bad;
   if constexpr (KIND == kEven) {
@@ -126,7 +127,7 @@ __global__ void __launch_bounds__(kIB) k_probe(const SweepArgs a) {
   uint32_t s[L::Q];
   double t[L::Q];
   s[0] = c;
-  sfor<1, L::Q>([&](auto q) { s[q] = __ldcs(a.idx + size_t(q - 1) * a.n_fluid + c); });
+  sfor<1, L::Q>([&](auto q) { s[q] = __ldcs(a.idx + size_t(q - 1) * a.idx_pitch + c); });
   sfor<0, L::Q>([&](auto q) { t[q] = a.pdf[s[q]]; });
   sfor<0, L::Q>([&](auto q) { a.pdf[s[L::INV[q]]] = t[q]; });
 }
@@ -363,7 +364,8 @@ SweepArgs sweep_args(SlbmEngine* e) {
   a.cids = nullptr;
   a.n_fluid = uint32_t(e->n_fluid);
   a.n_cells = uint32_t(e->n_fluid);
-  for (int q = 0; q <= e->q && q < 28; ++q) a.base[q] = uint32_t(e->base[q]);
+  a.idx_pitch = uint32_t(e->idx_pitch);
+  for (int q = 0; q <= e->q && q < 28; ++q) a.base[q] = uint32_t(e->pbase[q]);
   a.omega = e->omega;
   a.lam = e->lambda_odd;
   a.bad = e->d_bad;
@@ -396,9 +398,11 @@ int set_tuning(int knob, int value) {
 int launch_slot_lookup(SlbmEngine* e, const int64_t* d_qs, const int64_t* d_pflat, int64_t n,
                        int64_t* d_out, int* d_err) {
   if (n == 0) return SLBM_OK;
+  SweepArgs a = sweep_args(e);  // slot ids: the reference's layout, not the device one
+  for (int q = 0; q <= e->q && q < 28; ++q) a.base[q] = uint32_t(e->base[q]);
   k_slot_lookup<<<grid_for(n, 256), 256, 0, e->stream>>>(d_qs, d_pflat, n, e->cid_map,
-                                                          e->geo.n_padded(), sweep_args(e), e->q,
-                                                          d_out, d_err);
+                                                          e->geo.n_padded(), a, e->q, d_out,
+                                                          d_err);
   SLBM_CUDA_TRY(cudaGetLastError());
   return SLBM_OK;
 }

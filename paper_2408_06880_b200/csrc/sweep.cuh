@@ -26,7 +26,7 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 // them), without one they are cell ids.  `first` is this CTA's first
 // position, `end` one past the sweep's last.
 template <int QM1, int BLOCK>
-__device__ __forceinline__ void prefetch_idx_ahead(const uint32_t* idx, uint32_t n_fluid,
+__device__ __forceinline__ void prefetch_idx_ahead(const uint32_t* idx, uint32_t pitch,
                                                    const uint32_t* cids, uint32_t end,
                                                    uint32_t first, uint32_t ahead) {
   constexpr int kLines = BLOCK * 4 / 128;
@@ -35,7 +35,7 @@ __device__ __forceinline__ void prefetch_idx_ahead(const uint32_t* idx, uint32_t
   const uint32_t pos = first + ahead * BLOCK + line * 32;
   if (pos >= end) return;
   const uint32_t cell = cids ? __ldcs(cids + pos) : pos;
-  prefetch_l2(idx + size_t(row) * n_fluid + cell);
+  prefetch_l2(idx + size_t(row) * pitch + cell);
 }
 
 }  // namespace slbm

@@ -343,16 +343,25 @@ class SparseEngine:
         _abi.call("slbm_macroscopic", self._h, _abi.ptr(rho, C.c_double), _abi.ptr(u, C.c_double))
         return rho, u
 
+    def pdf_layout(self) -> tuple[np.ndarray, int]:
+        """Device layout of the PDF array: direction-group starts (Q + 1) and
+        the element count.  Sparse engines pad each group to 32 slots; slot
+        ids in every other call are the reference's."""
+        starts = np.zeros(self.stencil.q + 1, dtype=np.int64)
+        n = C.c_int64()
+        _abi.call("slbm_pdf_layout", self._h, _abi.ptr(starts, C.c_int64), C.byref(n))
+        return starts, int(n.value)
+
     def device_state(self):
-        """Zero-copy torch view (float64, ``total_slots``) of the active PDF
-        buffer on the device, slot-numbered like the reference's flat array
-        (synchronizes first).  For device-side checks at full size."""
+        """Zero-copy torch view (float64) of the active PDF buffer in its
+        device layout (see :meth:`pdf_layout`; synchronizes first).  For
+        device-side checks at full size."""
         import torch
 
         ptr = C.c_void_p()
         _abi.call("slbm_pdf_pointer", self._h, C.byref(ptr))
         self.synchronize()
-        n = int(self.total_slots)
+        n = self.pdf_layout()[1]
 
         class _View:
             __cuda_array_interface__ = {"shape": (n,), "typestr": "<f8",
