@@ -72,7 +72,9 @@ enum Kind { kPull = 0, kEven = 1, kOdd = 2 };
 // re-reading idx before each store (RELOAD); cp.async gather into shared
 // memory; persistent CTAs with a cp.async idx double buffer; a cell-major
 // idx copy; ld.global.nc / L1::no_allocate PDF gathers (-40%: the gathers
-// want L1 sector merging); st.global.cs stores (-4%) — all slower than the
+// want L1 sector merging); st.global.cs stores (-4%); 5 or 6 CTAs/SM (94 /
+// 80 + spill registers: -1% / -10%); FMA contraction (no change under the
+// power cap, which costs the sweep ~6% of SM clock) — all slower than the
 // plain gather.  What pays is the L2 prefetch of the index list one quarter
 // wave ahead (sweep.cuh): +7-9%.
 template <class L, int MODEL, int KIND, int MINB, bool PF>
@@ -183,6 +185,7 @@ void launch_kind(int kind, const SweepArgs& a, unsigned grid, cudaStream_t s) {
   } else if (kind == kEven) {
     if (g_even_variant == 1)
       launch_index<L, MODEL, kEven, MINB, false>(a, s);
+
     else if (g_even_variant == 2)
       k_probe<L><<<(a.n_cells + kIB - 1) / kIB, kIB, 0, s>>>(a);
     else
