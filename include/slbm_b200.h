@@ -212,6 +212,25 @@ int slbm_nccl_comm_init(const void* unique_id, int nranks, int rank, int device,
 int slbm_nccl_get_unique_id(void* unique_id_out);
 int slbm_nccl_comm_destroy(void* comm);
 
+/* Peer transport (no NCCL): remote edges move through CUDA IPC mappings of
+ * each peer's receive buffer and flag words, over NVLink P2P.  Call
+ * slbm_halo_use_peer before commit; after commit exchange
+ * slbm_halo_ipc_handles (2 x 64 bytes) and, per phase, the receive section
+ * each rank reserved for every sender (slbm_halo_recv_section), then
+ * slbm_halo_connect every peer this rank sends to or receives from
+ * (peer == own rank: loopback through its own buffers).  The pack kernel
+ * stores each message directly into the peer's buffer and publishes the
+ * exchange epoch with a system-scope release store; the receiver's unpack
+ * waits for it (acquire) and acknowledges.  Replaces exchange.py's
+ * deliver/mailbox (exchange.py:222-253) for GPUs on one NVSwitch node.    */
+int slbm_halo_use_peer(SlbmHalo* halo, int rank);
+int slbm_halo_ipc_handles(const SlbmHalo* halo, void* recv_handle, void* flags_handle);
+int slbm_halo_recv_section(const SlbmHalo* halo, int phase, int peer, int64_t* offset,
+                           int64_t* count);
+int slbm_halo_connect(SlbmHalo* halo, int peer, const void* recv_handle,
+                      const void* flags_handle, const int64_t* section_offset /* [2 phases] */,
+                      const int64_t* section_count /* [2 phases] */);
+
 /* ---- geometry helper: overlapping-sphere voxelizer on the GPU -----------
  * Same rasterization rule as geometry.py:150-178 (cell solid iff its centre
  * lies strictly inside a sphere; resolution 1).  solid: host uint8 over

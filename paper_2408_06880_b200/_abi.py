@@ -94,6 +94,10 @@ SIGNATURES = {
     "slbm_nccl_comm_init": [vp, C.c_int, C.c_int, C.c_int, C.POINTER(vp)],
     "slbm_nccl_get_unique_id": [vp],
     "slbm_nccl_comm_destroy": [vp],
+    "slbm_halo_use_peer": [vp, C.c_int],
+    "slbm_halo_ipc_handles": [vp, vp, vp],
+    "slbm_halo_recv_section": [vp, C.c_int, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
+    "slbm_halo_connect": [vp, C.c_int, vp, vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
     "slbm_voxelize_spheres": [c_i32p, c_dp, C.c_int64, C.c_double, C.c_int, c_u8p],
     "slbm_set_tuning": [C.c_int, C.c_int],
     "slbm_group_create": [C.POINTER(vp), C.c_int, C.POINTER(vp)],

@@ -13,6 +13,17 @@
 // an NCCL group, on the halo's own comm stream, so the interior sweep on the
 // compute stream overlaps pack -> NVLink -> unpack (the interior
 // sweep touches none of the exchanged slots).
+//
+// Peer transport (slbm_halo_use_peer + slbm_halo_connect): no NCCL.  Every
+// rank maps its peers' receive buffers and flag words through CUDA IPC; the
+// pack kernel gathers from the local PDFs and stores each message straight
+// into the peer's receive buffer over NVLink (gather and transfer are one
+// kernel), then a release store of the step's epoch into the peer's flag
+// tells it the message is complete.  The receiver's unpack waits (acquire
+// spin) on that flag and acknowledges into the sender's ack word, which the
+// sender waits on before overwriting the buffer one exchange later:
+//   comm stream:  wait acks(e-1) -> remote pack -> signal(e) -> local edges
+//                 -> wait data(e) -> unpack -> ack(e) -> e += 1
 #include <nccl.h>
 
 #include <algorithm>
@@ -47,6 +58,72 @@ __global__ void k_unpack(PdfTable t, const uint64_t* pos, const uint16_t* e, con
                          int64_t n, const double* buf) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) t.p[e[i]][s[i]] = buf[pos[i]];
+}
+
+// ---- peer transport: epoch flags with system-scope release / acquire ----
+constexpr int kMaxPeers = 64;
+
+struct FlagPtrs {
+  uint64_t* p[kMaxPeers];
+  int n;
+};
+
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// every flag in `f` reaches epoch + delta; a peer that never arrives is a
+// fatal error (trap after 30 s) rather than a hung device
+__global__ void k_wait_flags(FlagPtrs f, const uint64_t* epoch, int64_t delta) {
+  if (int(threadIdx.x) >= f.n) return;
+  const uint64_t want = uint64_t(int64_t(*epoch) + delta);
+  const uint64_t t0 = globaltimer();
+  while (ld_acquire_sys(f.p[threadIdx.x]) < want) {
+    __nanosleep(200);
+    if (globaltimer() - t0 > 30ull * 1000000000ull) __trap();
+  }
+}
+
+// publish the epoch to every flag in `f` after this stream's earlier writes
+__global__ void k_signal_flags(FlagPtrs f, const uint64_t* epoch) {
+  if (int(threadIdx.x) >= f.n) return;
+  __threadfence_system();
+  st_release_sys(f.p[threadIdx.x], *epoch);
+}
+
+__global__ void k_epoch_advance(uint64_t* epoch) { *epoch += 1; }
+
+// Peer pack: gather this rank's entries for one peer and store them straight
+// into the peer's receive buffer over NVLink; the CTA that finishes last
+// publishes the epoch in the peer's flag word.  Every CTA fences its remote
+// stores at system scope before it counts itself done, so the release store
+// of the last one orders all of them (the "last block" pattern; no reliance
+// on kernel-boundary visibility of peer writes).
+__global__ void k_pack_signal(PdfTable t, const uint16_t* e, const uint32_t* s, int64_t n,
+                              double* remote, unsigned int* done, uint64_t* remote_flag,
+                              const uint64_t* epoch) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) remote[i] = t.p[e[i]][s[i]];
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int prev = atomicAdd(done, 1u);
+    if (prev == gridDim.x - 1) {
+      __threadfence_system();
+      st_release_sys(remote_flag, *epoch);
+      *done = 0;  // every CTA has counted: reset for the next exchange
+    }
+  }
 }
 
 inline unsigned grid_for(int64_t n) { return unsigned(std::max<int64_t>((n + 255) / 256, 1)); }
@@ -86,6 +163,8 @@ struct PhaseProg {
   int64_t send_total = 0, recv_total = 0;
   // unpack entries per peer (for the host-staged path)
   std::vector<int64_t> unpack_off, unpack_cnt;
+  // peer transport: where each send section lands in its peer's receive buffer
+  std::vector<double*> remote_dst;
 };
 
 }  // namespace
@@ -103,6 +182,15 @@ struct SlbmHalo {
   double* d_recv = nullptr;
   ncclComm_t nccl = nullptr;
   bool committed = false;
+  // peer transport
+  bool peer = false;
+  int rank = 0;
+  uint64_t* d_flags = nullptr;  // [0, kMaxPeers): data epoch per sender; [kMaxPeers, 2k): ack per receiver
+  uint64_t* d_epoch = nullptr;
+  unsigned int* d_done = nullptr;       // per send slot: CTAs finished in k_pack_signal
+  std::map<int, double*> peer_recv;    // peer -> its receive buffer (mapped)
+  std::map<int, uint64_t*> peer_flags; // peer -> its flag words (mapped)
+  std::vector<void*> opened;           // IPC mappings to close
 
   int engine_id(SlbmEngine* e, uint16_t* id) {
     auto it = std::find(engines.begin(), engines.end(), e);
@@ -148,6 +236,52 @@ int check_phase(const SlbmHalo* h, int phase) {
 
 }  // namespace
 
+namespace {
+
+FlagPtrs flag_ptrs(SlbmHalo* h, const std::vector<int>& peers, bool remote, int base) {
+  FlagPtrs f{};
+  f.n = int(peers.size());
+  for (size_t i = 0; i < peers.size(); ++i) {
+    // remote: the peer's word for this rank; local: this rank's word for the peer
+    f.p[i] = remote ? h->peer_flags[peers[i]] + base + h->rank : h->d_flags + base + peers[i];
+  }
+  return f;
+}
+
+int peer_start(SlbmHalo* h, PhaseProg& p, int phase) {
+  const PdfTable t = h->table();
+  cudaStream_t s = h->comm;
+  if (!p.send_peer.empty()) {
+    // the receivers have consumed the previous message in their buffers
+    k_wait_flags<<<1, kMaxPeers, 0, s>>>(flag_ptrs(h, p.send_peer, false, kMaxPeers), h->d_epoch,
+                                         -1);
+    const FlagPtrs data = flag_ptrs(h, p.send_peer, true, 0);
+    for (size_t i = 0; i < p.send_peer.size(); ++i) {
+      if (!p.remote_dst[i]) return fail(SLBM_ECONFIG, "peer transport: halo not connected");
+      k_pack_signal<<<grid_for(p.send_cnt[i]), 256, 0, s>>>(
+          t, p.d_pe + p.send_off[i], p.d_ps + p.send_off[i], p.send_cnt[i], p.remote_dst[i],
+          h->d_done + phase * kMaxPeers + i, data.p[i], h->d_epoch);
+    }
+    SLBM_CUDA_TRY(cudaGetLastError());
+  }
+  SLBM_TRY(slbm_halo_local(h, phase));
+  if (!p.recv_peer.empty()) {
+    k_wait_flags<<<1, kMaxPeers, 0, s>>>(flag_ptrs(h, p.recv_peer, false, 0), h->d_epoch, 0);
+    if (p.n_unpack)
+      k_unpack<<<grid_for(p.n_unpack), 256, 0, s>>>(t, p.d_upos, p.d_ue, p.d_us, p.n_unpack,
+                                                     h->d_recv);
+    k_signal_flags<<<1, kMaxPeers, 0, s>>>(flag_ptrs(h, p.recv_peer, true, kMaxPeers),
+                                           h->d_epoch);
+    SLBM_CUDA_TRY(cudaGetLastError());
+  }
+  k_epoch_advance<<<1, 1, 0, s>>>(h->d_epoch);
+  SLBM_CUDA_TRY(cudaGetLastError());
+  SLBM_CUDA_TRY(cudaEventRecord(h->ev_done, s));
+  return SLBM_OK;
+}
+
+}  // namespace
+
 extern "C" {
 
 int slbm_halo_create(int device, SlbmHalo** out) {
@@ -180,6 +314,10 @@ int slbm_halo_destroy(SlbmHalo* h) {
   }
   if (h->d_send) cudaFree(h->d_send);
   if (h->d_recv) cudaFree(h->d_recv);
+  for (void* m : h->opened) cudaIpcCloseMemHandle(m);
+  if (h->d_flags) cudaFree(h->d_flags);
+  if (h->d_epoch) cudaFree(h->d_epoch);
+  if (h->d_done) cudaFree(h->d_done);
   cudaEventDestroy(h->ev_ready);
   cudaEventDestroy(h->ev_done);
   cudaStreamDestroy(h->comm);
@@ -295,8 +433,19 @@ int slbm_halo_commit(SlbmHalo* h, void* nccl_comm) {
     max_send = std::max(max_send, p.send_total);
     max_recv = std::max(max_recv, p.recv_total);
   }
-  if (max_send) SLBM_CUDA_TRY(cudaMalloc(&h->d_send, max_send * sizeof(double)));
-  if (max_recv) SLBM_CUDA_TRY(cudaMalloc(&h->d_recv, max_recv * sizeof(double)));
+  if (max_send && !h->peer) SLBM_CUDA_TRY(cudaMalloc(&h->d_send, max_send * sizeof(double)));
+  if (max_recv || h->peer)
+    SLBM_CUDA_TRY(cudaMalloc(&h->d_recv, std::max<int64_t>(max_recv, 1) * sizeof(double)));
+  if (h->peer) {
+    SLBM_CUDA_TRY(cudaMalloc(&h->d_flags, 2 * kMaxPeers * sizeof(uint64_t)));
+    SLBM_CUDA_TRY(cudaMemset(h->d_flags, 0, 2 * kMaxPeers * sizeof(uint64_t)));
+    SLBM_CUDA_TRY(cudaMalloc(&h->d_epoch, sizeof(uint64_t)));
+    SLBM_CUDA_TRY(cudaMalloc(&h->d_done, 2 * kMaxPeers * sizeof(unsigned int)));
+    SLBM_CUDA_TRY(cudaMemset(h->d_done, 0, 2 * kMaxPeers * sizeof(unsigned int)));
+    const uint64_t one = 1;
+    SLBM_CUDA_TRY(cudaMemcpy(h->d_epoch, &one, sizeof(one), cudaMemcpyHostToDevice));
+    for (auto& p : h->ph) p.remote_dst.assign(p.send_peer.size(), nullptr);
+  }
   h->committed = true;
   return SLBM_OK;
 }
@@ -324,6 +473,7 @@ int slbm_halo_start(SlbmHalo* h, int phase, void* after_stream) {
   }
   PhaseProg& p = h->ph[phase];
   const PdfTable t = h->table();
+  if (h->peer) return peer_start(h, p, phase);
   if (p.n_pack) {
     k_pack<<<grid_for(p.n_pack), 256, 0, h->comm>>>(t, p.d_pe, p.d_ps, p.n_pack, h->d_send);
     SLBM_CUDA_TRY(cudaGetLastError());
@@ -419,6 +569,78 @@ int slbm_halo_unpack_host(SlbmHalo* h, int phase, int peer, const double* host_i
     SLBM_CUDA_TRY(cudaGetLastError());
   }
   SLBM_CUDA_TRY(cudaStreamSynchronize(h->comm));
+  return SLBM_OK;
+}
+
+int slbm_halo_use_peer(SlbmHalo* h, int rank) {
+  if (!h) return fail(SLBM_ECONFIG, "null halo");
+  if (h->committed) return fail(SLBM_ECONFIG, "halo already committed");
+  if (rank < 0 || rank >= kMaxPeers) return fail(SLBM_ECONFIG, "peer transport: rank out of range");
+  h->peer = true;
+  h->rank = rank;
+  return SLBM_OK;
+}
+
+int slbm_halo_ipc_handles(const SlbmHalo* h, void* recv_handle, void* flags_handle) {
+  if (!h || !h->committed || !h->peer) return fail(SLBM_ECONFIG, "peer halo not committed");
+  cudaSetDevice(h->device);
+  cudaIpcMemHandle_t a, b;
+  SLBM_CUDA_TRY(cudaIpcGetMemHandle(&a, h->d_recv));
+  SLBM_CUDA_TRY(cudaIpcGetMemHandle(&b, h->d_flags));
+  std::memcpy(recv_handle, &a, sizeof(a));
+  std::memcpy(flags_handle, &b, sizeof(b));
+  return SLBM_OK;
+}
+
+int slbm_halo_recv_section(const SlbmHalo* h, int phase, int peer, int64_t* offset,
+                           int64_t* count) {
+  SLBM_TRY(check_phase(h, phase));
+  if (!h->committed) return fail(SLBM_ECONFIG, "halo not committed");
+  const PhaseProg& p = h->ph[phase];
+  *offset = -1;
+  *count = 0;
+  for (size_t i = 0; i < p.recv_peer.size(); ++i)
+    if (p.recv_peer[i] == peer) {
+      *offset = p.recv_off[i];
+      *count = p.recv_cnt[i];
+    }
+  return SLBM_OK;
+}
+
+int slbm_halo_connect(SlbmHalo* h, int peer, const void* recv_handle, const void* flags_handle,
+                      const int64_t* section_offset, const int64_t* section_count) {
+  if (!h || !h->committed || !h->peer) return fail(SLBM_ECONFIG, "peer halo not committed");
+  if (peer < 0 || peer >= kMaxPeers) return fail(SLBM_ECONFIG, "peer rank out of range");
+  cudaSetDevice(h->device);
+  double* recv = nullptr;
+  uint64_t* flags = nullptr;
+  if (peer == h->rank) {  // loopback: this process's own buffers
+    recv = h->d_recv;
+    flags = h->d_flags;
+  } else {
+    cudaIpcMemHandle_t a, b;
+    std::memcpy(&a, recv_handle, sizeof(a));
+    std::memcpy(&b, flags_handle, sizeof(b));
+    void* pa = nullptr;
+    void* pb = nullptr;
+    SLBM_CUDA_TRY(cudaIpcOpenMemHandle(&pa, a, cudaIpcMemLazyEnablePeerAccess));
+    SLBM_CUDA_TRY(cudaIpcOpenMemHandle(&pb, b, cudaIpcMemLazyEnablePeerAccess));
+    h->opened.push_back(pa);
+    h->opened.push_back(pb);
+    recv = static_cast<double*>(pa);
+    flags = static_cast<uint64_t*>(pb);
+  }
+  h->peer_recv[peer] = recv;
+  h->peer_flags[peer] = flags;
+  for (int ph = 0; ph < 2; ++ph) {
+    PhaseProg& p = h->ph[ph];
+    for (size_t i = 0; i < p.send_peer.size(); ++i) {
+      if (p.send_peer[i] != peer) continue;
+      if (section_count[ph] != p.send_cnt[i] || section_offset[ph] < 0)
+        return fail(SLBM_EPROTOCOL, "peer transport: message length disagrees with the receiver");
+      p.remote_dst[i] = recv + section_offset[ph];
+    }
+  }
   return SLBM_OK;
 }
 

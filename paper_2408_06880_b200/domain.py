@@ -723,7 +723,9 @@ def _cudart():
 class DistributedDomain(Domain):
     """One process per GPU.  Blocks go to ranks by ``assignment`` (default:
     the reference's Hilbert/greedy ``balance``); cross-rank edges use NCCL
-    through the library's own communicator (``transport="nccl"``), or host
+    through the library's own communicator (``transport="nccl"``), peer
+    memory — the pack kernel storing into the peers' buffers through CUDA IPC
+    over NVLink, epoch flags instead of NCCL (``transport="p2p"``) — or host
     staging over a gloo group (``transport="host"``)."""
 
     def __init__(self, global_flags, block_size, stencil, params, pattern="aa", frame_width="halo",
@@ -736,15 +738,19 @@ class DistributedDomain(Domain):
         world = dist.get_world_size() if world is None else world
         # loopback (tests): all edges become NCCL messages from this rank to itself
         self._loopback = bool(loopback)
-        if loopback and comm is None:
+        if loopback and comm is None and transport == "nccl":
             comm = NcclComm(rank, 1, default_device() if device is None else device)
         if assignment is None:
             assignment = _balance_without_engines(global_flags, block_size, stencil, world)
-        if transport not in ("nccl", "host"):
+        if transport not in ("nccl", "host", "p2p"):
             raise errors.make("ConfigurationError", f"unknown transport {transport!r}")
         if halo_factory is None and transport == "host":
             group = dist.new_group(backend="gloo") if dist.get_backend() != "gloo" else None
             halo_factory = lambda dev: HostStagedHalo(dev, group, world)  # noqa: E731
+        if halo_factory is None and transport == "p2p":
+            # peer memory over NVLink: loopback keeps every edge a message to itself
+            peer = (0, 1, None) if loopback else (rank, world, None)
+            halo_factory = lambda dev: DeviceHalo(dev, peer=peer)  # noqa: E731
         if comm is None and world > 1 and transport == "nccl" and halo_factory is None:
             comm = NcclComm(rank, world, default_device() if device is None else device)
         super().__init__(global_flags, block_size, stencil, params, pattern=pattern,

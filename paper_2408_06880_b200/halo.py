@@ -187,15 +187,24 @@ def _i64(a):
 
 
 class DeviceHalo:
-    """The CUDA exchange program of one process (slbm_halo_*)."""
+    """The CUDA exchange program of one process (slbm_halo_*).
 
-    def __init__(self, device: int):
+    ``peer=(rank, world, group)`` selects the peer transport: remote
+    messages are stored by the pack kernel straight into the peers' receive
+    buffers (CUDA IPC over NVLink) with epoch flags instead of NCCL; the
+    IPC handles and receive sections travel once through ``group`` (any
+    torch.distributed backend; not used when world == 1)."""
+
+    def __init__(self, device: int, peer: tuple | None = None):
         self.device = int(device)
         h = C.c_void_p()
         _abi.call("slbm_halo_create", self.device, C.byref(h))
         self._h = h
         self.committed = False
         self.has_remote = False
+        self.peer = peer
+        if peer is not None:
+            _abi.call("slbm_halo_use_peer", self._h, int(peer[0]))
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
@@ -229,6 +238,45 @@ class DeviceHalo:
     def commit(self, nccl_comm: int | None = None):
         _abi.call("slbm_halo_commit", self._h, C.c_void_p(nccl_comm or 0))
         self.committed = True
+        if self.peer is not None:
+            self._connect_peers()
+
+    def _connect_peers(self):
+        rank, world, group = self.peer
+        recv_h = (C.c_char * 64)()
+        flag_h = (C.c_char * 64)()
+        _abi.call("slbm_halo_ipc_handles", self._h, C.cast(recv_h, C.c_void_p),
+                  C.cast(flag_h, C.c_void_p))
+        # per sender s and phase: where s's message lands in this rank's buffer
+        sections = {}
+        for s in range(world):
+            rows = []
+            for ph in (Phase.CANONICAL, Phase.REVERSED):
+                off, cnt = C.c_int64(), C.c_int64()
+                _abi.call("slbm_halo_recv_section", self._h, ph.value, s, C.byref(off),
+                          C.byref(cnt))
+                rows.append((off.value, cnt.value))
+            sections[s] = rows
+        mine = {"rank": rank, "recv": bytes(recv_h), "flags": bytes(flag_h), "sections": sections}
+        if world == 1:
+            infos = [mine]
+        else:
+            import torch.distributed as dist
+
+            infos = [None] * world
+            dist.all_gather_object(infos, mine, group=group)
+        for info in infos:
+            r = info["rank"]
+            to_r = info["sections"][rank]  # my message's place in r's buffer, per phase
+            from_r = sections[r]           # r's message in my buffer
+            if not any(c for _, c in to_r) and not any(c for _, c in from_r):
+                continue
+            off = np.array([o for o, _ in to_r], np.int64)
+            cnt = np.array([c for _, c in to_r], np.int64)
+            a = (C.c_char * 64).from_buffer_copy(info["recv"])
+            b = (C.c_char * 64).from_buffer_copy(info["flags"])
+            _abi.call("slbm_halo_connect", self._h, r, C.cast(a, C.c_void_p),
+                      C.cast(b, C.c_void_p), _abi.ptr(off, C.c_int64), _abi.ptr(cnt, C.c_int64))
 
     def start(self, phase: Phase, after_stream: int | None):
         _abi.call("slbm_halo_start", self._h, phase.value, C.c_void_p(after_stream or 0))

@@ -3,6 +3,9 @@
 * loopback: every halo edge travels as a real NCCL message (ncclSend /
   ncclRecv inside one group on the comm stream) from rank 0 to itself, so
   pack kernel -> NCCL -> unpack kernel is exercised exactly as between GPUs;
+* the peer transport (CUDA IPC + epoch flags, no NCCL) in loopback and with
+  two processes sharing the GPU through IPC mappings of each other's
+  buffers;
 * two processes sharing the GPU with the host-staged transport (gloo),
   blocks split between the ranks by the reference's balance.
 
@@ -37,7 +40,24 @@ def test_nccl_loopback_matches_golden(name, pattern, gpu_lib):
     np.testing.assert_array_equal(dom.gather_canonical(), rec[f"{pattern}_final"])
 
 
-def _worker(rank, world, port, path, pattern, out_dir):
+@pytest.mark.parametrize("pattern", ["aa", "pull"])
+@pytest.mark.parametrize("name", ["domain_d3q19_2x2x2", "domain_d3q27_riverbed"])
+def test_peer_loopback_matches_golden(name, pattern, gpu_lib):
+    """Peer transport, every edge a message to this rank through its own
+    buffers: remote pack -> release flag -> acquire wait -> unpack -> ack."""
+    from paper_2408_06880_b200.domain import DistributedDomain
+
+    rec = load_golden(DOMAIN[name])
+    for use_graph in (False, True):
+        dom = DistributedDomain(flags_of(rec), tuple(int(b) for b in rec["block"]),
+                                stencil_of(rec), params_of(rec), pattern=pattern, frame_width=1,
+                                rank=0, world=1, device=0, loopback=True, transport="p2p")
+        dom.init_random(int(rec["seed"]))
+        dom.run(int(rec["steps"]), driver="overlapped", use_graph=use_graph)
+        np.testing.assert_array_equal(dom.gather_canonical(), rec[f"{pattern}_final"])
+
+
+def _worker(rank, world, port, path, pattern, out_dir, transport="host"):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -48,7 +68,7 @@ def _worker(rank, world, port, path, pattern, out_dir):
     rec = load_golden(path)
     dom = DistributedDomain(flags_of(rec), tuple(int(b) for b in rec["block"]), stencil_of(rec),
                             params_of(rec), pattern=pattern, frame_width=1, rank=rank, world=world,
-                            device=0, transport="host")
+                            device=0, transport=transport)
     dom.init_random(int(rec["seed"]))
     dom.run(int(rec["steps"]), driver="overlapped")
     full = dom.gather_canonical_global()
@@ -70,5 +90,16 @@ def test_two_ranks_host_staged_match_golden(name, pattern, tmp_path, gpu_lib):
     path = DOMAIN[name]
     mp.start_processes(_worker, args=(2, _free_port(), path, pattern, str(tmp_path)), nprocs=2,
                        join=True, start_method="spawn")
+    rec = load_golden(path)
+    np.testing.assert_array_equal(np.load(tmp_path / "full.npy"), rec[f"{pattern}_final"])
+
+
+@pytest.mark.parametrize("name,pattern", [("domain_d3q19_2x2x2", "aa")])
+def test_two_ranks_peer_ipc_match_golden(name, pattern, tmp_path, gpu_lib):
+    """Two processes on one GPU, each mapping the other's receive buffer and
+    flags through CUDA IPC: the same code path as two GPUs over NVLink."""
+    path = DOMAIN[name]
+    mp.start_processes(_worker, args=(2, _free_port(), path, pattern, str(tmp_path), "p2p"),
+                       nprocs=2, join=True, start_method="spawn")
     rec = load_golden(path)
     np.testing.assert_array_equal(np.load(tmp_path / "full.npy"), rec[f"{pattern}_final"])

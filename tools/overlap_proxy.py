@@ -53,13 +53,13 @@ n_fluid = eng.n_fluid
 del eng
 torch.cuda.empty_cache()
 
-for name in ("local", "nccl_loopback"):
+for name in ("local", "nccl_loopback", "p2p_loopback"):
     block = (edge, edge, edge // slabs)
     if name == "local":
         d = Domain(fl, block, st, p, pattern="aa", frame_width="halo", check="deferred")
     else:
         d = DistributedDomain(fl, block, st, p, pattern="aa", rank=0, world=1, device=0,
-                              loopback=True)
+                              loopback=True, transport=name.split("_")[0])
     d.init_equilibrium(1.0, np.array([0.01, 0.0, 0.0]))
     d.run(4, driver="overlapped", use_graph=True)
     s = torch.cuda.ExternalStream(d.stream())
