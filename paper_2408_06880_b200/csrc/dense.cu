@@ -111,9 +111,14 @@ __device__ __forceinline__ bool in_phase(const DenseArgs& a, int64_t x, int64_t 
 // sparse sweep's idx prefetch (sweep.cuh), each CTA touches into L2 the mask
 // chunk of the row `ahead` rows later (4 lines of 128 B), so that CTA's mask
 // load is an L2 hit.
-template <class L, int MODEL, int KIND>
-__global__ void __launch_bounds__(128, 4) k_dense(const DenseArgs a,
-                                                                uint32_t ahead) {
+//
+// SPEC (blocks of porosity >= 0.75 — the ones the hybrid policy makes dense):
+// the PDF loads do not wait for the mask.  The cell-local step loads its own
+// slots and drops a solid cell's values afterwards; the index-free combined
+// step loads every upwind neighbour's slot and re-reads only the folded
+// directions (walls), which are rare in such blocks.
+template <class L, int MODEL, int KIND, bool SPEC>
+__global__ void __launch_bounds__(128, 4) k_dense(const DenseArgs a, uint32_t ahead) {
   const int32_t X = a.g.n[0], Y = a.g.n[1], Z = a.g.n[2];
   // CTA b -> (row, chunk) with the chunk fastest: consecutive CTAs sweep
   // consecutive memory of every direction plane (rows on the slow index
@@ -133,7 +138,7 @@ __global__ void __launch_bounds__(128, 4) k_dense(const DenseArgs a,
   const int32_t y = row % Y, z = row / Y;
   const uint32_t i = uint32_t(row) * uint32_t(X) + uint32_t(x);
   const uint32_t m = a.mask[i];
-  if (m == kSolid) return;
+  if (!SPEC && m == kSolid) return;
   if (!in_phase(a, x, y, z)) return;
   const uint32_t PX = uint32_t(a.g.p[0]), PY = uint32_t(a.g.p[1]);
   const uint32_t p = ((uint32_t(z + a.g.off[2]) * PY) + uint32_t(y + 1)) * PX + uint32_t(x + 1);
@@ -146,6 +151,7 @@ __global__ void __launch_bounds__(128, 4) k_dense(const DenseArgs a,
       constexpr int qb = L::INV[q];
       t[q] = pdf[uint32_t(qb) * np + p];
     });
+    if (SPEC && m == kSolid) return;  // loads above were harmless reads
     bad = collide<L, MODEL>(t, a.omega, a.lam, [&](auto q, double v) {
       pdf[uint32_t(decltype(q)::value) * np + p] = v;
     });
@@ -154,20 +160,35 @@ __global__ void __launch_bounds__(128, 4) k_dense(const DenseArgs a,
                       (L::DIM == 3 && (z == 0 || z == Z - 1));
     uint32_t addr[L::Q];
     addr[0] = p;
+    // upwind slots (periodic in-block wrap only on face cells)
     if (!face) {
+      sfor<1, L::Q>([&](auto q) { addr[q] = uint32_t(int(q)) * np + p - uint32_t(a.stride[q]); });
+    } else {
       sfor<1, L::Q>([&](auto q) {
-        constexpr int qb = L::INV[q];
-        addr[q] = ((m >> q) & 1u) ? uint32_t(qb) * np + p
-                                  : uint32_t(int(q)) * np + p - uint32_t(a.stride[q]);
+        addr[q] = uint32_t(int(q)) * np + p - uint32_t(a.stride[q]) +
+                  uint32_t(wrap_delta<L, q>(a, x, y, z));
       });
+    }
+    constexpr uint32_t kFolds = (L::Q == 32 ? 0xffffffffu : ((1u << L::Q) - 1u)) & ~1u;
+    if constexpr (SPEC) {
+      sfor<0, L::Q>([&](auto q) { t[q] = pdf[addr[q]]; });
+      if (m == kSolid) return;
+      if (m & kFolds) {  // wall reads: the cell's own opposite slot instead
+        sfor<1, L::Q>([&](auto q) {
+          constexpr int qb = L::INV[q];
+          if ((m >> q) & 1u) {
+            addr[q] = uint32_t(qb) * np + p;
+            t[q] = pdf[addr[q]];
+          }
+        });
+      }
     } else {
       sfor<1, L::Q>([&](auto q) {
         constexpr int qb = L::INV[q];
-        const uint32_t src = p - uint32_t(a.stride[q]) + uint32_t(wrap_delta<L, q>(a, x, y, z));
-        addr[q] = ((m >> q) & 1u) ? uint32_t(qb) * np + p : uint32_t(int(q)) * np + src;
+        if ((m >> q) & 1u) addr[q] = uint32_t(qb) * np + p;
       });
+      sfor<0, L::Q>([&](auto q) { t[q] = pdf[addr[q]]; });
     }
-    sfor<0, L::Q>([&](auto q) { t[q] = pdf[addr[q]]; });
     if (m & kHasUbb) {
       sfor<1, L::Q>([&](auto q) {
         if ((m >> q) & 1u) t[q] += ubb_corr_of(a, i, q);
@@ -423,16 +444,25 @@ int dense_step(SlbmEngine* e, int phase) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint32_t ahead = uint32_t(sms);  // ~ a quarter wave of 128-thread CTAs
+  // speculative loads pay off when few box cells are solid
+  const bool spec = double(e->n_fluid) >= 0.75 * double(e->geo.n_cells());
   with_lattice(e->q, [&](auto lat) {
     using L = decltype(lat);
     auto go = [&](auto model) {
       constexpr int M = decltype(model)::value;
-      if (kind == 0)
-        k_dense<L, M, 0><<<grid, 128, 0, e->stream>>>(a, ahead);
-      else if (kind == 1)
-        k_dense<L, M, 1><<<grid, 128, 0, e->stream>>>(a, ahead);
+      auto launch = [&](auto sp) {
+        constexpr bool S = decltype(sp)::value;
+        if (kind == 0)
+          k_dense<L, M, 0, S><<<grid, 128, 0, e->stream>>>(a, ahead);
+        else if (kind == 1)
+          k_dense<L, M, 1, S><<<grid, 128, 0, e->stream>>>(a, ahead);
+        else
+          k_dense<L, M, 2, S><<<grid, 128, 0, e->stream>>>(a, ahead);
+      };
+      if (spec)
+        launch(std::true_type{});
       else
-        k_dense<L, M, 2><<<grid, 128, 0, e->stream>>>(a, ahead);
+        launch(std::false_type{});
     };
     if (e->model == SLBM_SRT)
       go(std::integral_constant<int, SLBM_SRT>{});
