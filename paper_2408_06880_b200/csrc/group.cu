@@ -55,6 +55,19 @@ struct SlbmGroup {
   unsigned long long** steps = nullptr;  // per engine d_step
   int flip = 0;  // pull: which buffer of each engine is current
   bool has_outlets = false;
+  // batched outlet program: entry -> (engine, index in its outlet arrays)
+  struct OutletTab* out_tab = nullptr;
+  uint16_t* out_eng = nullptr;
+  uint32_t* out_idx = nullptr;
+  int64_t n_out = 0;
+};
+
+// an engine's outlet program arrays (kernels.cu k_outlet reads the same)
+struct OutletTab {
+  const uint32_t *slot, *partner, *cell;
+  const uint8_t* dir;
+  const double* rho;
+  double* u;
 };
 
 namespace {
@@ -143,6 +156,19 @@ __global__ void k_group_refresh(const GroupArgs* table, const uint16_t* eng, con
     pdf[slot[i]] = pdf[partner[i]] + corr[i];
   else
     pdf[partner[i]] = pdf[slot[i]] + corr[i];
+}
+
+template <class L>
+__global__ void k_group_outlet(const GroupArgs* table, const OutletTab* ot, const uint16_t* eng,
+                               const uint32_t* idx, int64_t n, int parity) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int e = eng[i];
+  const uint32_t k = idx[i];
+  const OutletTab& o = ot[e];
+  const GroupArgs& a = table[e];
+  outlet_entry<L>(a.pdf, a.base, o.slot[k], o.partner[k], o.cell[k], o.dir[k], o.rho[k],
+                  o.u + 3 * size_t(k), parity);
 }
 
 __global__ void k_group_advance(unsigned long long** steps, int n) {
@@ -238,6 +264,26 @@ int slbm_group_create(SlbmEngine** engines, int n, SlbmGroup** out) {
   // concatenated UBB program with engine ids
   for (int i = 0; i < n; ++i) g->n_ubb += engines[i]->n_ubb;
   for (int i = 0; i < n; ++i) g->has_outlets |= engines[i]->n_out > 0;
+  if (g->has_outlets) {
+    std::vector<OutletTab> tab(n);
+    std::vector<uint16_t> oe;
+    std::vector<uint32_t> oi;
+    for (int i = 0; i < n; ++i) {
+      SlbmEngine* e = engines[i];
+      tab[i] = OutletTab{e->out_slot, e->out_partner, e->out_cell, e->out_dir, e->out_rho, e->out_u};
+      for (int64_t k = 0; k < e->n_out; ++k) {
+        oe.push_back(uint16_t(i));
+        oi.push_back(uint32_t(k));
+      }
+    }
+    g->n_out = int64_t(oe.size());
+    SLBM_CUDA_TRY(cudaMalloc(&g->out_tab, n * sizeof(OutletTab)));
+    SLBM_CUDA_TRY(cudaMemcpy(g->out_tab, tab.data(), n * sizeof(OutletTab), cudaMemcpyHostToDevice));
+    SLBM_CUDA_TRY(cudaMalloc(&g->out_eng, oe.size() * sizeof(uint16_t)));
+    SLBM_CUDA_TRY(cudaMemcpy(g->out_eng, oe.data(), oe.size() * 2, cudaMemcpyHostToDevice));
+    SLBM_CUDA_TRY(cudaMalloc(&g->out_idx, oi.size() * sizeof(uint32_t)));
+    SLBM_CUDA_TRY(cudaMemcpy(g->out_idx, oi.data(), oi.size() * 4, cudaMemcpyHostToDevice));
+  }
   if (g->n_ubb) {
     SLBM_CUDA_TRY(cudaMalloc(&g->ubb_eng, g->n_ubb * sizeof(uint16_t)));
     SLBM_CUDA_TRY(cudaMalloc(&g->ubb_slot, g->n_ubb * sizeof(uint32_t)));
@@ -273,7 +319,8 @@ int slbm_group_destroy(SlbmGroup* g) {
       if (g->table[p][f]) cudaFree(g->table[p][f]);
     if (g->cta_start[p]) cudaFree(g->cta_start[p]);
   }
-  void* ptrs[] = {g->ubb_eng, g->ubb_slot, g->ubb_partner, g->ubb_corr, g->steps};
+  void* ptrs[] = {g->ubb_eng, g->ubb_slot, g->ubb_partner, g->ubb_corr, g->steps,
+                  g->out_tab, g->out_eng, g->out_idx};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete g;
@@ -290,18 +337,14 @@ int slbm_group_refresh(SlbmGroup* g, int parity, void* stream) {
         g->table[0][flip], g->ubb_eng, g->ubb_slot, g->ubb_partner, g->ubb_corr, g->n_ubb, parity);
     SLBM_CUDA_TRY(cudaGetLastError());
   }
-  if (g->has_outlets) {  // few outlet blocks: per-engine launches
-    for (SlbmEngine* e : g->engines) {
-      if (!e->n_out) continue;
-      cudaStream_t keep = e->stream;
-      e->stream = s;
-      const int n_ubb = int(e->n_ubb);
-      e->n_ubb = 0;  // UBB already done above
-      int st = launch_refresh(e, parity);
-      e->n_ubb = n_ubb;
-      e->stream = keep;
-      if (st != SLBM_OK) return st;
-    }
+  if (g->n_out) {  // every outlet entry of every block: one launch
+    const int flip = g->pattern == SLBM_PULL ? g->flip : 0;
+    on_lattice(g->q, [&](auto lat) {
+      using L = decltype(lat);
+      k_group_outlet<L><<<unsigned((g->n_out + 127) / 128), 128, 0, s>>>(
+          g->table[0][flip], g->out_tab, g->out_eng, g->out_idx, g->n_out, parity);
+    });
+    SLBM_CUDA_TRY(cudaGetLastError());
   }
   return SLBM_OK;
 }

@@ -221,61 +221,16 @@ __global__ void k_refresh(double* pdf, const uint32_t* slot, const uint32_t* par
 
 __global__ void k_advance(unsigned long long* step) { *step += 1; }
 
-// Fixed-density outlet (extension; the reference has none).
-// Anti-bounce-back for a read of direction q from an OUTLET cell:
-//   f_q = 2 w_q rho_o (1 + 4.5 (c_q.u)^2 - 1.5 u.u) - f*_{inv q}
-// u = velocity of the adjacent fluid cell from its EVEN-parity slots
-// (post-collision, momentum conserving), kept for the following ODD refresh.
-// EVEN fills the appended outlet slot, ODD the cell's partner slot, mirroring
-// the UBB refresh (sparse.py:301-304).  CPU restatement:
-// oracle/sparse_ref.py OracleSparseEngine._refresh_outlet (same op order).
+// Fixed-density outlet (extension; the reference has none):
+// outlet_entry (sweep.cuh) per appended outlet slot.
 template <class L>
 __global__ void k_outlet(double* pdf, SweepArgs a, const uint32_t* slot, const uint32_t* partner,
                          const uint32_t* cell, const uint8_t* dir, const double* rho_o,
                          double* u_store, uint32_t n, int parity) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  double u[3];
-  if (parity == SLBM_EVEN) {
-    const uint32_t c = cell[i];
-    double t[L::Q];
-    sfor<0, L::Q>([&](auto q) { t[q] = pdf[a.base[q] + c]; });
-    double rho = t[0] + t[1];
-    sfor<2, L::Q>([&](auto q) { rho = rho + t[q]; });
-    u[0] = component_sum<L, 0>(t) / rho;
-    u[1] = component_sum<L, 1>(t) / rho;
-    u[2] = (L::DIM == 3) ? component_sum<L, 2>(t) / rho : 0.0;
-    for (int k = 0; k < 3; ++k) u_store[3 * i + k] = u[k];
-  } else {
-    for (int k = 0; k < 3; ++k) u[k] = u_store[3 * i + k];
-  }
-  double usq = u[0] * u[0];
-  usq = usq + u[1] * u[1];
-  if constexpr (L::DIM == 3) usq = usq + u[2] * u[2];
-  // c_q . u, seeded with the first nonzero component (x, y, z order)
-  int cq[3] = {0, 0, 0};
-  double w = 0.0;
-  const int qd = dir[i];
-  sfor<0, L::Q>([&](auto q) {
-    if (qd == decltype(q)::value) {
-      cq[0] = L::CX[q];
-      cq[1] = L::CY[q];
-      cq[2] = L::CZ[q];
-      w = weight<L>(q);
-    }
-  });
-  double cu = 0.0;
-  bool any = false;
-  for (int k = 0; k < L::DIM; ++k) {
-    if (cq[k] == 0) continue;
-    cu = any ? (cq[k] > 0 ? cu + u[k] : cu - u[k]) : (cq[k] > 0 ? u[k] : -u[k]);
-    any = true;
-  }
-  const double feq_sym = (w * rho_o[i]) * ((1.0 + (4.5 * cu) * cu) - 1.5 * usq);
-  if (parity == SLBM_EVEN)
-    pdf[slot[i]] = 2.0 * feq_sym - pdf[partner[i]];
-  else
-    pdf[partner[i]] = 2.0 * feq_sym - pdf[slot[i]];
+  outlet_entry<L>(pdf, a.base, slot[i], partner[i], cell[i], dir[i], rho_o[i], u_store + 3 * i,
+                  parity);
 }
 
 // canonical (q, n) values per cell straight from the groups (sparse.py:308-321)

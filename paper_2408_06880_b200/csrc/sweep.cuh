@@ -2,7 +2,7 @@
 // engine kernels (kernels.cu) and the block-group kernels (group.cu).
 #pragma once
 
-#include "common.cuh"
+#include "collide.cuh"
 
 namespace slbm {
 
@@ -36,6 +36,60 @@ __device__ __forceinline__ void prefetch_idx_ahead(const uint32_t* idx, uint32_t
   if (pos >= end) return;
   const uint32_t cell = cids ? __ldcs(cids + pos) : pos;
   prefetch_l2(idx + size_t(row) * pitch + cell);
+}
+
+// Fixed-density outlet (extension; the reference has none).
+// Anti-bounce-back for a read of direction q from an OUTLET cell:
+//   f_q = 2 w_q rho_o (1 + 4.5 (c_q.u)^2 - 1.5 u.u) - f*_{inv q}
+// u = velocity of the adjacent fluid cell from its EVEN-parity slots
+// (post-collision, momentum conserving), kept for the following ODD refresh.
+// EVEN fills the appended outlet slot, ODD the cell's partner slot, mirroring
+// the UBB refresh (sparse.py:301-304).  CPU restatement:
+// oracle/sparse_ref.py OracleSparseEngine._refresh_outlet (same op order).
+// `base` = device group starts; `u_store` = this entry's 3 velocity words.
+template <class L>
+__device__ __forceinline__ void outlet_entry(double* pdf, const uint32_t* base, uint32_t slot,
+                                             uint32_t partner, uint32_t c, int qd, double rho_o,
+                                             double* u_store, int parity) {
+  double u[3];
+  if (parity == SLBM_EVEN) {
+    double t[L::Q];
+    sfor<0, L::Q>([&](auto q) { t[q] = pdf[base[q] + c]; });
+    double rho = t[0] + t[1];
+    sfor<2, L::Q>([&](auto q) { rho = rho + t[q]; });
+    u[0] = component_sum<L, 0>(t) / rho;
+    u[1] = component_sum<L, 1>(t) / rho;
+    u[2] = (L::DIM == 3) ? component_sum<L, 2>(t) / rho : 0.0;
+    for (int k = 0; k < 3; ++k) u_store[k] = u[k];
+  } else {
+    for (int k = 0; k < 3; ++k) u[k] = u_store[k];
+  }
+  double usq = u[0] * u[0];
+  usq = usq + u[1] * u[1];
+  if constexpr (L::DIM == 3) usq = usq + u[2] * u[2];
+  // c_q . u, seeded with the first nonzero component (x, y, z order)
+  int cq[3] = {0, 0, 0};
+  double w = 0.0;
+  sfor<0, L::Q>([&](auto q) {
+    if (qd == decltype(q)::value) {
+      cq[0] = L::CX[q];
+      cq[1] = L::CY[q];
+      cq[2] = L::CZ[q];
+      w = weight<L>(q);
+    }
+  });
+  double cu = 0.0;
+  bool any = false;
+  for (int k = 0; k < L::DIM; ++k) {
+    if (cq[k] == 0) continue;
+    cu = any ? (cq[k] > 0 ? cu + u[k] : cu - u[k]) : (cq[k] > 0 ? u[k] : -u[k]);
+    any = true;
+  }
+  const double feq_sym = (w * rho_o) * ((1.0 + (4.5 * cu) * cu) - 1.5 * usq);
+  if (parity == SLBM_EVEN)
+    pdf[slot] = 2.0 * feq_sym - pdf[partner];
+  else
+    pdf[partner] = 2.0 * feq_sym - pdf[slot];
 }
 
 }  // namespace slbm

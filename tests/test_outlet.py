@@ -94,3 +94,35 @@ def test_gpu_outlet_bitwise_equals_restatement(name, pattern, model, gpu_lib):
     rc, uc = cpu.macroscopic_fields()
     np.testing.assert_array_equal(rg, rc)
     np.testing.assert_array_equal(ug, uc)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pattern", ["aa", "pull"])
+def test_gpu_outlets_in_block_group_equal_single_block(pattern, gpu_lib):
+    """Several blocks with inlet and outlet faces run as one block group
+    (batched UBB and outlet refresh, group sweeps): same bits as one engine."""
+    from paper_2408_06880_b200 import geometry
+    from paper_2408_06880_b200.domain import Domain
+    from paper_2408_06880_b200.engine import SparseEngine
+
+    st = make_stencil("d3q19")
+    dims = (24, 8, 8)
+    inlet = FaceSpec(FaceKind.WALL, velocity=(0.02, 0.0, 0.0))
+    outlet = FaceSpec(FaceKind.WALL, density=1.0)
+    fl = make_flags(dims, [(inlet, outlet), (WALL, WALL), (WALL, WALL)],
+                    solid=geometry.random_obstacles(dims, 0.85, 5))
+    p = CollisionParams(1.3, "trt", 0.9)
+    one = SparseEngine(fl, st, p, pattern)
+    one.init_equilibrium()
+    drive(one, 12)
+    dom = Domain(fl, (8, 8, 8), st, p, pattern=pattern, frame_width=1)
+    assert dom._group is not None and len(dom.local_engines()) == 3
+    dom.init_equilibrium()
+    dom.run(12, driver="overlapped")
+    rho_d, u_d = dom.gather_macroscopics()
+    rho_1, u_1 = one.macroscopic_fields()
+    np.testing.assert_array_equal(rho_d, rho_1)
+    np.testing.assert_array_equal(u_d, u_1)
+    box = dom.gather_canonical()  # (q, z, y, x) over the box
+    x, y, z = one.fluid_coords.T
+    np.testing.assert_array_equal(box[:, z, y, x], one.canonical_state())
