@@ -117,6 +117,10 @@ int slbm_export_lists(const SlbmEngine* eng, uint32_t* idx, int64_t* fluid_coord
                       int64_t* ubb_slot, int64_t* ubb_partner, double* ubb_corr,
                       int64_t* ghost_q, int64_t* ghost_pflat, int64_t* ghost_slot);
 /* frame / interior cell ids (sparse.py:80-88); NULL pointers skipped */
+/* per-face interior/frame split (extension): frame = cells within lo[a] of
+ * the low face or hi[a] of the high face of axis a (0 = none); the
+ * reference's frame_mask (flags.py:83-108) is lo == hi >= 1.  Sparse only. */
+int slbm_engine_set_frame(SlbmEngine* eng, const int32_t* lo, const int32_t* hi);
 int slbm_export_split(const SlbmEngine* eng, int64_t* interior, int64_t* frame);
 
 /* ---- state (sparse.py:199-222, :308-331) --------------------------------- */
@@ -206,6 +210,11 @@ int slbm_halo_peer_sizes(const SlbmHalo* halo, int phase, int npeers, int64_t* s
 int slbm_halo_pack_host(SlbmHalo* halo, int phase, int peer, double* host_out);
 int slbm_halo_unpack_host(SlbmHalo* halo, int phase, int peer, const double* host_in);
 int slbm_halo_local(SlbmHalo* halo, int phase); /* only the local edges, on comm stream */
+/* start without the local edges / run only the local edges on `stream`:
+ * the overlapped driver runs local edges ahead of the interior sweep on the
+ * compute stream when frames cover only the faces with remote neighbours  */
+int slbm_halo_start_ex(SlbmHalo* halo, int phase, void* after_stream, int with_local);
+int slbm_halo_local_on(SlbmHalo* halo, int phase, void* stream);
 
 /* NCCL communicator from a 128-byte ncclUniqueId (broadcast by the caller) */
 int slbm_nccl_comm_init(const void* unique_id, int nranks, int rank, int device, void** comm);

@@ -91,6 +91,9 @@ SIGNATURES = {
     "slbm_halo_pack_host": [vp, C.c_int, C.c_int, c_dp],
     "slbm_halo_unpack_host": [vp, C.c_int, C.c_int, c_dp],
     "slbm_halo_local": [vp, C.c_int],
+    "slbm_halo_start_ex": [vp, C.c_int, vp, C.c_int],
+    "slbm_halo_local_on": [vp, C.c_int, vp],
+    "slbm_engine_set_frame": [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32)],
     "slbm_nccl_comm_init": [vp, C.c_int, C.c_int, C.c_int, C.POINTER(vp)],
     "slbm_nccl_get_unique_id": [vp],
     "slbm_nccl_comm_destroy": [vp],

@@ -392,6 +392,20 @@ int slbm_export_lists(const SlbmEngine* e, uint32_t* idx, int64_t* fluid_coords,
   return SLBM_OK;
 }
 
+int slbm_engine_set_frame(SlbmEngine* e, const int32_t* lo, const int32_t* hi) {
+  CHECK_ENGINE(e);
+  if (e->layout) return fail(SLBM_ECONFIG, "per-face frames are for sparse engines");
+  if (!lo || !hi) return fail(SLBM_ECONFIG, "null widths");
+  int32_t l[3] = {0, 0, 0}, h[3] = {0, 0, 0};
+  for (int a = 0; a < e->dim; ++a) {
+    if (lo[a] < 0 || hi[a] < 0) return fail(SLBM_ECONFIG, "frame widths must be >= 0");
+    l[a] = lo[a];
+    h[a] = hi[a];
+  }
+  DeviceGuard guard(e->device);
+  return set_frame(e, l, h);
+}
+
 int slbm_export_split(const SlbmEngine* e, int64_t* interior, int64_t* frame) {
   CHECK_ENGINE(e);
   if (!e->has_split) return fail(SLBM_ECONFIG, "engine has no split lists; build with frame_width");

@@ -80,16 +80,18 @@ struct ReadsTag {
   }
 };
 
+// frame cell: within lo[a] of the low face or hi[a] of the high face of any
+// axis (flags.py:83-108 uses lo == hi)
 struct InFrame {
   const uint32_t* x_flat;
   Geometry g;
-  int32_t w[3];
+  int32_t lo[3], hi[3];
   bool want;
   __device__ bool operator()(uint32_t c) const {
     int64_t v[3];
     g.coords(x_flat[c], v[0], v[1], v[2]);
     bool in = false;
-    for (int a = 0; a < g.dim; ++a) in |= (v[a] < w[a]) || (v[a] >= g.n[a] - w[a]);
+    for (int a = 0; a < g.dim; ++a) in |= (v[a] < lo[a]) || (v[a] >= g.n[a] - hi[a]);
     return in == want;
   }
 };
@@ -651,45 +653,70 @@ int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
   }
 
   // -- interior / frame split (sparse.py:80-88) --
+  int st = SLBM_OK;
   if (frame_width) {
-    InFrame fr{e->x_flat, g, {1, 1, 1}, true};
-    for (int a = 0; a < 3; ++a) {
-      int32_t w = a < g.dim ? frame_width[a] : 1;
-      fr.w[a] = std::min<int32_t>(w, g.n[a]);
-    }
-    // frame: explicit cell list; interior: the complement, as a bitmask
-    int64_t nf = 0;
-    SLBM_TRY(select_if(thrust::counting_iterator<uint32_t>(0), sel_buf, n, fr, &nf, s));
-    SLBM_TRY(dalloc(e, &e->frame_cids, nf));
-    SLBM_CUDA_TRY(cudaMemcpyAsync(e->frame_cids, sel_buf, nf * sizeof(uint32_t),
-                                  cudaMemcpyDeviceToDevice, s));
-    e->n_frame = nf;
-    e->n_interior = n - nf;
-    e->has_split = true;
-    // frame = a cid prefix + a cid suffix (faces only across z, e.g. slab
-    // decompositions): the interior is one contiguous cid range and needs
-    // no mask at all
-    std::vector<uint32_t> h(size_t(std::max<int64_t>(nf, 1)));
-    if (nf)
-      SLBM_CUDA_TRY(cudaMemcpyAsync(h.data(), e->frame_cids, nf * 4, cudaMemcpyDeviceToHost, s));
-    SLBM_CUDA_TRY(cudaStreamSynchronize(s));
-    int64_t lo = 0;
-    while (lo < nf && int64_t(h[lo]) == lo) ++lo;
-    const int64_t hi = n - (nf - lo);
-    bool ranged = true;
-    for (int64_t k = lo; k < nf && ranged; ++k) ranged = int64_t(h[k]) == hi + (k - lo);
-    if (ranged) {
-      e->interior_lo = lo;
-    } else {
-      e->interior_lo = -1;
-      SLBM_TRY(dalloc(e, &e->frame_bits, (n + 31) / 32));
-      k_frame_bits<<<grid_for(n, 256), 256, 0, s>>>(fr, n, e->frame_bits);
-      SLBM_CUDA_TRY(cudaGetLastError());
-    }
+    int32_t w[3];
+    for (int a = 0; a < 3; ++a) w[a] = a < g.dim ? frame_width[a] : 1;
+    st = build_split(e, w, w, sel_buf);
   }
   SLBM_CUDA_TRY(cudaStreamSynchronize(s));
   cleanup();
+  return st;
+}
+
+// frame cids (explicit list) and the interior (one cid range, or the
+// complement of a frame bitmask) for per-face widths; `scratch` holds n cids
+int build_split(SlbmEngine* e, const int32_t* lo_w, const int32_t* hi_w, uint32_t* scratch) {
+  const Geometry& g = e->geo;
+  const int64_t n = e->n_fluid;
+  cudaStream_t s = e->stream;
+  InFrame fr{e->x_flat, g, {0, 0, 0}, {0, 0, 0}, true};
+  for (int a = 0; a < 3; ++a) {
+    fr.lo[a] = std::min<int32_t>(lo_w[a], g.n[a]);
+    fr.hi[a] = std::min<int32_t>(hi_w[a], g.n[a]);
+  }
+  if (e->frame_cids) cudaFree(e->frame_cids);
+  if (e->frame_bits) cudaFree(e->frame_bits);
+  e->frame_cids = nullptr;
+  e->frame_bits = nullptr;
+  int64_t nf = 0;
+  SLBM_TRY(select_if(thrust::counting_iterator<uint32_t>(0), scratch, n, fr, &nf, s));
+  SLBM_TRY(dalloc(e, &e->frame_cids, nf));
+  SLBM_CUDA_TRY(cudaMemcpyAsync(e->frame_cids, scratch, nf * sizeof(uint32_t),
+                                cudaMemcpyDeviceToDevice, s));
+  e->n_frame = nf;
+  e->n_interior = n - nf;
+  e->has_split = true;
+  // frame = a cid prefix + a cid suffix (faces only across z, e.g. slab
+  // decompositions): the interior is one contiguous cid range and needs
+  // no mask at all
+  std::vector<uint32_t> h(size_t(std::max<int64_t>(nf, 1)));
+  if (nf)
+    SLBM_CUDA_TRY(cudaMemcpyAsync(h.data(), e->frame_cids, nf * 4, cudaMemcpyDeviceToHost, s));
+  SLBM_CUDA_TRY(cudaStreamSynchronize(s));
+  int64_t lo = 0;
+  while (lo < nf && int64_t(h[lo]) == lo) ++lo;
+  const int64_t hi = n - (nf - lo);
+  bool ranged = true;
+  for (int64_t k = lo; k < nf && ranged; ++k) ranged = int64_t(h[k]) == hi + (k - lo);
+  if (ranged) {
+    e->interior_lo = lo;
+  } else {
+    e->interior_lo = -1;
+    SLBM_TRY(dalloc(e, &e->frame_bits, (n + 31) / 32));
+    k_frame_bits<<<grid_for(n, 256), 256, 0, s>>>(fr, n, e->frame_bits);
+    SLBM_CUDA_TRY(cudaGetLastError());
+  }
+  SLBM_CUDA_TRY(cudaStreamSynchronize(s));
   return SLBM_OK;
+}
+
+int set_frame(SlbmEngine* e, const int32_t* lo_w, const int32_t* hi_w) {
+  uint32_t* scratch = nullptr;
+  SLBM_CUDA_TRY(cudaMalloc(&scratch, size_t(std::max<int64_t>(e->n_fluid, 1)) * 4));
+  const int st = build_split(e, lo_w, hi_w, scratch);
+  cudaFree(scratch);
+  return st;
 }
 
 // the index list in the reference's layout (slot ids, contiguous rows)

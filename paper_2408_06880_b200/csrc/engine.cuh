@@ -125,6 +125,8 @@ int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
                 const int32_t* frame_width);
 int enumerate_fluid(SlbmEngine* e, const uint8_t* tags_pad);
 int export_idx_logical(SlbmEngine* e, uint32_t* host);
+int build_split(SlbmEngine* e, const int32_t* lo_w, const int32_t* hi_w, uint32_t* scratch);
+int set_frame(SlbmEngine* e, const int32_t* lo_w, const int32_t* hi_w);
 
 // dense.cu (direct-addressing engine)
 int build_dense(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,

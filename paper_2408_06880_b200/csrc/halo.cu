@@ -248,6 +248,8 @@ FlagPtrs flag_ptrs(SlbmHalo* h, const std::vector<int>& peers, bool remote, int 
   return f;
 }
 
+int nccl_start(SlbmHalo* h, PhaseProg& p, int phase, const PdfTable& t);
+
 int peer_start(SlbmHalo* h, PhaseProg& p, int phase) {
   const PdfTable t = h->table();
   cudaStream_t s = h->comm;
@@ -463,7 +465,20 @@ int slbm_halo_local(SlbmHalo* h, int phase) {
   return SLBM_OK;
 }
 
-int slbm_halo_start(SlbmHalo* h, int phase, void* after_stream) {
+int slbm_halo_local_on(SlbmHalo* h, int phase, void* stream) {
+  SLBM_TRY(check_phase(h, phase));
+  if (!h->committed) return fail(SLBM_ECONFIG, "halo not committed");
+  cudaSetDevice(h->device);
+  PhaseProg& p = h->ph[phase];
+  if (p.n_local) {
+    k_local<<<grid_for(p.n_local), 256, 0, (cudaStream_t)stream>>>(h->table(), p.d_lse, p.d_lss,
+                                                                    p.d_lde, p.d_lds, p.n_local);
+    SLBM_CUDA_TRY(cudaGetLastError());
+  }
+  return SLBM_OK;
+}
+
+int slbm_halo_start_ex(SlbmHalo* h, int phase, void* after_stream, int with_local) {
   SLBM_TRY(check_phase(h, phase));
   if (!h->committed) return fail(SLBM_ECONFIG, "halo not committed");
   cudaSetDevice(h->device);
@@ -473,7 +488,26 @@ int slbm_halo_start(SlbmHalo* h, int phase, void* after_stream) {
   }
   PhaseProg& p = h->ph[phase];
   const PdfTable t = h->table();
-  if (h->peer) return peer_start(h, p, phase);
+  const int64_t n_local = p.n_local;
+  if (!with_local) p.n_local = 0;  // local edges run elsewhere (slbm_halo_local_on)
+  int st;
+  if (h->peer) {
+    st = peer_start(h, p, phase);
+  } else {
+    st = nccl_start(h, p, phase, t);
+  }
+  p.n_local = n_local;
+  return st;
+}
+
+int slbm_halo_start(SlbmHalo* h, int phase, void* after_stream) {
+  return slbm_halo_start_ex(h, phase, after_stream, 1);
+}
+
+}  // extern "C"
+
+namespace {
+int nccl_start(SlbmHalo* h, PhaseProg& p, int phase, const PdfTable& t) {
   if (p.n_pack) {
     k_pack<<<grid_for(p.n_pack), 256, 0, h->comm>>>(t, p.d_pe, p.d_ps, p.n_pack, h->d_send);
     SLBM_CUDA_TRY(cudaGetLastError());
@@ -498,6 +532,9 @@ int slbm_halo_start(SlbmHalo* h, int phase, void* after_stream) {
   SLBM_CUDA_TRY(cudaEventRecord(h->ev_done, h->comm));
   return SLBM_OK;
 }
+}  // namespace
+
+extern "C" {
 
 int slbm_halo_wait(SlbmHalo* h, void* stream) {
   if (!h) return fail(SLBM_ECONFIG, "null halo");

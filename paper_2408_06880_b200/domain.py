@@ -269,9 +269,37 @@ class Domain:
                                             ba.engine, bb.engine, src_layout=ba.kind))
         self._comm = _comm
         self._halo = self._build_halo()
+        self._face_frames = self._narrow_frames() if engine_factory is None else False
         self._group = self._build_group() if engine_factory is None else None
         self.overlap_samples: list[tuple[float, float]] = []
         self.steps_done = 0
+
+    def _narrow_frames(self) -> bool:
+        """``frame_width="halo"`` with remote edges: frame only the faces that
+        have a neighbour on another rank (any stencil offset with that sign),
+        per face, on sparse blocks.  Local edges then run on the compute
+        stream before the interior sweep, so faces towards blocks of this
+        rank need no frame.  Returns whether the driver must do so."""
+        if not (isinstance(self.frame_width, str) and self.frame_width == "halo"):
+            return False
+        if not self._has_remote or not hasattr(self._halo, "local_on"):
+            return False
+        dim = self.stencil.dim
+        loopback = getattr(self, "_loopback", False)
+        for blk in self.local_blocks():
+            if getattr(blk.engine, "layout", "") != "sparse":
+                continue
+            lo, hi = [0] * dim, [0] * dim
+            for sigma, nbid in blk.neighbors.items():
+                if not loopback and self.blocks[nbid].rank == self.rank:
+                    continue
+                for a in range(dim):
+                    if sigma[a] < 0:
+                        lo[a] = 1
+                    elif sigma[a] > 0:
+                        hi[a] = 1
+            blk.engine.set_frame(lo, hi)
+        return True
 
     def _block_frame(self, frame_width):
         """``frame_width="halo"`` (extension): width 1 only on axes with more
@@ -433,7 +461,12 @@ class Domain:
         Counters still record the interior/frame split the reference's
         overlapped driver reports."""
         phase = phase_for(self.pattern, self.parity)
-        self._halo.start(phase, self._stream)
+        if self._face_frames:
+            # remote edges on the comm stream; local edges first on this one
+            self._halo.start(phase, self._stream, with_local=False)
+            self._halo.local_on(phase, self._stream)
+        else:
+            self._halo.start(phase, self._stream)
         self._count_exchange(phase)
         self._refresh_all()
         if not self._has_remote:
@@ -678,12 +711,16 @@ class HostStagedHalo:
     def commit(self, nccl_comm=None):
         self.inner.commit(None)
 
-    def start(self, phase, after_stream):
+    def local_on(self, phase, stream):
+        self.inner.local_on(phase, stream)
+
+    def start(self, phase, after_stream, with_local=True):
         import torch
         import torch.distributed as dist
 
         _abi_sync_stream(after_stream)
-        self.inner.local_only(phase)
+        if with_local:
+            self.inner.local_only(phase)
         sends, recvs = self.inner.peer_sizes(phase, self.world)
         reqs, bufs = [], {}
         for peer in range(self.world):

@@ -210,6 +210,21 @@ class SparseEngine:
         return {"ubb_slots": us, "ubb_partner": up, "ubb_corr": uc,
                 "ghost_q": gq, "ghost_pflat": gp, "ghost_slot": gs}
 
+    def set_frame(self, lo, hi) -> None:
+        """Per-face interior/frame split (extension; the reference's
+        frame_mask is lo == hi >= 1): frame cells lie within lo[a] of the low
+        face or hi[a] of the high face of axis a, 0 meaning none.  Used by
+        the domain drivers to frame only the faces with remote neighbours."""
+        dim = self.stencil.dim
+        lo32 = np.array(list(lo) + [0] * (3 - dim), dtype=np.int32)
+        hi32 = np.array(list(hi) + [0] * (3 - dim), dtype=np.int32)
+        _abi.call("slbm_engine_set_frame", self._h, _abi.ptr(lo32, C.c_int32),
+                  _abi.ptr(hi32, C.c_int32))
+        info = self.info()
+        self._n_interior = int(info.n_interior)
+        self._n_frame = int(info.n_frame)
+        self._has_split = True
+
     def split_lists(self) -> tuple[np.ndarray, np.ndarray]:
         """(interior cids, frame cids) (sparse.py:80-88)."""
         a = np.empty(self._n_interior, np.int64)

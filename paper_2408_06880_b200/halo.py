@@ -278,8 +278,13 @@ class DeviceHalo:
             _abi.call("slbm_halo_connect", self._h, r, C.cast(a, C.c_void_p),
                       C.cast(b, C.c_void_p), _abi.ptr(off, C.c_int64), _abi.ptr(cnt, C.c_int64))
 
-    def start(self, phase: Phase, after_stream: int | None):
-        _abi.call("slbm_halo_start", self._h, phase.value, C.c_void_p(after_stream or 0))
+    def start(self, phase: Phase, after_stream: int | None, with_local: bool = True):
+        _abi.call("slbm_halo_start_ex", self._h, phase.value, C.c_void_p(after_stream or 0),
+                  1 if with_local else 0)
+
+    def local_on(self, phase: Phase, stream: int | None):
+        """Only the device-local edges, on ``stream``."""
+        _abi.call("slbm_halo_local_on", self._h, phase.value, C.c_void_p(stream or 0))
 
     def wait(self, stream: int | None):
         _abi.call("slbm_halo_wait", self._h, C.c_void_p(stream or 0))

@@ -57,7 +57,7 @@ def test_peer_loopback_matches_golden(name, pattern, gpu_lib):
         np.testing.assert_array_equal(dom.gather_canonical(), rec[f"{pattern}_final"])
 
 
-def _worker(rank, world, port, path, pattern, out_dir, transport="host"):
+def _worker(rank, world, port, path, pattern, out_dir, transport="host", frame=1):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -67,8 +67,14 @@ def _worker(rank, world, port, path, pattern, out_dir, transport="host"):
 
     rec = load_golden(path)
     dom = DistributedDomain(flags_of(rec), tuple(int(b) for b in rec["block"]), stencil_of(rec),
-                            params_of(rec), pattern=pattern, frame_width=1, rank=rank, world=world,
-                            device=0, transport=transport)
+                            params_of(rec), pattern=pattern, frame_width=frame, rank=rank,
+                            world=world, device=0, transport=transport)
+    if frame == "halo":
+        # per-face frames: only faces towards the other rank's blocks
+        local = {b.bid for b in dom.local_blocks()}
+        assert dom._face_frames
+        assert any(dom.blocks[n].rank == rank for b in dom.local_blocks()
+                   for n in b.neighbors.values() if n not in (b.bid,)) or len(local) == 1
     dom.init_random(int(rec["seed"]))
     dom.run(int(rec["steps"]), driver="overlapped")
     full = dom.gather_canonical_global()
@@ -100,6 +106,22 @@ def test_two_ranks_peer_ipc_match_golden(name, pattern, tmp_path, gpu_lib):
     flags through CUDA IPC: the same code path as two GPUs over NVLink."""
     path = DOMAIN[name]
     mp.start_processes(_worker, args=(2, _free_port(), path, pattern, str(tmp_path), "p2p"),
+                       nprocs=2, join=True, start_method="spawn")
+    rec = load_golden(path)
+    np.testing.assert_array_equal(np.load(tmp_path / "full.npy"), rec[f"{pattern}_final"])
+
+
+@pytest.mark.parametrize("transport", ["host", "p2p"])
+@pytest.mark.parametrize("name,pattern", [("domain_d3q19_2x2x2", "aa"),
+                                          ("domain_d3q27_riverbed", "pull")])
+def test_two_ranks_face_frames_match_golden(name, pattern, transport, tmp_path, gpu_lib):
+    """frame_width="halo" with blocks of both ranks interleaved: frames only
+    on faces towards remote blocks, local edges ahead of the interior sweep
+    on the compute stream, remote ones overlapped — same bits as the
+    reference's single-process run."""
+    path = DOMAIN[name]
+    mp.start_processes(_worker, args=(2, _free_port(), path, pattern, str(tmp_path), transport,
+                                      "halo"),
                        nprocs=2, join=True, start_method="spawn")
     rec = load_golden(path)
     np.testing.assert_array_equal(np.load(tmp_path / "full.npy"), rec[f"{pattern}_final"])
