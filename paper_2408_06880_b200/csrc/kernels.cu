@@ -73,8 +73,9 @@ enum Kind { kPull = 0, kEven = 1, kOdd = 2 };
 // memory; persistent CTAs with a cp.async idx double buffer; a cell-major
 // idx copy; ld.global.nc / L1::no_allocate PDF gathers (-40%: the gathers
 // want L1 sector merging); st.global.cs stores (-4%); 5 or 6 CTAs/SM (94 /
-// 80 + spill registers: -1% / -10%); L1::no_allocate or L1::evict_first
-// gathers through inline PTX (-40%, like .nc); FMA contraction (no change under the
+// 80 + spill registers: -1% / -10%); __ldg gathers (same); L1::no_allocate,
+// L1::evict_first or __ldlu gathers (-40%: evicting the line the thread is
+// about to overwrite in place costs the store); FMA contraction (no change under the
 // power cap, which costs the sweep ~6% of SM clock) — all slower than the
 // plain gather.  What pays is the L2 prefetch of the index list one quarter
 // wave ahead (sweep.cuh): +7-9%.
