@@ -362,7 +362,7 @@ def impl_ours(args, rank, world, local_rank):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        edge, c_steps = 64, 10
+        edge, c_steps = 96, 40  # ~10 s of CPU work per worker
         procs = max(1, os.cpu_count() or 1)
         mfl, nf = run_cpu_reference_parallel(c_steps, 2, edge, procs)
         cpu = {"value": round(mfl, 4), "unit": "MFLUPS", "cores": procs, "kind": "port",
