@@ -68,6 +68,28 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def live_copy_gbs(torch, dev):
+    """This box's copy bandwidth, measured the way MEASURED_PEAKS.json's
+    hbm_gbs is (b.copy_(a) over 1 Gi bf16 elements, read + write bytes, best
+    of 10, CUDA events): boxes differ by a few percent, so the roofline line
+    carries both."""
+    a = torch.empty(1 << 30, dtype=torch.bfloat16, device=f"cuda:{dev}")
+    b = torch.empty_like(a)
+    best = float("inf")
+    for _ in range(10):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        b.copy_(a)
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    gbs = 2 * a.numel() * 2 / (best / 1e3) / 1e9
+    del a, b
+    torch.cuda.empty_cache()
+    return gbs
+
+
 # ---------------------------------------------------------------- clocks
 
 
@@ -355,6 +377,7 @@ def impl_ours(args, rank, world, local_rank):
     # unpack kernels and splits the sweep into interior + frame
     launches_per_step = 2 + (1 if eng.n_ubb_slots else 0) + (3 if world > 1 else 0)
     hbm, hbm_src = peaks()
+    live = live_copy_gbs(torch, dev)
     ach_even = eng.n_fluid * BYTES_EVEN / (t_even / 1e3) / 1e9
     ach_odd = eng.n_fluid * BYTES_ODD / (t_odd / 1e3) / 1e9
     pair = eng.n_fluid * (BYTES_EVEN + BYTES_ODD) / ((t_even + t_odd) / 1e3) / 1e9
@@ -415,6 +438,9 @@ def impl_ours(args, rank, world, local_rank):
                            "frac": round(ach_odd / hbm, 4), "bytes_per_cell": BYTES_ODD,
                            "ms_per_launch": round(t_odd, 4)},
             "pair_frac": round(pair / hbm, 4),
+            "peak_live_copy_gbs": round(live, 1),
+            "frac_vs_live_peak": round(ach_even / live, 4),
+            "pair_frac_vs_live_peak": round(pair / live, 4),
         },
         "clocks": csum,
         "gpu_launches": launches_per_step * steps,
