@@ -26,7 +26,7 @@ namespace {
 constexpr int kMaxLanes = 16;
 constexpr size_t kMinStaged = size_t(4) << 20;  // below this: plain copy
 size_t g_chunk = size_t(4) << 20;  // bytes per pinned chunk (tuning knob 10, MiB)
-int g_max_threads = 8;             // lanes used per transfer (tuning knob 11)
+int g_max_threads = 16;            // lanes used per transfer (tuning knob 11; capped by cores)
 
 struct Lane {
   int device = -1;
