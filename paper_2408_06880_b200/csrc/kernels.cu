@@ -75,7 +75,10 @@ enum Kind { kPull = 0, kEven = 1, kOdd = 2 };
 // want L1 sector merging); st.global.cs stores (-4%); 5 or 6 CTAs/SM (94 /
 // 80 + spill registers: -1% / -10%); __ldg gathers (same); L1::no_allocate,
 // L1::evict_first or __ldlu gathers (-40%: evicting the line the thread is
-// about to overwrite in place costs the store); FMA contraction (no change under the
+// about to overwrite in place costs the store); a compressed index list
+// (16-bit deltas against a per-32-cell base, escapes for folds/halo: 342
+// instead of 376 B/cell, -4% burst / -2.5% sustained: more load
+// instructions than bytes saved); FMA contraction (no change under the
 // power cap, which costs the sweep ~6% of SM clock) — all slower than the
 // plain gather.  What pays is the L2 prefetch of the index list one quarter
 // wave ahead (sweep.cuh): +7-9%.
