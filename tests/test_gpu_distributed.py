@@ -76,7 +76,13 @@ def _worker(rank, world, port, path, pattern, out_dir, transport="host", frame=1
         assert any(dom.blocks[n].rank == rank for b in dom.local_blocks()
                    for n in b.neighbors.values() if n not in (b.bid,)) or len(local) == 1
     dom.init_random(int(rec["seed"]))
-    dom.run(int(rec["steps"]), driver="overlapped")
+    steps = int(rec["steps"])
+    if transport == "p2p":
+        # device-side epochs: CUDA-graph replays across processes stay in step
+        dom.run(1, driver="overlapped")
+        dom.run(steps - 1, driver="overlapped", use_graph=True)
+    else:
+        dom.run(steps, driver="overlapped")
     full = dom.gather_canonical_global()
     if rank == 0:
         np.save(os.path.join(out_dir, "full.npy"), full)
