@@ -11,16 +11,19 @@ kept even).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 N > 1 (torchrun, one rank per GPU) is weak scaling: the global box is
-N x 512^3 cut into one 512^3 block per rank along x, halo exchange by NCCL
-send/recv overlapped with the interior sweep.
+512 x 512 x (N * 512) cut into one 512^3 slab per rank along z, halo
+exchange by NCCL send/recv (SLBM_TRANSPORT=p2p: stores into the peers'
+buffers through CUDA IPC; =host: host staging for ranks sharing a GPU)
+overlapped with the interior sweep.
 
 The JSON line carries: value (device-resident throughput, CUDA events,
 max over ranks), e2e (same metric through the public Python API with host
 buffers, H2D of the initial state + D2H of the macroscopic fields inside
 the timed region), roofline of the dominant kernel (index-list AA sweep)
-vs MEASURED_PEAKS.json, cpu_baseline (the oracle port, i.e. the reference
-algorithm in numpy, on a bounded sample), clocks sampled during the timed
-region, and gpu_launches.
+vs MEASURED_PEAKS.json (and this box's live copy bandwidth), cpu_baseline
+(the oracle port, i.e. the reference algorithm in numpy, one process per
+host core on bounded samples), clocks and board power sampled during the
+timed region, and gpu_launches.
 """
 
 from __future__ import annotations
