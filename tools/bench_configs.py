@@ -1,7 +1,7 @@
 """Measure BASELINE.json configs other than the headline (which bench.py owns)
 on one B200 and print one JSON line per measurement.
 
-    python tools/bench_configs.py [c1] [c3] [c4] [c5] [--steps K]
+    python tools/bench_configs.py [c1] [c3] [c3h] [c4] [c5] [--steps K]
 
 c1  D3Q19 SRT, 64^3 periodic channel, overlapping-sphere bed porosity ~0.5,
     100 steps, pull and AA: GPU MFLUPS, bitwise parity with the reference's
@@ -10,6 +10,8 @@ c1  D3Q19 SRT, 64^3 periodic channel, overlapping-sphere bed porosity ~0.5,
 c3  D3Q27 cumulant, 512^3 per GPU: particle bed (porosity ~0.35) in the lower
     half, free flow above, periodic x/y, no-slip floor, moving lid (N = 1
     here; the weak-scaling series runs through bench.py's DistributedDomain).
+c3h the paper's hybrid riverbed: the C3 riverbed (D3Q19 TRT) in 128^3 blocks
+    under the sparse, dense and hybrid layout policies (MFLUPS, memory).
 c4  vessel-like branching tube tree, ~5% fluid, 512^3 box cut into 128^3
     blocks (empty blocks dropped), D3Q19 TRT, UBB inlet + fixed-density
     outlets; Domain on one GPU with the whole step pair captured as one CUDA
@@ -136,6 +138,53 @@ def c3(steps):
         del eng
 
 
+def c3h(steps):
+    """The paper's hybrid riverbed on one GPU: the C3
+    riverbed (D3Q19 TRT here) cut into 128^3 blocks, run with the sparse,
+    dense and hybrid layout policies (hybrid: dense at block porosity >=
+    phi_s = 0.8, domain.py:58-65).  All three give the same bits."""
+    from paper_2408_06880_b200.domain import Domain
+
+    edge = 512
+    dims = (edge, edge, edge)
+    d = 16.0
+    half = (edge, edge, edge // 2)
+    n = geometry.overlapping_sphere_count(half, d, 0.35)
+    solid = geometry.voxelize_spheres(dims, geometry.sphere_centers(half, d, n, 3), d, 0)
+    lid = FaceSpec(FaceKind.WALL, velocity=(0.02, 0.0, 0.0))
+    fl = make_flags(dims, [(PERIODIC, PERIODIC), (PERIODIC, PERIODIC), (WALL, lid)], solid=solid)
+    st = make_stencil("d3q19")
+    p = CollisionParams(1.6, "trt", trt_magic_lambda(1.6))
+    sums = {}
+    for policy in ("sparse", "dense", "hybrid"):
+        dom = Domain(fl, 128, st, p, pattern="aa", policy=policy, frame_width=1, device=0,
+                     check="deferred")
+        dom.init_equilibrium()
+        dom.run(4, driver="overlapped", use_graph=True)
+        stream = torch.cuda.ExternalStream(dom.stream())
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(stream)
+        dom.run(steps, driver="overlapped", use_graph=True)
+        b.record(stream)
+        b.synchronize()
+        ms = a.elapsed_time(b)
+        dom.poll()
+        rho, _ = dom.gather_macroscopics()
+        sums[policy] = float(np.abs(rho).sum())
+        kinds = [blk.kind for blk in dom.blocks.values()]
+        nf = dom.total_fluid()
+        emit({"config": "c3h", "policy": policy, "n_fluid": nf, "blocks": len(kinds),
+              "dense_blocks": kinds.count("dense"), "steps": steps,
+              "mflups": round(nf * steps / ms * 1e3 / 1e6, 1),
+              "device_gb": round(sum(e.device_bytes for e in dom.local_engines()) / 1e9, 2),
+              "rho_abs_sum": sums[policy]})
+        del dom
+        torch.cuda.empty_cache()
+    assert len(set(sums.values())) == 1, sums
+
+
 def c4(steps):
     from paper_2408_06880_b200.domain import Domain
 
@@ -223,8 +272,8 @@ def main():
     which = args or ["c1", "c3", "c4", "c5"]
     torch.cuda.set_device(0)
     for w in which:
-        {"c1": lambda: c1(), "c3": lambda: c3(steps), "c4": lambda: c4(steps),
-         "c5": lambda: c5(steps)}[w]()
+        {"c1": lambda: c1(), "c3": lambda: c3(steps), "c3h": lambda: c3h(steps),
+         "c4": lambda: c4(steps), "c5": lambda: c5(steps)}[w]()
 
 
 if __name__ == "__main__":
