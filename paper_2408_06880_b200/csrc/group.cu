@@ -116,32 +116,16 @@ __global__ void __launch_bounds__(kGB, KIND == 2 ? 6 : 4) k_group(const GroupArg
   if (i >= n_cells) return;
   const uint32_t c = cids ? cids[i] : offset + i;
   if (c < a.lo || (a.skip && ((__ldg(a.skip + (c >> 5)) >> (c & 31)) & 1u))) return;
-  double t[L::Q];
-  double* pdf = a.pdf;
   bool bad;
-  if constexpr (KIND == 2) {  // AA odd (sparse.py:273-282)
-    sfor<0, L::Q>([&](auto q) {
-      constexpr int qb = L::INV[q];
-      t[q] = pdf[a.base[qb] + c];
-    });
-    bad = collide<L, MODEL>(t, omega, lam,
-                            [&](auto q, double v) { pdf[a.base[decltype(q)::value] + c] = v; });
+  if constexpr (KIND == 2) {
+    bad = cell_local<L, MODEL>(a.pdf, a.base, c, omega, lam);
   } else {
     uint32_t s[L::Q];
-    s[0] = c;
-    sfor<1, L::Q>([&](auto q) { s[q] = __ldcs(idx + size_t(q - 1) * pitch + c); });
-    sfor<0, L::Q>([&](auto q) { t[q] = pdf[s[q]]; });
+    double t[L::Q];
+    load_slots<L>(s, idx, pitch, c);
+    gather<L>(t, a.pdf, s);
     if (cids) prefetch_idx_ahead<L::Q - 1, kGB>(idx, pitch, cids, n_cells, pos0, ahead);
-    if constexpr (KIND == 1) {  // AA even (sparse.py:264-271)
-      bad = collide<L, MODEL>(t, omega, lam, [&](auto q, double v) {
-        constexpr int qb = L::INV[decltype(q)::value];
-        pdf[s[qb]] = v;
-      });
-    } else {  // pull (sparse.py:257-262)
-      double* dst = a.dst;
-      bad = collide<L, MODEL>(t, omega, lam,
-                              [&](auto q, double v) { dst[a.base[decltype(q)::value] + c] = v; });
-    }
+    bad = collide_scatter<L, MODEL, KIND == 1>(t, s, a.pdf, a.dst, a.base, c, omega, lam);
   }
   if (bad) atomicMin(a.bad, *a.step);
 }

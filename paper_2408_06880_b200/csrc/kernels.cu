@@ -96,31 +96,19 @@ __global__ void __launch_bounds__(kIB, MINB) k_index_sweep(const SweepArgs a, ui
   if (c < a.lo) return;
   uint32_t s[L::Q];
   double t[L::Q];
-  s[0] = c;
   // the skip word (interior sweep) is loaded alongside the index list, not
   // in front of it: a frame cell reads its idx row for nothing (~1% extra)
   // but no cell waits for the mask before its own loads start
   const uint32_t skip_word = a.skip ? __ldg(a.skip + (c >> 5)) : 0u;
-  sfor<1, L::Q>([&](auto q) { s[q] = __ldcs(a.idx + size_t(q - 1) * a.idx_pitch + c); });
+  load_slots<L>(s, a.idx, a.idx_pitch, c);
   if ((skip_word >> (c & 31)) & 1u) return;
-  sfor<0, L::Q>([&](auto q) { t[q] = a.pdf[s[q]]; });
+  gather<L>(t, a.pdf, s);
   if constexpr (PF) {
     if (a.cids != nullptr)
       prefetch_idx_ahead<L::Q - 1, kIB>(a.idx, a.idx_pitch, a.cids, a.n_cells, first, ahead);
   }
-  bool bad;
-  if constexpr (KIND == kEven) {
-    double* pdf = a.pdf;
-    bad = collide<L, MODEL>(t, a.omega, a.lam, [&](auto q, double v) {
-      constexpr int qb = L::INV[decltype(q)::value];
-      pdf[s[qb]] = v;
-    });
-  } else {
-    double* dst = a.dst;
-    bad = collide<L, MODEL>(t, a.omega, a.lam,
-                            [&](auto q, double v) { dst[a.base[decltype(q)::value] + c] = v; });
-  }
-  if (bad) flag_bad(a);
+  if (collide_scatter<L, MODEL, KIND == kEven>(t, s, a.pdf, a.dst, a.base, c, a.omega, a.lam))
+    flag_bad(a);
 }
 
 // Memory-pattern probe (tuning only; does NOT compute LBM): the even sweep's
@@ -147,16 +135,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_aa_odd(const SweepArgs a) {
   if (i >= a.n_cells) return;
   const uint32_t c = a.cids ? a.cids[i] : a.offset + i;
   if (c < a.lo || (a.skip && ((__ldg(a.skip + (c >> 5)) >> (c & 31)) & 1u))) return;
-  double t[L::Q];
-  sfor<0, L::Q>([&](auto q) {
-    constexpr int qb = L::INV[q];
-    t[q] = a.pdf[a.base[qb] + c];
-  });
-  double* pdf = a.pdf;
-  const bool bad = collide<L, MODEL>(t, a.omega, a.lam, [&](auto q, double v) {
-    pdf[a.base[decltype(q)::value] + c] = v;
-  });
-  if (bad) flag_bad(a);
+  if (cell_local<L, MODEL>(a.pdf, a.base, c, a.omega, a.lam)) flag_bad(a);
 }
 
 int num_sms() {

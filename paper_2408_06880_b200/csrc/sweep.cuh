@@ -38,6 +38,55 @@ __device__ __forceinline__ void prefetch_idx_ahead(const uint32_t* idx, uint32_t
   prefetch_l2(idx + size_t(row) * pitch + cell);
 }
 
+// ---- per-cell bodies shared by the single-engine sweeps (kernels.cu) and
+// the block-group sweeps (group.cu); `base` = the device group starts ----
+
+// the cell's Q-1 slot ids (s[0] = c is the rest direction's own slot)
+template <class L>
+__device__ __forceinline__ void load_slots(uint32_t (&s)[L::Q], const uint32_t* idx,
+                                           uint32_t pitch, uint32_t c) {
+  s[0] = c;
+  sfor<1, L::Q>([&](auto q) { s[q] = __ldcs(idx + size_t(q - 1) * pitch + c); });
+}
+
+template <class L>
+__device__ __forceinline__ void gather(double (&t)[L::Q], const double* pdf,
+                                       const uint32_t (&s)[L::Q]) {
+  sfor<0, L::Q>([&](auto q) { t[q] = pdf[s[q]]; });
+}
+
+// collide the gathered values; AA even (sparse.py:264-271): out[q] goes back
+// through the slot direction inv q was read from; pull (sparse.py:257-262):
+// out[q] to the cell's own group q of the other buffer.  True if unstable.
+template <class L, int MODEL, bool EVEN>
+__device__ __forceinline__ bool collide_scatter(const double (&t)[L::Q], const uint32_t (&s)[L::Q],
+                                                double* pdf, double* dst, const uint32_t* base,
+                                                uint32_t c, double omega, double lam) {
+  if constexpr (EVEN) {
+    return collide<L, MODEL>(t, omega, lam, [&](auto q, double v) {
+      constexpr int qb = L::INV[decltype(q)::value];
+      pdf[s[qb]] = v;
+    });
+  } else {
+    return collide<L, MODEL>(t, omega, lam,
+                             [&](auto q, double v) { dst[base[decltype(q)::value] + c] = v; });
+  }
+}
+
+// AA odd (cell-local reversed step, sparse.py:273-282): read the opposite
+// groups, write the own groups — every access a coalesced row
+template <class L, int MODEL>
+__device__ __forceinline__ bool cell_local(double* pdf, const uint32_t* base, uint32_t c,
+                                           double omega, double lam) {
+  double t[L::Q];
+  sfor<0, L::Q>([&](auto q) {
+    constexpr int qb = L::INV[q];
+    t[q] = pdf[base[qb] + c];
+  });
+  return collide<L, MODEL>(t, omega, lam,
+                           [&](auto q, double v) { pdf[base[decltype(q)::value] + c] = v; });
+}
+
 // Fixed-density outlet (extension; the reference has none).
 // Anti-bounce-back for a read of direction q from an OUTLET cell:
 //   f_q = 2 w_q rho_o (1 + 4.5 (c_q.u)^2 - 1.5 u.u) - f*_{inv q}
