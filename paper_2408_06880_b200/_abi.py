@@ -64,6 +64,7 @@ SIGNATURES = {
     "slbm_init_equilibrium": [vp, c_dp, C.c_int, c_dp, C.c_int],
     "slbm_canonical_state": [vp, c_dp],
     "slbm_macroscopic": [vp, c_dp, c_dp],
+    "slbm_macroscopic_compact": [vp, C.POINTER(C.c_double), C.POINTER(C.c_double)],
     "slbm_total_mass": [vp, c_dp],
     "slbm_refresh_boundary": [vp, C.c_int],
     "slbm_step": [vp, C.c_int],

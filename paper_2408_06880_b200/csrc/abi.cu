@@ -544,6 +544,30 @@ int slbm_macroscopic(SlbmEngine* e, double* rho, double* u) {
   return copy_d2h(u, d_u, cells * e->dim * sizeof(double), e->device, e->stream);
 }
 
+int slbm_macroscopic_compact(SlbmEngine* e, double* rho, double* u) {
+  CHECK_ENGINE(e);
+  if (!rho || !u) return fail(SLBM_ECONFIG, "null rho/u");
+  DeviceGuard guard(e->device);
+  const bool odd = e->pattern == SLBM_AA && e->parity == SLBM_ODD;
+  if (odd) SLBM_TRY(launch_refresh(e, SLBM_ODD));
+  const size_t n = size_t(e->n_fluid);
+  const size_t nq = e->layout ? size_t(e->q) * n : 0;
+  SLBM_TRY(e->ensure_scratch((n * (1 + e->dim) + nq) * sizeof(double)));
+  double* d_rho = e->d_scratch;
+  double* d_u = e->d_scratch + n;
+  int st;
+  if (e->layout) {
+    double* d_f = e->d_scratch + n * (1 + e->dim);
+    SLBM_TRY(dense_canonical(e, d_f));
+    st = launch_macroscopic(e, d_f, d_rho, d_u, true);
+  } else {
+    st = launch_macroscopic(e, nullptr, d_rho, d_u, true);
+  }
+  if (st != SLBM_OK) return st;
+  SLBM_TRY(copy_d2h(rho, d_rho, n * sizeof(double), e->device, e->stream));
+  return copy_d2h(u, d_u, n * e->dim * sizeof(double), e->device, e->stream);
+}
+
 int slbm_total_mass(SlbmEngine* e, double* mass) {
   CHECK_ENGINE(e);
   DeviceGuard guard(e->device);

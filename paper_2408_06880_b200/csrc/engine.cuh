@@ -97,7 +97,9 @@ int launch_step(SlbmEngine* e, int phase);
 int launch_refresh(SlbmEngine* e, int parity);
 int launch_advance(SlbmEngine* e);
 int launch_canonical(SlbmEngine* e, double* dev_out);  // (q, n) at current parity
-int launch_macroscopic(SlbmEngine* e, const double* dev_canon, double* dev_rho, double* dev_u);
+// box layout (zeros at solids must be pre-set) or compact: one value per fluid cell
+int launch_macroscopic(SlbmEngine* e, const double* dev_canon, double* dev_rho, double* dev_u,
+                       bool compact = false);
 int launch_gather(const double* src, const uint32_t* slots, int64_t n, double* out,
                   cudaStream_t s);
 int launch_scatter(double* dst, const uint32_t* slots, int64_t n, const double* in,

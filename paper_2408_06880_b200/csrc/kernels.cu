@@ -230,9 +230,12 @@ __global__ void k_macro(const double* pdf, SweepArgs a, int odd, Geometry g,
   });
   const Moments<L> m = moments<L>(t);
   if (m.bad) atomicOr(bad, 1);
-  int64_t x, y, z;
-  g.coords(x_flat[c], x, y, z);
-  const int64_t f = g.interior_flat(x, y, z);
+  int64_t f = c;  // compact output (one value per fluid cell) without x_flat
+  if (x_flat) {
+    int64_t x, y, z;
+    g.coords(x_flat[c], x, y, z);
+    f = g.interior_flat(x, y, z);
+  }
   rho_f[f] = m.rho;
   u_f[f * L::DIM + 0] = m.ux;
   u_f[f * L::DIM + 1] = m.uy;
@@ -402,7 +405,8 @@ int launch_advance(SlbmEngine* e) {
 
 // canonical: nullptr -> read the sparse groups of e->pdf at the current
 // parity; else a (q, n_fluid) canonical array (dense engine)
-int launch_macroscopic(SlbmEngine* e, const double* canonical, double* dev_rho, double* dev_u) {
+int launch_macroscopic(SlbmEngine* e, const double* canonical, double* dev_rho, double* dev_u,
+                       bool compact) {
   SweepArgs a = sweep_args(e);
   const double* src = e->pdf;
   int odd = (e->pattern == SLBM_AA && e->parity == SLBM_ODD) ? 1 : 0;
@@ -416,8 +420,8 @@ int launch_macroscopic(SlbmEngine* e, const double* canonical, double* dev_rho, 
   SLBM_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int), e->stream));
   by_lattice(e->q, [&](auto lat) {
     using L = decltype(lat);
-    k_macro<L><<<grid_for(e->n_fluid, 256), 256, 0, e->stream>>>(src, a, odd, e->geo,
-                                                                   e->x_flat, dev_rho, dev_u, bad);
+    k_macro<L><<<grid_for(e->n_fluid, 256), 256, 0, e->stream>>>(
+        src, a, odd, e->geo, compact ? nullptr : e->x_flat, dev_rho, dev_u, bad);
   });
   int h_bad = 0;
   SLBM_CUDA_TRY(cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, e->stream));

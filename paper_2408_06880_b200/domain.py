@@ -562,13 +562,26 @@ class Domain:
         return self.global_flags.tags_interior == FLUID
 
     def gather_macroscopics(self):
+        """domain.py:246-268: global (rho, u) with zeros at solids.  Sparse
+        blocks below porosity 0.5 move only their fluid cells' values
+        (slbm_macroscopic_compact) and scatter them here; denser ones move
+        their whole box."""
         shape = rev_shape(self.global_dims)
+        dim = self.stencil.dim
         rho = np.zeros(shape)
-        u = np.zeros(shape + (self.stencil.dim,))
+        u = np.zeros(shape + (dim,))
         for blk in self.local_blocks():
-            r, v = blk.engine.macroscopic_fields()
+            e = blk.engine
+            if getattr(e, "layout", "") == "sparse" and blk.porosity < 0.5 and hasattr(
+                    e, "macroscopic_compact"):
+                r, v = e.macroscopic_compact()
+                g = tuple(e.fluid_coords[:, a] + blk.origin[a] for a in reversed(range(dim)))
+                rho[g] = r
+                u[g] = v
+                continue
+            r, v = e.macroscopic_fields()
             sel = tuple(slice(blk.origin[a], blk.origin[a] + self.block_size[a])
-                        for a in reversed(range(self.stencil.dim)))
+                        for a in reversed(range(dim)))
             rho[sel] = r
             u[sel] = v
         return rho, u

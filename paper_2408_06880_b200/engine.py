@@ -384,6 +384,18 @@ class SparseEngine:
 
         return torch.as_tensor(_View(), device=f"cuda:{self.device}")
 
+    def macroscopic_compact(self) -> tuple[np.ndarray, np.ndarray]:
+        """(rho, u) per fluid cell in cid order, shapes (n_fluid,) and
+        (n_fluid, dim): the values macroscopic_fields scatters into the box
+        (pair with ``fluid_coords``)."""
+        if self.check == "deferred":
+            self.poll()
+        rho = np.empty(self.n_fluid, dtype=np.float64)
+        u = np.empty((self.n_fluid, self.stencil.dim), dtype=np.float64)
+        _abi.call("slbm_macroscopic_compact", self._h, _abi.ptr(rho, C.c_double),
+                  _abi.ptr(u, C.c_double))
+        return rho, u
+
     def total_mass(self) -> float:
         m = C.c_double()
         _abi.call("slbm_total_mass", self._h, C.byref(m))
