@@ -82,26 +82,41 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
-// every flag in `f` reaches epoch + delta; a peer that never arrives is a
-// fatal error (trap after 30 s) rather than a hung device
-__global__ void k_wait_flags(FlagPtrs f, const uint64_t* epoch, int64_t delta) {
-  if (int(threadIdx.x) >= f.n) return;
-  const uint64_t want = uint64_t(int64_t(*epoch) + delta);
+// a peer that never arrives is a fatal error (trap after 30 s), not a hang
+__device__ __forceinline__ void spin_until(const uint64_t* flag, uint64_t want) {
   const uint64_t t0 = globaltimer();
-  while (ld_acquire_sys(f.p[threadIdx.x]) < want) {
-    __nanosleep(200);
+  while (ld_acquire_sys(flag) < want) {
+    __nanosleep(100);
     if (globaltimer() - t0 > 30ull * 1000000000ull) __trap();
   }
 }
 
-// publish the epoch to every flag in `f` after this stream's earlier writes
-__global__ void k_signal_flags(FlagPtrs f, const uint64_t* epoch) {
-  if (int(threadIdx.x) >= f.n) return;
-  __threadfence_system();
-  st_release_sys(f.p[threadIdx.x], *epoch);
-}
-
 __global__ void k_epoch_advance(uint64_t* epoch) { *epoch += 1; }
+
+// Peer unpack: every CTA waits (one thread) for all senders' epoch flags,
+// scatters its entries; the CTA that finishes last acknowledges to every
+// sender (they may overwrite this buffer again) and advances the epoch.
+__global__ void k_unpack_ack(PdfTable t, const uint64_t* pos, const uint16_t* e,
+                             const uint32_t* s, int64_t n, const double* buf, FlagPtrs data,
+                             FlagPtrs acks, unsigned int* done, uint64_t* epoch) {
+  const uint64_t ep = *epoch;
+  if (threadIdx.x == 0)
+    for (int k = 0; k < data.n; ++k) spin_until(data.p[k], ep);
+  __syncthreads();
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) t.p[e[i]][s[i]] = buf[pos[i]];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned int prev = atomicAdd(done, 1u);
+    if (prev == gridDim.x - 1) {
+      __threadfence_system();
+      for (int k = 0; k < acks.n; ++k) st_release_sys(acks.p[k], ep);
+      *done = 0;
+      *epoch = ep + 1;
+    }
+  }
+}
 
 // Peer pack: gather this rank's entries for one peer and store them straight
 // into the peer's receive buffer over NVLink; the CTA that finishes last
@@ -109,9 +124,13 @@ __global__ void k_epoch_advance(uint64_t* epoch) { *epoch += 1; }
 // stores at system scope before it counts itself done, so the release store
 // of the last one orders all of them (the "last block" pattern; no reliance
 // on kernel-boundary visibility of peer writes).
+// Every CTA first waits (one thread) until the peer acknowledged the
+// previous exchange through this buffer (`ack` >= epoch - 1).
 __global__ void k_pack_signal(PdfTable t, const uint16_t* e, const uint32_t* s, int64_t n,
                               double* remote, unsigned int* done, uint64_t* remote_flag,
-                              const uint64_t* epoch) {
+                              const uint64_t* ack, const uint64_t* epoch) {
+  if (threadIdx.x == 0) spin_until(ack, *epoch - 1);
+  __syncthreads();
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) remote[i] = t.p[e[i]][s[i]];
   __threadfence_system();
@@ -254,29 +273,25 @@ int peer_start(SlbmHalo* h, PhaseProg& p, int phase) {
   const PdfTable t = h->table();
   cudaStream_t s = h->comm;
   if (!p.send_peer.empty()) {
-    // the receivers have consumed the previous message in their buffers
-    k_wait_flags<<<1, kMaxPeers, 0, s>>>(flag_ptrs(h, p.send_peer, false, kMaxPeers), h->d_epoch,
-                                         -1);
-    const FlagPtrs data = flag_ptrs(h, p.send_peer, true, 0);
+    const FlagPtrs data = flag_ptrs(h, p.send_peer, true, 0);      // peers' words for us
+    const FlagPtrs acks = flag_ptrs(h, p.send_peer, false, kMaxPeers);  // their acks to us
     for (size_t i = 0; i < p.send_peer.size(); ++i) {
       if (!p.remote_dst[i]) return fail(SLBM_ECONFIG, "peer transport: halo not connected");
       k_pack_signal<<<grid_for(p.send_cnt[i]), 256, 0, s>>>(
           t, p.d_pe + p.send_off[i], p.d_ps + p.send_off[i], p.send_cnt[i], p.remote_dst[i],
-          h->d_done + phase * kMaxPeers + i, data.p[i], h->d_epoch);
+          h->d_done + phase * kMaxPeers + i, data.p[i], acks.p[i], h->d_epoch);
     }
     SLBM_CUDA_TRY(cudaGetLastError());
   }
   SLBM_TRY(slbm_halo_local(h, phase));
   if (!p.recv_peer.empty()) {
-    k_wait_flags<<<1, kMaxPeers, 0, s>>>(flag_ptrs(h, p.recv_peer, false, 0), h->d_epoch, 0);
-    if (p.n_unpack)
-      k_unpack<<<grid_for(p.n_unpack), 256, 0, s>>>(t, p.d_upos, p.d_ue, p.d_us, p.n_unpack,
-                                                     h->d_recv);
-    k_signal_flags<<<1, kMaxPeers, 0, s>>>(flag_ptrs(h, p.recv_peer, true, kMaxPeers),
-                                           h->d_epoch);
-    SLBM_CUDA_TRY(cudaGetLastError());
+    k_unpack_ack<<<grid_for(p.n_unpack), 256, 0, s>>>(
+        t, p.d_upos, p.d_ue, p.d_us, p.n_unpack, h->d_recv, flag_ptrs(h, p.recv_peer, false, 0),
+        flag_ptrs(h, p.recv_peer, true, kMaxPeers), h->d_done + 2 * kMaxPeers + phase,
+        h->d_epoch);
+  } else {
+    k_epoch_advance<<<1, 1, 0, s>>>(h->d_epoch);
   }
-  k_epoch_advance<<<1, 1, 0, s>>>(h->d_epoch);
   SLBM_CUDA_TRY(cudaGetLastError());
   SLBM_CUDA_TRY(cudaEventRecord(h->ev_done, s));
   return SLBM_OK;
@@ -442,8 +457,8 @@ int slbm_halo_commit(SlbmHalo* h, void* nccl_comm) {
     SLBM_CUDA_TRY(cudaMalloc(&h->d_flags, 2 * kMaxPeers * sizeof(uint64_t)));
     SLBM_CUDA_TRY(cudaMemset(h->d_flags, 0, 2 * kMaxPeers * sizeof(uint64_t)));
     SLBM_CUDA_TRY(cudaMalloc(&h->d_epoch, sizeof(uint64_t)));
-    SLBM_CUDA_TRY(cudaMalloc(&h->d_done, 2 * kMaxPeers * sizeof(unsigned int)));
-    SLBM_CUDA_TRY(cudaMemset(h->d_done, 0, 2 * kMaxPeers * sizeof(unsigned int)));
+    SLBM_CUDA_TRY(cudaMalloc(&h->d_done, (2 * kMaxPeers + 2) * sizeof(unsigned int)));
+    SLBM_CUDA_TRY(cudaMemset(h->d_done, 0, (2 * kMaxPeers + 2) * sizeof(unsigned int)));
     const uint64_t one = 1;
     SLBM_CUDA_TRY(cudaMemcpy(h->d_epoch, &one, sizeof(one), cudaMemcpyHostToDevice));
     for (auto& p : h->ph) p.remote_dst.assign(p.send_peer.size(), nullptr);
