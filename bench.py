@@ -536,6 +536,118 @@ def load_traffic():
         return None
 
 
+def _riverbed_c3(dims, device):
+    """configs[2]'s geometry: overlapping-sphere bed (porosity ~0.35, d = 16)
+    in the lower half, free flow above, periodic x / y, no-slip floor,
+    moving lid u = (0.02, 0, 0)."""
+    from paper_2408_06880_b200 import geometry
+    from paper_2408_06880_b200.tags import PERIODIC, WALL, FaceKind, FaceSpec, make_flags
+
+    half = (dims[0], dims[1], dims[2] // 2)
+    n = geometry.overlapping_sphere_count(half, 16.0, 0.35)
+    solid = geometry.voxelize_spheres(dims, geometry.sphere_centers(half, 16.0, n, 3), 16.0, device)
+    lid = FaceSpec(FaceKind.WALL, velocity=(0.02, 0.0, 0.0))
+    return make_flags(dims, [(PERIODIC, PERIODIC), (PERIODIC, PERIODIC), (WALL, lid)], solid=solid)
+
+
+def impl_riverbed(args, rank, world, local_rank):
+    """``--workload c3`` (BASELINE configs[2]): D3Q27 cumulant, 512^3 cells per
+    GPU, WEAK scaling with the blocks tiling x / y — grid (1,1,1), (2,1,1),
+    (2,2,1), (4,2,1) for 1 / 2 / 4 / 8 GPUs — so every GPU holds the same
+    bed + free-flow column; halo frames on the x / y faces only, exchange
+    overlapped with the interior sweep, one CUDA graph per step pair."""
+    import torch
+
+    from paper_2408_06880_b200.collision import CollisionParams
+    from paper_2408_06880_b200.domain import DistributedDomain
+    from paper_2408_06880_b200.engine import SparseEngine
+    from paper_2408_06880_b200.lattice import make_stencil
+
+    grids = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (4, 2, 1)}
+    grid = grids.get(world, (world, 1, 1))
+    dev = int(os.environ.get("SLBM_DEVICE", local_rank))
+    torch.cuda.set_device(dev)
+    steps = args.steps + (args.steps % 2)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+    def reduce(x, op="max"):
+        if dist is None:
+            return x
+        t = torch.tensor([float(x)], dtype=torch.float64,
+                         device=f"cuda:{dev}" if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+        return float(t.item())
+
+    st = make_stencil("d3q27")
+    p = CollisionParams(1.6, "cumulant")
+    t0 = time.perf_counter()
+    fl = _riverbed_c3((EDGE * grid[0], EDGE * grid[1], EDGE * grid[2]), dev)
+    if world == 1:
+        runner = SparseEngine(fl, st, p, "aa", device=dev, check="deferred")
+        engines = [runner]
+        run = lambda n: runner.run(n)  # noqa: E731
+    else:
+        assignment = {i: i for i in range(world)}
+        runner = DistributedDomain(fl, (EDGE, EDGE, EDGE), st, p, pattern="aa", rank=rank,
+                                   world=world, device=dev, assignment=assignment,
+                                   transport=os.environ.get("SLBM_TRANSPORT", "nccl"))
+        engines = runner.local_engines()
+        run = lambda n: runner.run(n, driver="overlapped", use_graph=True)  # noqa: E731
+    build_s = reduce(time.perf_counter() - t0)
+    runner.init_equilibrium(1.0, np.array([0.0, 0.0, 0.0]))
+    run(args.warmup + (args.warmup % 2))
+    runner.synchronize()
+    stream = torch.cuda.ExternalStream(engines[0].stream())
+    clocks = ClockSampler(dev)
+    clocks.start()
+    time.sleep(0.3)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.mark("t0")
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    run(steps)
+    e1.record(stream)
+    e1.synchronize()
+    clocks.mark("t1")
+    ms = reduce(e0.elapsed_time(e1))
+    runner.poll()
+    clocks.stop()
+    local = sum(e.n_fluid for e in engines)
+    total = int(reduce(local, "sum"))
+    value = total * steps / (ms / 1e3) / 1e6
+    te, to = time_kernels(engines[0], torch)
+    be, bo = 2 * 27 * 8 + 26 * 4, 2 * 27 * 8
+    n0 = engines[0].n_fluid
+    hbm, hbm_src = peaks()
+    if rank != 0:
+        return
+    print(json.dumps({
+        "metric": METRIC, "value": round(value, 2), "unit": "MFLUPS", "n_gpus": world,
+        "steps": steps, "warmup": args.warmup, "ms_per_step": round(ms / steps, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": "D3Q27 cumulant AA sparse, 512^3 per GPU: overlapping-sphere bed "
+                               "(porosity 0.35) in the lower half, free flow above, periodic x/y, "
+                               "no-slip floor, moving lid (configs[2])",
+                   "grid": list(grid), "n_fluid_per_gpu": local, "build_s": round(build_s, 2),
+                   "l2": "inputs larger than L2 (~30 GB per GPU)"},
+        "roofline": {"bound": "hbm", "kernel": "k_index_sweep<D3Q27,cumulant,even>",
+                     "achieved": round(n0 * be / te / 1e6, 1), "peak": hbm, "unit": "GB/s",
+                     "frac": round(n0 * be / te / 1e6 / hbm, 4), "traffic": None,
+                     "bytes_per_cell": be, "peak_source": hbm_src,
+                     "odd_kernel": {"kernel": "k_aa_odd<D3Q27,cumulant>",
+                                    "frac": round(n0 * bo / to / 1e6 / hbm, 4)},
+                     "pair_frac": round(n0 * (be + bo) / (te + to) / 1e6 / hbm, 4)},
+        "clocks": clocks.summary(),
+        "gpu_launches": None,
+    }), flush=True)
+
+
 def impl_artery(args, rank, world, local_rank):
     """``--workload c4`` (BASELINE configs[3]): STRONG scaling on the vessel-
     like branching tube (~5 % fluid) in a 512^3 box cut into 128^3 blocks
@@ -653,8 +765,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--workload", default="c2", choices=["c2", "c4"],
-                    help="c2: the headline weak-scaling bed (default); c4: strong-scaling artery")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4"],
+                    help="c2: the headline weak-scaling bed (default); c3: D3Q27 cumulant "
+                         "riverbed, weak scaling; c4: strong-scaling artery")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -677,6 +790,8 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
     if args.workload == "c4":
         impl_artery(args, rank, world, local_rank)
+    elif args.workload == "c3":
+        impl_riverbed(args, rank, world, local_rank)
     else:
         impl_ours(args, rank, world, local_rank)
     if world > 1:

@@ -107,8 +107,7 @@ def slice_block(gf: FlagField, origin, size, block_periodic) -> FlagField:
     nd = len(size)
     sel = tuple(slice(origin[a], origin[a] + size[a] + 2) for a in reversed(range(nd)))
     tags = gf.tags[sel].copy()
-    ubb = gf.ubb_u[sel]
-    ubb = ubb.copy() if ubb.flags.writeable else ubb
+    ubb = gf.ubb_u[sel]  # a view: blocks never modify it, engines copy what they upload
     # halo fluid -> EXCHANGE on axes that leave the block (domain.py:390-404)
     ring = np.zeros(tags.shape, dtype=bool)
     for arr_axis in range(nd):

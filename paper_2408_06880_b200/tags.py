@@ -122,6 +122,81 @@ class FlagField:
         return self.ubb_u[self._padded_index(coord)]
 
 
+# boxes at least this large (padded cells) with moving walls / outlets keep
+# ubb_u as a RingField instead of a dense float64 array (24 B per cell)
+RING_MIN_CELLS = 1 << 27
+
+
+class RingField:
+    """``ubb_u`` of :func:`make_flags` without the dense (Z+2)(Y+2)(X+2) x dim
+    float64 array.
+
+    make_flags paints wall values face by face (flags.py:196-249), so a
+    cell's value depends only on which side of each axis it sits on — low
+    ring, interior or high ring — and on whether its final tag is UBB /
+    OUTLET (everything else is zeroed).  The 3^dim side classes are painted
+    once on a 1-cell box with the same faces (the same code path), and any
+    window of the field is materialised on demand from that table and the
+    tags.  Slicing with slices keeps a lazy window (block slices of a
+    partition), ``np.asarray`` materialises.  Read-only."""
+
+    def __init__(self, tags, table, origin=None, window=None):
+        self._tags = tags
+        self._table = table  # (3,) * nd + (nd,)
+        nd = tags.ndim
+        self._origin = tuple(origin) if origin is not None else (0,) * nd
+        self._window = tuple(window) if window is not None else tuple(tags.shape)
+        self.dtype = np.dtype(np.float64)
+        self.shape = self._window + (nd,)
+        self.ndim = len(self.shape)
+        self.flags = type("Flags", (), {"writeable": False})()
+
+    @property
+    def nbytes(self) -> int:
+        return int(np.prod(self.shape)) * 8
+
+    def __array__(self, dtype=None, copy=None):
+        tags = self._tags
+        nd = tags.ndim
+        sel = tuple(slice(o, o + w) for o, w in zip(self._origin, self._window))
+        cls = np.zeros(self._window, dtype=np.int64)
+        for a in range(nd):
+            n_pad = tags.shape[a]
+            c = np.arange(self._origin[a], self._origin[a] + self._window[a])
+            side = np.where(c == 0, 0, np.where(c == n_pad - 1, 2, 1))
+            shape = [1] * nd
+            shape[a] = self._window[a]
+            cls = cls * 3 + side.reshape(shape)
+        out = self._table.reshape(-1, nd)[cls]
+        t = tags[sel]
+        out[(t != UBB) & (t != OUTLET)] = 0.0
+        return out if dtype is None else out.astype(dtype)
+
+    def __getitem__(self, key):
+        nd = self._tags.ndim
+        if not isinstance(key, tuple):
+            key = (key,)
+        simple = all(isinstance(k, (int, np.integer)) or (isinstance(k, slice) and k.step in (None, 1))
+                     for k in key)
+        if len(key) <= nd and simple:
+            origin, window = list(self._origin), list(self._window)
+            for a, k in enumerate(key):
+                if isinstance(k, slice):
+                    lo, hi, _ = k.indices(self._window[a])
+                else:
+                    lo = int(k) + (self._window[a] if k < 0 else 0)
+                    hi = lo + 1
+                origin[a] = self._origin[a] + lo
+                window[a] = max(hi - lo, 0)
+            view = RingField(self._tags, self._table, origin, window)
+            if all(isinstance(k, slice) for k in key):
+                return view  # lazy window
+            # integer axes: materialise only the small window, then drop them
+            return np.asarray(view)[tuple(0 if not isinstance(k, slice) else slice(None)
+                                          for k in key)]
+        return np.asarray(self)[key]
+
+
 def _wall_tag(spec: FaceSpec) -> int:
     if spec.density is not None:
         return OUTLET
@@ -164,9 +239,11 @@ def _check_faces(dims, faces):
             )
 
 
-def make_flags(dims, faces, solid: np.ndarray | None = None) -> FlagField:
+def make_flags(dims, faces, solid: np.ndarray | None = None, ring: bool | None = None) -> FlagField:
     """Padded tag box for a domain with the given per-axis face pairs
-    (``flags.py:196-249``)."""
+    (``flags.py:196-249``).  ``ring`` (default: for boxes of at least
+    RING_MIN_CELLS padded cells) keeps a moving-wall ``ubb_u`` as a
+    :class:`RingField` instead of a dense array."""
     dims = tuple(int(d) for d in dims)
     nd = len(dims)
     if nd not in (2, 3):
@@ -181,7 +258,14 @@ def make_flags(dims, faces, solid: np.ndarray | None = None) -> FlagField:
     padded = tuple(n + 2 for n in shape)
     tags = np.zeros(padded, dtype=np.uint8)
     moving = any(_wall_tag(s) in (UBB, OUTLET) for pair in faces for s in pair)
-    if moving:
+    if ring is None:
+        ring = moving and int(np.prod(padded, dtype=np.int64)) >= RING_MIN_CELLS
+    if moving and ring:
+        # side-class table: the same painting on a 1-cell box, unmasked
+        cls_vel = _paint_unmasked(faces, nd)
+        moving = False  # tags only below; values come from the table
+        vel = None
+    elif moving:
         vel = np.zeros(padded + (nd,), dtype=np.float64)
     else:
         # no moving wall: a read-only zero view instead of 24 B/cell of zeros
@@ -223,5 +307,31 @@ def make_flags(dims, faces, solid: np.ndarray | None = None) -> FlagField:
         hi_idx[arr_axis] = n + 2
     if moving:
         vel[(tags != UBB) & (tags != OUTLET)] = 0.0
+    if vel is None:
+        vel = RingField(tags, cls_vel)
     periodic = tuple(faces[a][0].kind is FaceKind.PERIODIC for a in range(nd))
     return FlagField(dims=dims, tags=tags, ubb_u=vel, periodic=periodic)
+
+
+def _paint_unmasked(faces, nd):
+    """make_flags' value painting on a 1-cell box without the final masking:
+    the value each side class (low ring / interior / high ring per axis)
+    receives, whatever tag the real box ends up with there."""
+    vel = np.zeros((3,) * nd + (nd,), dtype=np.float64)
+    lo_idx, hi_idx = [1] * nd, [2] * nd
+    for arr_axis in range(nd):
+        lo, hi = faces[nd - 1 - arr_axis]
+        region = [slice(lo_idx[a], hi_idx[a]) for a in range(nd)]
+        dst_lo, dst_hi = list(region), list(region)
+        dst_lo[arr_axis] = slice(0, 1)
+        dst_hi[arr_axis] = slice(2, 3)
+        if lo.kind is FaceKind.PERIODIC:
+            src = list(region)
+            src[arr_axis] = slice(1, 2)
+            vel[tuple(dst_lo)] = vel[tuple(src)]
+            vel[tuple(dst_hi)] = vel[tuple(src)]
+        else:
+            vel[tuple(dst_lo)] = _face_value(lo, nd)
+            vel[tuple(dst_hi)] = _face_value(hi, nd)
+        lo_idx[arr_axis], hi_idx[arr_axis] = 0, 3
+    return vel

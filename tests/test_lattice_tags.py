@@ -160,3 +160,46 @@ def test_voxel_mask_roundtrip(tmp_path):
     p.write_bytes(b"NOTAMASK" + bytes(12))
     with pytest.raises(errors.FormatError):
         geometry.read_voxel_mask(p)
+
+
+def test_ring_field_equals_dense_painting():
+    """make_flags(ring=True) keeps moving-wall values as a RingField
+    (side-class table + tags); every window materialises to exactly the
+    dense array make_flags paints, for every face combination drawn."""
+    import numpy as np
+
+    from paper_2408_06880_b200.tags import FaceKind, FaceSpec, RingField, make_flags
+
+    rng = np.random.default_rng(3)
+    for trial in range(60):
+        nd = 2 + trial % 2
+        dims = tuple(int(v) for v in rng.integers(1, 7, size=nd))
+        faces = []
+        for a in range(nd):
+            if rng.random() < 0.3:
+                faces.append((FaceSpec(FaceKind.PERIODIC), FaceSpec(FaceKind.PERIODIC)))
+                continue
+            pair = []
+            for _ in range(2):
+                k = rng.integers(0, 3)
+                if k == 0:
+                    pair.append(FaceSpec(FaceKind.WALL))
+                elif k == 1:
+                    pair.append(FaceSpec(FaceKind.WALL,
+                                         velocity=tuple(float(v) for v in rng.normal(size=nd))))
+                else:
+                    pair.append(FaceSpec(FaceKind.WALL, density=float(rng.uniform(0.9, 1.1))))
+            faces.append(tuple(pair))
+        solid = rng.random(tuple(reversed(dims))) < 0.3
+        dense = make_flags(dims, faces, solid=solid, ring=False)
+        lazy = make_flags(dims, faces, solid=solid, ring=True)
+        assert np.array_equal(dense.tags, lazy.tags)
+        if not isinstance(lazy.ubb_u, RingField):
+            continue  # no moving wall: both keep the zero view
+        assert lazy.ubb_u.shape == dense.ubb_u.shape
+        assert np.array_equal(np.asarray(lazy.ubb_u), dense.ubb_u)
+        # a lazy window (a block slice) equals the dense slice
+        sel = tuple(slice(int(rng.integers(0, s)), None) for s in dense.tags.shape)
+        assert np.array_equal(np.asarray(lazy.ubb_u[sel]), dense.ubb_u[sel])
+        c = tuple(int(rng.integers(0, d)) for d in dims)
+        assert np.array_equal(lazy.ubb_at(c), dense.ubb_at(c))
