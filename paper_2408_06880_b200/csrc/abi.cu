@@ -525,6 +525,13 @@ int slbm_macroscopic(SlbmEngine* e, double* rho, double* u) {
   const bool odd = e->pattern == SLBM_AA && e->parity == SLBM_ODD;
   if (odd) SLBM_TRY(launch_refresh(e, SLBM_ODD));
   const int64_t cells = e->geo.n_cells();
+  if (!e->layout) {
+    // pinned destinations: the kernel writes the fields straight into them
+    // over PCIe (no device staging buffer, no separate DMA)
+    void* drho = mapped_device_ptr(rho);
+    void* du = mapped_device_ptr(u);
+    if (drho && du) return launch_macroscopic_box(e, (double*)drho, (double*)du);
+  }
   const size_t nq = e->layout ? size_t(e->q) * e->n_fluid : 0;
   SLBM_TRY(e->ensure_scratch((size_t(cells) * (1 + e->dim) + nq) * sizeof(double)));
   double* d_rho = e->d_scratch;

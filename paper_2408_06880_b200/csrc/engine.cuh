@@ -120,6 +120,10 @@ int set_tuning(int knob, int value);
 int copy_d2h(void* host, const void* dev, size_t bytes, int device, cudaStream_t s);
 int copy_h2d(void* dev, const void* host, size_t bytes, int device, cudaStream_t s);
 int hostcopy_reserve(int device);
+void* mapped_device_ptr(void* host);  // pinned host buffer -> device address, else nullptr
+// macroscopic fields of every box cell written straight into (mapped) host
+// memory: zeros at solids, no device staging
+int launch_macroscopic_box(SlbmEngine* e, double* rho, double* u);
 int hostcopy_tune(int knob, int value);  // 10: chunk MiB, 11: max threads
 
 // builder.cu

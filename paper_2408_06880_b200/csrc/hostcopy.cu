@@ -177,6 +177,18 @@ int hostcopy_tune(int knob, int value) {
   return SLBM_OK;
 }
 
+// device-visible address of a pinned (page-locked, mapped) host buffer, or
+// nullptr for pageable memory
+void* mapped_device_ptr(void* host) {
+  if (!is_pinned(host)) return nullptr;
+  void* d = nullptr;
+  if (cudaHostGetDevicePointer(&d, host, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return d;
+}
+
 int copy_d2h(void* host, const void* dev, size_t bytes, int device, cudaStream_t s) {
   if (!bytes) return SLBM_OK;
   if (bytes < kMinStaged || is_pinned(host)) {

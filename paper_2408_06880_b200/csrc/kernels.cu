@@ -242,6 +242,49 @@ __global__ void k_macro(const double* pdf, SweepArgs a, int odd, Geometry g,
   if constexpr (L::DIM == 3) u_f[f * L::DIM + 2] = m.uz;
 }
 
+// One thread per box cell (x fastest); cells that are not fluid (cid_map <
+// 0) get zeros (sparse.py:323-331).  The interleaved u is transposed
+// through shared memory so every warp store is one contiguous 256-B run of
+// host memory — PCIe writes from SMs only stream at full width when
+// coalesced.
+constexpr int kMacroBlock = 256;
+
+template <class L>
+__global__ void __launch_bounds__(kMacroBlock) k_macro_box(const double* pdf, SweepArgs a, int odd,
+                                                           Geometry g, const int32_t* cid_map,
+                                                           double* rho_h, double* u_h, int* bad) {
+  __shared__ double su[kMacroBlock * L::DIM];
+  const int64_t cells = g.n_cells();
+  const int64_t f0 = int64_t(blockIdx.x) * kMacroBlock;
+  const int64_t f = f0 + threadIdx.x;
+  double rho = 0.0, uv[3] = {0.0, 0.0, 0.0};
+  if (f < cells) {
+    const int64_t x = f % g.n[0];
+    const int64_t r = f / g.n[0];
+    const int64_t y = r % g.n[1];
+    const int64_t z = r / g.n[1];
+    const int32_t c = cid_map[g.padded_flat(x, y, z)];
+    if (c >= 0) {
+      double t[L::Q];
+      sfor<0, L::Q>([&](auto q) {
+        constexpr int qb = L::INV[q];
+        t[q] = pdf[a.base[odd ? qb : int(q)] + uint32_t(c)];
+      });
+      const Moments<L> m = moments<L>(t);
+      if (m.bad) atomicOr(bad, 1);
+      rho = m.rho;
+      uv[0] = m.ux;
+      uv[1] = m.uy;
+      uv[2] = m.uz;
+    }
+    rho_h[f] = rho;
+  }
+  for (int k = 0; k < L::DIM; ++k) su[threadIdx.x * L::DIM + k] = uv[k];
+  __syncthreads();
+  const int64_t n_here = std::min<int64_t>(kMacroBlock, cells - f0) * L::DIM;
+  for (int k = threadIdx.x; k < n_here; k += kMacroBlock) u_h[f0 * L::DIM + k] = su[k];
+}
+
 template <class L>
 __global__ void k_equilibrium(double* pdf, SweepArgs a, const double* rho, int rho_scalar,
                               const double* u, int u_scalar) {
@@ -423,6 +466,26 @@ int launch_macroscopic(SlbmEngine* e, const double* canonical, double* dev_rho, 
     k_macro<L><<<grid_for(e->n_fluid, 256), 256, 0, e->stream>>>(
         src, a, odd, e->geo, compact ? nullptr : e->x_flat, dev_rho, dev_u, bad);
   });
+  int h_bad = 0;
+  SLBM_CUDA_TRY(cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, e->stream));
+  SLBM_CUDA_TRY(cudaFreeAsync(bad, e->stream));
+  SLBM_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  if (h_bad) return fail(SLBM_EUNSTABLE, "non-positive or non-finite density in collision input");
+  return SLBM_OK;
+}
+
+int launch_macroscopic_box(SlbmEngine* e, double* rho, double* u) {
+  SweepArgs a = sweep_args(e);
+  const int odd = (e->pattern == SLBM_AA && e->parity == SLBM_ODD) ? 1 : 0;
+  int* bad = nullptr;
+  SLBM_CUDA_TRY(cudaMallocAsync(&bad, sizeof(int), e->stream));
+  SLBM_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int), e->stream));
+  by_lattice(e->q, [&](auto lat) {
+    using L = decltype(lat);
+    k_macro_box<L><<<grid_for(e->geo.n_cells(), kMacroBlock), kMacroBlock, 0, e->stream>>>(
+        e->pdf, a, odd, e->geo, e->cid_map, rho, u, bad);
+  });
+  SLBM_CUDA_TRY(cudaGetLastError());
   int h_bad = 0;
   SLBM_CUDA_TRY(cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, e->stream));
   SLBM_CUDA_TRY(cudaFreeAsync(bad, e->stream));

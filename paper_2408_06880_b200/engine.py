@@ -349,12 +349,26 @@ class SparseEngine:
         _abi.call("slbm_canonical_state", self._h, _abi.ptr(out, C.c_double))
         return out
 
-    def macroscopic_fields(self) -> tuple[np.ndarray, np.ndarray]:
+    def macroscopic_fields(self, out=None) -> tuple[np.ndarray, np.ndarray]:
+        """sparse.py:323-331: (rho, u) over the block, zeros at solids.
+        ``out=(rho, u)`` (extension) writes into caller-owned C-contiguous
+        float64 arrays of those shapes — e.g. pinned host buffers, which the
+        library reads back with one DMA instead of the staged copy."""
         if self.check == "deferred":
             self.poll()
         shape = rev_shape(self.dims)
-        rho = np.empty(shape, dtype=np.float64)
-        u = np.empty(shape + (self.stencil.dim,), dtype=np.float64)
+        ushape = shape + (self.stencil.dim,)
+        if out is None:
+            rho = np.empty(shape, dtype=np.float64)
+            u = np.empty(ushape, dtype=np.float64)
+        else:
+            rho, u = out
+            for a, want in ((rho, shape), (u, ushape)):
+                if (a.shape != want or a.dtype != np.float64 or not a.flags.c_contiguous
+                        or not a.flags.writeable):
+                    raise errors.make("ConfigurationError",
+                                      f"out arrays must be writeable C-contiguous float64 of "
+                                      f"shapes {shape} and {ushape}")
         _abi.call("slbm_macroscopic", self._h, _abi.ptr(rho, C.c_double), _abi.ptr(u, C.c_double))
         return rho, u
 

@@ -380,6 +380,31 @@ def test_staged_host_copies_roundtrip(chunk_mib, threads, gpu_lib):
         lib.slbm_set_tuning(11, 16)
 
 
+def test_macroscopic_fields_into_pinned_out(gpu_lib):
+    """macroscopic_fields(out=...) with pinned buffers (one DMA) equals the
+    default staged path; bad out arrays are rejected."""
+    import torch
+
+    from paper_2408_06880_b200 import errors, geometry
+    from paper_2408_06880_b200.collision import CollisionParams
+
+    st = make_stencil_d3q19()
+    fl = geometry.packed_bed_flags((64, 48, 40), 0.5, 8.0, 2, periodic=True)
+    eng = _engine(fl, st, CollisionParams(1.2, "trt", 0.9), "aa")
+    eng.init_equilibrium(1.0, np.array([0.01, 0.0, 0.0]))
+    drive(eng, 3)
+    rho, u = eng.macroscopic_fields()
+    shape = rho.shape
+    out = (torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy(),
+           torch.empty(shape + (3,), dtype=torch.float64, pin_memory=True).numpy())
+    r2, u2 = eng.macroscopic_fields(out=out)
+    assert r2 is out[0] and u2 is out[1]
+    np.testing.assert_array_equal(r2, rho)
+    np.testing.assert_array_equal(u2, u)
+    with pytest.raises(errors.ConfigurationError):
+        eng.macroscopic_fields(out=(np.empty(shape, np.float32), u2))
+
+
 def make_stencil_d3q19():
     from paper_2408_06880_b200.lattice import make_stencil
 
