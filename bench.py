@@ -660,7 +660,9 @@ def impl_riverbed(args, rank, world, local_rank):
                                     "frac": round(n0 * bo / to / 1e6 / hbm, 4)},
                      "pair_frac": round(n0 * (be + bo) / (te + to) / 1e6 / hbm, 4)},
         "clocks": clocks.summary(),
-        "gpu_launches": None,
+        # per step: sweep + step counter + lid refresh; N > 1 splits the sweep
+        # (interior + frame) and adds the pack and unpack kernels
+        "gpu_launches": steps * (3 if world == 1 else 6),
     }), flush=True)
 
 
@@ -767,7 +769,9 @@ def impl_artery(args, rank, world, local_rank):
                      "frac": round(achieved / hbm, 4), "traffic": None,
                      "bytes_per_cell": (BYTES_EVEN + BYTES_ODD) / 2, "peak_source": hbm_src},
         "clocks": clocks.summary(),
-        "gpu_launches": None,
+        # per step: local halo, UBB refresh, outlet refresh, block-group sweep,
+        # step counters; N > 1 splits the sweep and adds pack + unpack
+        "gpu_launches": steps * (5 if world == 1 else 8),
         "e2e": {"value": round(total * steps / dt / 1e6, 2), "unit": "MFLUPS",
                 "h2d_bytes_per_step": int(h2d // steps), "d2h_bytes_per_step": int(d2h // steps),
                 "seconds": round(dt, 4), "steps": steps},
