@@ -803,8 +803,9 @@ def main():
 
         dev = int(os.environ.get("SLBM_DEVICE", local_rank))
         torch.cuda.set_device(dev)
-        if os.environ.get("SLBM_TRANSPORT") == "host":
-            # test mode: several ranks on one GPU, halo over host memory + gloo
+        if os.environ.get("SLBM_TRANSPORT") in ("host", "p2p"):
+            # no NCCL on the data path: gloo carries the setup (IPC handles)
+            # and the scalar reductions; also lets several ranks share a GPU
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
