@@ -5,15 +5,16 @@
 // scatter needs no synchronisation and any cell subset (interior / frame)
 // composes bitwise with the whole-block sweep.
 //
-//   k_aa_even  combined pull-collide-push step   sparse.py:264-271
+//   k_index_sweep<kEven>  combined pull-collide-push step  sparse.py:264-271
 //              t0 = pdf[c], t_q = pdf[idx[q-1][c]];  collide;
 //              pdf[c] = out0, pdf[idx[q-1][c]] = out[inv q]
 //              traffic 19x8 R + 19x8 W + 18x4 idx = 376 B/cell (D3Q19)
-//   k_aa_odd   cell-local reversed step          sparse.py:273-282
+//   k_aa_odd   cell-local reversed step                  sparse.py:273-282
 //              t_r = pdf[base[inv r] + c]; pdf[base[r] + c] = out_r
 //              304 B/cell, every access coalesced
-//   k_pull     two-buffer pull                   sparse.py:257-262
-//              gather as k_aa_even, dst[base[r] + c] = out_r; 376 B/cell
+//   k_index_sweep<kPull>  two-buffer pull                 sparse.py:257-262
+//              gather as the even step, dst[base[r] + c] = out_r; 376 B/cell
+// base[] / idx hold device addresses (256-B aligned groups, engine.cuh).
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -51,7 +52,6 @@ constexpr int kIB = 128;     // index-list sweeps: 128-thread CTAs, 4 per SM
 __device__ __forceinline__ void flag_bad(const SweepArgs& a) {
   atomicMin(a.bad, *a.step);
 }
-
 
 // tuning knobs (slbm_set_tuning), kept for tools/variants.py
 int g_even_variant = 0;     // knob 0: 0 = production, 1 = no idx prefetch, 2 = probe

@@ -18,6 +18,11 @@ Differences a caller can observe:
 * ``run(n)`` advances ``n`` whole single-block steps without returning to
   Python (optionally via a captured CUDA graph of one step pair).
 * ``fluid_coords`` and ``idx`` are exported from the device on first access.
+* Extensions: ``macroscopic_fields(out=...)`` (pinned buffers are written
+  directly by the field kernel), ``macroscopic_compact()``, ``set_frame``
+  (per-face frames), ``device_state()`` / ``pdf_layout()`` (the device PDF
+  array: 256-B aligned direction groups; slot ids elsewhere are the
+  reference's), ``frame_width=HaloWidths(...)`` (0 = no frame on an axis).
 """
 
 from __future__ import annotations
