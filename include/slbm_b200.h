@@ -163,6 +163,9 @@ int slbm_set_parity(SlbmEngine* eng, int parity);
 /* pflat: padded flat index of the cell (C order over the padded box)       */
 int slbm_slot_index(const SlbmEngine* eng, const int64_t* qs, const int64_t* pflat,
                     int64_t n, int64_t* out);
+/* padded flat index -> cid (or -1) over the block's padded box: hosts that
+ * resolve many slot_index queries (halo planning) keep a copy             */
+int slbm_export_cid_map(const SlbmEngine* eng, int32_t* out);
 int slbm_ghost_slot_index(const SlbmEngine* eng, const int64_t* qs, const int64_t* pflat,
                           int64_t n, int64_t* out);
 int slbm_read_slots(SlbmEngine* eng, const int64_t* slots, int64_t n, double* out);

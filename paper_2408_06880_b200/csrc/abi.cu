@@ -720,6 +720,15 @@ int slbm_slot_index(const SlbmEngine* ce, const int64_t* qs, const int64_t* pfla
   return SLBM_OK;
 }
 
+int slbm_export_cid_map(const SlbmEngine* e, int32_t* out) {
+  CHECK_ENGINE(e);
+  if (!out) return fail(SLBM_ECONFIG, "null out");
+  if (e->layout || !e->cid_map) return fail(SLBM_ECONFIG, "a dense engine has no cid map");
+  DeviceGuard guard(e->device);
+  return copy_d2h(out, e->cid_map, size_t(e->geo.n_padded()) * sizeof(int32_t), e->device,
+                  e->stream);
+}
+
 int slbm_ghost_slot_index(const SlbmEngine* e, const int64_t* qs, const int64_t* pflat,
                           int64_t n, int64_t* out) {
   CHECK_ENGINE(e);

@@ -244,13 +244,29 @@ class Domain:
 
         self.assignment = dict(_assignment) if _assignment else {b: 0 for b in self.blocks}
         make_engine = engine_factory or _cuda_engine
+        local = []
         for bid, blk in self.blocks.items():
             blk.rank = self.assignment.get(bid, 0)
             # hybrid picks dense at or above phi_s (domain.py:58-65, :109-114)
             blk.kind = classify_kind(blk.porosity, policy, phi_s)
             if blk.rank == self.rank:
-                blk.engine = make_engine(blk.flags, stencil, params, pattern,
-                                         self._block_frame(frame_width), self.device, blk.kind)
+                local.append(blk)
+
+        def build(blk):
+            return make_engine(blk.flags, stencil, params, pattern,
+                               self._block_frame(frame_width), self.device, blk.kind)
+
+        if engine_factory is None and len(local) > 1:
+            # each engine builds its lists on its own stream and the C calls
+            # release the GIL: several blocks build concurrently
+            from concurrent.futures import ThreadPoolExecutor
+
+            with ThreadPoolExecutor(max_workers=min(8, len(local))) as pool:
+                for blk, eng in zip(local, pool.map(build, local)):
+                    blk.engine = eng
+        else:
+            for blk in local:
+                blk.engine = build(blk)
         engines = self.local_engines()
         self._stream = engines[0].stream() if engines and hasattr(engines[0], "stream") else 0
         for e in engines[1:]:

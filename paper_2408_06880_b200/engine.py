@@ -153,6 +153,7 @@ class SparseEngine:
         self.parity = Parity.EVEN
         self.counters = Counters()
         self._fluid_coords = None
+        self._cid_map = None  # host copy for slot_index, fetched on first use
         self._idx = None
         self._padded_shape = want
         self._steps_issued = 0
@@ -440,8 +441,23 @@ class SparseEngine:
         return out
 
     def slot_index(self, coords, qs) -> np.ndarray:
-        """sparse.py:335-343"""
-        return self._lookup("slbm_slot_index", coords, qs)
+        """sparse.py:335-343.  Sparse engines resolve it on the host from a
+        copy of the device cid map (fetched once): halo planning asks for
+        thousands of these, each a GPU round trip otherwise."""
+        if self.layout != "sparse":
+            return self._lookup("slbm_slot_index", coords, qs)
+        if self._cid_map is None:
+            cm = np.empty(int(np.prod(self._padded_shape)), dtype=np.int32)
+            _abi.call("slbm_export_cid_map", self._h, _abi.ptr(cm, C.c_int32))
+            self._cid_map = cm
+        pflat = self._pflat(coords)
+        qs = np.broadcast_to(np.asarray(qs, dtype=np.int64).reshape(-1), pflat.shape)
+        ok = (qs >= 0) & (qs < self.stencil.q) & (pflat >= 0) & (pflat < self._cid_map.size)
+        cid = np.full(pflat.shape, -1, dtype=np.int64)
+        cid[ok] = self._cid_map[pflat[ok]]
+        if not np.all(cid >= 0):
+            raise errors.make("ProtocolError", "exchange addressed a non-fluid cell slot")
+        return np.asarray(self.base, dtype=np.int64)[qs] + cid
 
     def ghost_slot_index(self, coords, qs) -> np.ndarray:
         """sparse.py:345-360"""

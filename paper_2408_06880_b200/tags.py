@@ -156,20 +156,41 @@ class RingField:
         return int(np.prod(self.shape)) * 8
 
     def __array__(self, dtype=None, copy=None):
+        # only cells on the global ring can be non-zero: start from zeros and
+        # fill the (at most 2 per axis) ring planes crossing the window
         tags = self._tags
         nd = tags.ndim
-        sel = tuple(slice(o, o + w) for o, w in zip(self._origin, self._window))
-        cls = np.zeros(self._window, dtype=np.int64)
+        out = np.zeros(self._window + (nd,), dtype=np.float64)
+        sides = []
         for a in range(nd):
             n_pad = tags.shape[a]
             c = np.arange(self._origin[a], self._origin[a] + self._window[a])
-            side = np.where(c == 0, 0, np.where(c == n_pad - 1, 2, 1))
-            shape = [1] * nd
-            shape[a] = self._window[a]
-            cls = cls * 3 + side.reshape(shape)
-        out = self._table.reshape(-1, nd)[cls]
-        t = tags[sel]
-        out[(t != UBB) & (t != OUTLET)] = 0.0
+            sides.append(np.where(c == 0, 0, np.where(c == n_pad - 1, 2, 1)))
+        table = self._table.reshape(-1, nd)
+        for a in range(nd):
+            for g in (0, tags.shape[a] - 1):
+                k = g - self._origin[a]
+                if not 0 <= k < self._window[a]:
+                    continue
+                cls = np.zeros([self._window[b] for b in range(nd) if b != a], dtype=np.int64)
+                for b in range(nd):
+                    side = sides[b] if b != a else np.array([0 if g == 0 else 2])
+                    if b == a:
+                        cls = cls * 3 + int(side[0])
+                        continue
+                    shape = [self._window[c] for c in range(nd) if c != a]
+                    bb = b if b < a else b - 1
+                    view = [1] * (nd - 1)
+                    view[bb] = shape[bb]
+                    cls = cls * 3 + side.reshape(view)
+                sel = [slice(o, o + w) for o, w in zip(self._origin, self._window)]
+                sel[a] = g
+                t = tags[tuple(sel)]
+                vals = table[cls]
+                vals[(t != UBB) & (t != OUTLET)] = 0.0
+                idx = [slice(None)] * nd
+                idx[a] = k
+                out[tuple(idx)] = vals
         return out if dtype is None else out.astype(dtype)
 
     def __getitem__(self, key):
