@@ -155,6 +155,9 @@ int slbm_run(SlbmEngine* eng, int64_t n, int use_graph);
 /* blocks until the engine's stream is idle, then reports the first unstable
  * step (SLBM_EUNSTABLE, *first_bad_step set) or SLBM_OK (-1).  Clears.     */
 int slbm_poll_instability(SlbmEngine* eng, int64_t* first_bad_step);
+/* slbm_poll_instability over several engines with one synchronisation per
+ * distinct stream; on failure `which` is the first unstable engine's index */
+int slbm_poll_engines(SlbmEngine** engines, int n, int64_t* first_bad_step, int* which);
 int slbm_synchronize(SlbmEngine* eng);
 int slbm_parity(const SlbmEngine* eng, int* parity);
 int slbm_set_parity(SlbmEngine* eng, int parity);

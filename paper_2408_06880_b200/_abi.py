@@ -80,6 +80,7 @@ SIGNATURES = {
     "slbm_write_slots": [vp, c_i64p, C.c_int64, c_dp],
     "slbm_pdf_pointer": [vp, C.POINTER(vp)],
     "slbm_export_cid_map": [vp, C.POINTER(C.c_int32)],
+    "slbm_poll_engines": [C.POINTER(vp), C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int)],
     "slbm_pdf_layout": [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
     "slbm_halo_create": [C.c_int, C.POINTER(vp)],
     "slbm_halo_destroy": [vp],

@@ -677,6 +677,36 @@ int slbm_poll_instability(SlbmEngine* e, int64_t* first_bad_step) {
   return fail(SLBM_EUNSTABLE, "non-positive or non-finite density in collision input");
 }
 
+int slbm_poll_engines(SlbmEngine** engines, int n, int64_t* first_bad_step, int* which) {
+  if (!engines || n < 0) return fail(SLBM_ECONFIG, "null engine list");
+  if (first_bad_step) *first_bad_step = -1;
+  if (which) *which = -1;
+  // every flag read is queued first, each distinct stream synchronised once:
+  // one host round trip for a whole block group instead of one per block
+  std::vector<cudaStream_t> streams;
+  for (int i = 0; i < n; ++i) {
+    SlbmEngine* e = engines[i];
+    CHECK_ENGINE(e);
+    DeviceGuard guard(e->device);
+    SLBM_CUDA_TRY(cudaMemcpyAsync(e->h_bad, e->d_bad, sizeof(unsigned long long),
+                                  cudaMemcpyDeviceToHost, e->stream));
+    if (std::find(streams.begin(), streams.end(), e->stream) == streams.end())
+      streams.push_back(e->stream);
+  }
+  for (cudaStream_t st : streams) SLBM_CUDA_TRY(cudaStreamSynchronize(st));
+  for (int i = 0; i < n; ++i) {
+    SlbmEngine* e = engines[i];
+    if (*e->h_bad == ULLONG_MAX) continue;
+    if (first_bad_step) *first_bad_step = int64_t(*e->h_bad);
+    if (which) *which = i;
+    DeviceGuard guard(e->device);
+    SLBM_CUDA_TRY(cudaMemsetAsync(e->d_bad, 0xff, sizeof(unsigned long long), e->stream));
+    SLBM_CUDA_TRY(cudaStreamSynchronize(e->stream));
+    return fail(SLBM_EUNSTABLE, "non-positive or non-finite density in collision input");
+  }
+  return SLBM_OK;
+}
+
 int slbm_synchronize(SlbmEngine* e) {
   CHECK_ENGINE(e);
   DeviceGuard guard(e->device);

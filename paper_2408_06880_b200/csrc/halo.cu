@@ -82,12 +82,12 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
-// a peer that never arrives is a fatal error (trap after 30 s), not a hang
+// a peer that never arrives is a fatal error (trap after 120 s), not a hang
 __device__ __forceinline__ void spin_until(const uint64_t* flag, uint64_t want) {
   const uint64_t t0 = globaltimer();
   while (ld_acquire_sys(flag) < want) {
     __nanosleep(100);
-    if (globaltimer() - t0 > 30ull * 1000000000ull) __trap();
+    if (globaltimer() - t0 > 120ull * 1000000000ull) __trap();
   }
 }
 

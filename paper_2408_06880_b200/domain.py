@@ -558,9 +558,13 @@ class Domain:
         raise errors.make("ConfigurationError", f"unknown driver {name!r}")
 
     def _poll_or_raise(self):
+        engines = self.local_engines()
         try:
-            for e in self.local_engines():
-                e.poll()
+            if engines and all(hasattr(e, "handle") for e in engines):
+                _poll_engines(engines)  # one host round trip for all blocks
+            else:
+                for e in engines:
+                    e.poll()
         except errors.error_class("NumericalInstabilityError") as exc:
             raise errors.make("NumericalInstabilityError", f"unstable at step {self.steps_done}: {exc}") from exc
 
@@ -699,6 +703,23 @@ class BlockGroup:
             if e.pattern == "aa":
                 e.parity = e.parity.flipped()
             e.counters.steps += 1
+
+
+def _poll_engines(engines):
+    """slbm_poll_engines: every block's instability flag, one sync per stream."""
+    import ctypes as C
+
+    from . import _abi
+
+    arr = (C.c_void_p * len(engines))(*[e.handle.value for e in engines])
+    bad, which = C.c_int64(-1), C.c_int(-1)
+    lib = _abi.load()
+    status = lib.slbm_poll_engines(arr, len(engines), C.byref(bad), C.byref(which))
+    if status != 0:
+        msg = lib.slbm_last_error().decode(errors="replace")
+        if bad.value >= 0:
+            msg = f"{msg} (engine step {bad.value})"
+        errors.raise_for_status(status, msg)
 
 
 def _cuda_engine(flags, stencil, params, pattern, frame_width, device, kind="sparse"):
