@@ -287,6 +287,9 @@ class Domain:
         self._face_frames = self._narrow_frames() if engine_factory is None else False
         self._group = self._build_group() if engine_factory is None else None
         self.overlap_samples: list[tuple[float, float]] = []
+        self.trace = False
+        self._pending = []
+        self._capturing = False
         self.steps_done = 0
 
     def _narrow_frames(self) -> bool:
@@ -455,11 +458,46 @@ class Domain:
         for e in self.local_engines():
             e.finish_step()
 
+    # -- tracing (exchange.py:333-374, domain.py:236-239) ----------------------
+    # With ``trace = True`` the drivers record CUDA events on the compute
+    # stream: exchange start, interior start / end, and the join after the
+    # halo wait (= the later of interior end and exchange completion).  Like
+    # the reference's perf_counter spans, a step contributes
+    # (interior span, exchange window) to ``overlap_samples``; events are
+    # resolved lazily (``overlap_ratio`` synchronises).  Off by default.
+
+    def _mark(self):
+        if not self.trace or self._capturing:
+            return None
+        import torch
+
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(torch.cuda.ExternalStream(self._stream))
+        return ev
+
+    def _sample(self, e0, e1, e2, e3):
+        if e0 is not None:
+            self._pending.append((e0, e1, e2, e3))
+
+    def overlap_ratio(self) -> float:
+        """domain.py:236-239: interior time / exchange window over the
+        traced steps (0 when nothing was traced)."""
+        for e0, e1, e2, e3 in self._pending:
+            e3.synchronize()
+            inner = e1.elapsed_time(e2) / 1e3 if e1 is not None else 0.0
+            self.overlap_samples.append((inner, e0.elapsed_time(e3) / 1e3))
+        self._pending = []
+        num = sum(s[0] for s in self.overlap_samples)
+        den = sum(s[1] for s in self.overlap_samples)
+        return num / den if den > 0 else 0.0
+
     def step_sequential(self) -> None:
         """exchange.py:330-346 on the device: exchange, then whole-block sweeps."""
         phase = phase_for(self.pattern, self.parity)
+        e0 = self._mark()
         self._halo.start(phase, self._stream)
         self._halo.wait(self._stream)
+        self._sample(e0, None, None, self._mark())
         self._count_exchange(phase)
         self._refresh_all()
         self._sweep("all")
@@ -476,6 +514,7 @@ class Domain:
         Counters still record the interior/frame split the reference's
         overlapped driver reports."""
         phase = phase_for(self.pattern, self.parity)
+        e0 = self._mark()
         if self._face_frames:
             # remote edges on the comm stream; local edges first on this one
             self._halo.start(phase, self._stream, with_local=False)
@@ -486,13 +525,17 @@ class Domain:
         self._refresh_all()
         if not self._has_remote:
             self._halo.wait(self._stream)
+            self._sample(e0, None, None, self._mark())
             self._sweep("all")
             for e in self.local_engines():
                 e.counters.cells_visited_interior += e.n_interior
                 e.counters.cells_visited_frame += e.n_frame
         else:
+            e1 = self._mark()
             self._sweep("interior")
+            e2 = self._mark()
             self._halo.wait(self._stream)
+            self._sample(e0, e1, e2, self._mark())
             self._sweep("frame")
         self._finish_all()
 
@@ -526,10 +569,12 @@ class Domain:
             engines = self.local_engines()
             snap = [(e.counters.copy(), e.parity) for e in engines]
             _abi.call("slbm_capture_begin", C.c_void_p(self._stream))
+            self._capturing = True
             try:
                 fn()
                 fn()
             finally:
+                self._capturing = False
                 exec_ = C.c_void_p()
                 _abi.call("slbm_capture_end", C.c_void_p(self._stream), C.byref(exec_))
             deltas = []

@@ -205,3 +205,30 @@ def test_gather_macroscopics_compact_and_box_paths(gpu_lib):
         u_b[sel] = v
     np.testing.assert_array_equal(rho_d, rho_b)
     np.testing.assert_array_equal(u_d, u_b)
+
+
+def test_overlap_ratio_tracing(gpu_lib):
+    """domain.py:236-239 / exchange.py:333-374: with tracing on, each step adds
+    (interior span, exchange window) from CUDA events; the overlapped driver
+    with remote (loopback NCCL) edges reports a ratio in (0, 1], the
+    sequential driver 0, and an untraced domain 0."""
+    from paper_2408_06880_b200 import geometry
+    from paper_2408_06880_b200.collision import CollisionParams
+    from paper_2408_06880_b200.domain import DistributedDomain
+    from paper_2408_06880_b200.lattice import make_stencil
+
+    st = make_stencil("d3q19")
+    gf = geometry.packed_bed_flags((32, 32, 64), 0.5, 6.0, 2, periodic=True)
+    p = CollisionParams(1.2, "trt", 0.9)
+    d = DistributedDomain(gf, (32, 32, 32), st, p, pattern="aa", rank=0, world=1, device=0,
+                          loopback=True)
+    d.init_random(1)
+    d.run(4, driver="overlapped")
+    assert d.overlap_ratio() == 0.0  # nothing traced yet
+    d.trace = True
+    d.run(6, driver="overlapped")
+    r = d.overlap_ratio()
+    assert 0.0 < r <= 1.0 and len(d.overlap_samples) == 6
+    d.overlap_samples.clear()
+    d.run(2, driver="sequential")
+    assert d.overlap_ratio() == 0.0 and len(d.overlap_samples) == 2
