@@ -288,6 +288,7 @@ class Domain:
         self._group = self._build_group() if engine_factory is None else None
         self.overlap_samples: list[tuple[float, float]] = []
         self.trace = False
+        self._nvtx_open = False
         self._pending = []
         self._capturing = False
         self.steps_done = 0
@@ -466,11 +467,19 @@ class Domain:
     # (interior span, exchange window) to ``overlap_samples``; events are
     # resolved lazily (``overlap_ratio`` synchronises).  Off by default.
 
-    def _mark(self):
+    def _mark(self, label: str | None = None):
+        """CUDA event on the compute stream (and an NVTX range boundary named
+        ``label`` for Nsight timelines) when tracing."""
         if not self.trace or self._capturing:
             return None
         import torch
 
+        if self._nvtx_open:
+            torch.cuda.nvtx.range_pop()
+            self._nvtx_open = False
+        if label:
+            torch.cuda.nvtx.range_push(label)
+            self._nvtx_open = True
         ev = torch.cuda.Event(enable_timing=True)
         ev.record(torch.cuda.ExternalStream(self._stream))
         return ev
@@ -494,14 +503,15 @@ class Domain:
     def step_sequential(self) -> None:
         """exchange.py:330-346 on the device: exchange, then whole-block sweeps."""
         phase = phase_for(self.pattern, self.parity)
-        e0 = self._mark()
+        e0 = self._mark("slbm.exchange")
         self._halo.start(phase, self._stream)
         self._halo.wait(self._stream)
-        self._sample(e0, None, None, self._mark())
+        self._sample(e0, None, None, self._mark("slbm.sweep"))
         self._count_exchange(phase)
         self._refresh_all()
         self._sweep("all")
         self._finish_all()
+        self._mark()  # closes the last NVTX range
 
     def step_overlapped(self) -> None:
         """exchange.py:349-374: pack/send/recv/unpack on the comm stream while
@@ -514,7 +524,7 @@ class Domain:
         Counters still record the interior/frame split the reference's
         overlapped driver reports."""
         phase = phase_for(self.pattern, self.parity)
-        e0 = self._mark()
+        e0 = self._mark("slbm.exchange_start")
         if self._face_frames:
             # remote edges on the comm stream; local edges first on this one
             self._halo.start(phase, self._stream, with_local=False)
@@ -525,19 +535,20 @@ class Domain:
         self._refresh_all()
         if not self._has_remote:
             self._halo.wait(self._stream)
-            self._sample(e0, None, None, self._mark())
+            self._sample(e0, None, None, self._mark("slbm.sweep"))
             self._sweep("all")
             for e in self.local_engines():
                 e.counters.cells_visited_interior += e.n_interior
                 e.counters.cells_visited_frame += e.n_frame
         else:
-            e1 = self._mark()
+            e1 = self._mark("slbm.interior")
             self._sweep("interior")
-            e2 = self._mark()
+            e2 = self._mark("slbm.halo_wait")
             self._halo.wait(self._stream)
-            self._sample(e0, e1, e2, self._mark())
+            self._sample(e0, e1, e2, self._mark("slbm.frame"))
             self._sweep("frame")
         self._finish_all()
+        self._mark()  # closes the last NVTX range
 
     def run(self, steps: int, driver: str = "sequential", use_graph: bool = False) -> None:
         """``steps`` time steps.  ``use_graph`` (check="deferred" only) captures
