@@ -635,6 +635,20 @@ int slbm_run(SlbmEngine* e, int64_t n, int use_graph) {
   CHECK_ENGINE(e);
   DeviceGuard guard(e->device);
   int64_t done = 0;
+  if (use_graph && resident_eligible(e, n)) {  // small block: one launch for all n steps
+    for (; done < n; done += kResidentChunk) {
+      const int64_t k = std::min<int64_t>(kResidentChunk, n - done);
+      SLBM_TRY(launch_resident(e, k));
+      if (k & 1) {
+        if (e->pattern == SLBM_PULL)
+          std::swap(e->pdf, e->tmp);
+        else
+          e->parity = 1 - e->parity;
+      }
+      e->steps_done += k;
+    }
+    return SLBM_OK;
+  }
   if (use_graph && n >= 2) {
     // state key: AA -> parity; pull -> which buffer is active (pdf < tmp)
     auto key = [&]() { return e->pattern == SLBM_AA ? e->parity : (e->pdf < e->tmp ? 0 : 1); };

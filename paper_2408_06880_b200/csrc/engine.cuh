@@ -95,6 +95,10 @@ namespace slbm {
 // kernels / launchers implemented in kernels.cu
 int launch_step(SlbmEngine* e, int phase);
 int launch_refresh(SlbmEngine* e, int parity);
+// small engines: n steps in one cooperative launch (kernels.cu k_resident)
+constexpr int64_t kResidentChunk = 1 << 12;
+bool resident_eligible(const SlbmEngine* e, int64_t n);
+int launch_resident(SlbmEngine* e, int64_t n);
 int launch_advance(SlbmEngine* e);
 int launch_canonical(SlbmEngine* e, double* dev_out);  // (q, n) at current parity
 // box layout (zeros at solids must be pre-set) or compact: one value per fluid cell

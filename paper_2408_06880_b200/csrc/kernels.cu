@@ -15,6 +15,7 @@
 //   k_index_sweep<kPull>  two-buffer pull                 sparse.py:257-262
 //              gather as the even step, dst[base[r] + c] = out_r; 376 B/cell
 // base[] / idx hold device addresses (256-B aligned groups, engine.cuh).
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -25,6 +26,8 @@
 #include "sweep.cuh"
 
 namespace slbm {
+
+namespace cg = cooperative_groups;
 
 struct SweepArgs {
   double* pdf;
@@ -58,6 +61,7 @@ int g_even_variant = 0;     // knob 0: 0 = production, 1 = no idx prefetch, 2 = 
 int g_odd_variant = 0;      // knob 1: odd-sweep CTAs per SM (0: 3)
 int g_ahead_quarters = 1;   // knob 2: idx prefetch distance in quarter waves
 int g_ahead_ctas = 0;       // knob 3: ... or in CTAs when > 0
+int64_t g_resident_cap = 1 << 19;  // knob 4: slbm_run uses k_resident up to this n_fluid (0: off)
 int g_num_sms = 0;
 
 enum Kind { kPull = 0, kEven = 1, kOdd = 2 };
@@ -204,6 +208,82 @@ __global__ void k_refresh(double* pdf, const uint32_t* slot, const uint32_t* par
 }
 
 __global__ void k_advance(unsigned long long* step) { *step += 1; }
+
+// Resident multi-step kernel for small engines (slbm_run, n_fluid <= the
+// knob-4 cap): one cooperative launch runs n whole steps — refresh, outlet,
+// sweep per step, a grid barrier between phases — instead of 2-3 launches
+// per step.  A block whose lists fit in L2 sweeps in ~2 us, so the per-step
+// launch latency (refresh + sweep + step counter ≈ 9 us in a graph, C1) was
+// the cost.  Same per-cell bodies and phase order as sweep_once, hence
+// bitwise identical; cells are strided over the resident threads.
+struct ResidentArgs {
+  const uint32_t* ubb_slot;
+  const uint32_t* ubb_partner;
+  const double* ubb_corr;
+  uint32_t n_ubb;
+  const uint32_t* out_slot;
+  const uint32_t* out_partner;
+  const uint32_t* out_cell;
+  const uint8_t* out_dir;
+  const double* out_rho;
+  double* out_u;
+  uint32_t n_out;
+  uint32_t steps;
+  int parity;  // AA parity of the first step
+  int pull;
+};
+
+template <class L, int MODEL, int MINB>
+__global__ void __launch_bounds__(kIB, MINB) k_resident(const SweepArgs a, const ResidentArgs r) {
+  cg::grid_group grid = cg::this_grid();
+  const uint32_t tid = blockIdx.x * kIB + threadIdx.x;
+  const uint32_t nth = gridDim.x * kIB;
+  const unsigned long long step0 = *a.step;
+  double* cur = a.pdf;
+  double* oth = a.dst;
+  int parity = r.parity;
+  for (uint32_t k = 0; k < r.steps; ++k) {
+    if (r.n_ubb) {  // sparse.py:301-304, as k_refresh
+      for (uint32_t i = tid; i < r.n_ubb; i += nth) {
+        if (parity == SLBM_EVEN)
+          cur[r.ubb_slot[i]] = cur[r.ubb_partner[i]] + r.ubb_corr[i];
+        else
+          cur[r.ubb_partner[i]] = cur[r.ubb_slot[i]] + r.ubb_corr[i];
+      }
+      grid.sync();
+    }
+    if (r.n_out) {
+      for (uint32_t i = tid; i < r.n_out; i += nth)
+        outlet_entry<L>(cur, a.base, r.out_slot[i], r.out_partner[i], r.out_cell[i], r.out_dir[i],
+                        r.out_rho[i], r.out_u + 3 * i, parity);
+      grid.sync();
+    }
+    bool bad = false;
+    if (r.pull || parity == SLBM_EVEN) {
+      for (uint32_t c = tid; c < a.n_fluid; c += nth) {
+        uint32_t s[L::Q];
+        double t[L::Q];
+        load_slots<L>(s, a.idx, a.idx_pitch, c);
+        gather<L>(t, cur, s);
+        bad |= r.pull ? collide_scatter<L, MODEL, false>(t, s, cur, oth, a.base, c, a.omega, a.lam)
+                      : collide_scatter<L, MODEL, true>(t, s, cur, oth, a.base, c, a.omega, a.lam);
+      }
+    } else {
+      for (uint32_t c = tid; c < a.n_fluid; c += nth)
+        bad |= cell_local<L, MODEL>(cur, a.base, c, a.omega, a.lam);
+    }
+    if (bad) atomicMin(a.bad, step0 + k);
+    grid.sync();
+    if (r.pull) {
+      double* t = cur;
+      cur = oth;
+      oth = t;
+    } else {
+      parity = 1 - parity;
+    }
+  }
+  if (tid == 0) *const_cast<unsigned long long*>(a.step) = step0 + r.steps;
+}
 
 // Fixed-density outlet (extension; the reference has none):
 // outlet_entry (sweep.cuh) per appended outlet slot.
@@ -378,6 +458,7 @@ int set_tuning(int knob, int value) {
   else if (knob == 1) g_odd_variant = value;
   else if (knob == 2) g_ahead_quarters = value;
   else if (knob == 3) g_ahead_ctas = value;
+  else if (knob == 4) g_resident_cap = value;
   else if (knob == 10 || knob == 11) return hostcopy_tune(knob, value);
   else return fail(SLBM_ECONFIG, "unknown tuning knob");
   return SLBM_OK;
@@ -443,6 +524,62 @@ int launch_refresh(SlbmEngine* e, int parity) {
 int launch_advance(SlbmEngine* e) {
   k_advance<<<1, 1, 0, e->stream>>>(e->d_step);
   SLBM_CUDA_TRY(cudaGetLastError());
+  return SLBM_OK;
+}
+
+namespace {
+template <class L, int MODEL>
+cudaError_t resident_launch(const SweepArgs& a, const ResidentArgs& r, cudaStream_t s) {
+  constexpr int MINB = L::Q == 9 ? 8 : 4;
+  auto fn = k_resident<L, MODEL, MINB>;
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kIB, 0);
+    per_sm = std::max(per_sm, 1);
+  }
+  // no more CTAs than cells need: fewer CTAs make the grid barrier cheaper
+  const int64_t need = (int64_t(a.n_fluid) + kIB - 1) / kIB;
+  const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(need, int64_t(per_sm) * num_sms())));
+  void* args[] = {const_cast<SweepArgs*>(&a), const_cast<ResidentArgs*>(&r)};
+  return cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kIB), args, 0, s);
+}
+}  // namespace
+
+bool resident_eligible(const SlbmEngine* e, int64_t n) {
+  return g_resident_cap > 0 && n >= 2 && e->layout == 0 && e->n_fluid > 0 &&
+         e->n_fluid <= g_resident_cap;
+}
+
+// n whole steps in one cooperative launch (k_resident); the caller updates
+// parity / buffers / steps_done as n calls of sweep_once would.
+int launch_resident(SlbmEngine* e, int64_t n) {
+  SweepArgs a = sweep_args(e);
+  ResidentArgs r{};
+  r.ubb_slot = e->ubb_slot;
+  r.ubb_partner = e->ubb_partner;
+  r.ubb_corr = e->ubb_corr;
+  r.n_ubb = uint32_t(e->n_ubb);
+  r.out_slot = e->out_slot;
+  r.out_partner = e->out_partner;
+  r.out_cell = e->out_cell;
+  r.out_dir = e->out_dir;
+  r.out_rho = e->out_rho;
+  r.out_u = e->out_u;
+  r.n_out = uint32_t(e->n_out);
+  r.steps = uint32_t(n);
+  r.parity = e->parity;
+  r.pull = e->pattern == SLBM_PULL ? 1 : 0;
+  cudaError_t ce = cudaSuccess;
+  by_lattice(e->q, [&](auto lat) {
+    using L = decltype(lat);
+    if (e->model == SLBM_SRT)
+      ce = resident_launch<L, SLBM_SRT>(a, r, e->stream);
+    else if (e->model == SLBM_TRT)
+      ce = resident_launch<L, SLBM_TRT>(a, r, e->stream);
+    else if constexpr (L::Q == 27)
+      ce = resident_launch<L, SLBM_CUMULANT>(a, r, e->stream);
+  });
+  if (ce != cudaSuccess) return fail(SLBM_ECUDA, std::string("resident sweep: ") + cudaGetErrorString(ce));
   return SLBM_OK;
 }
 
