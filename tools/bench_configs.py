@@ -103,7 +103,7 @@ def c1():
               "gpu_ms": round(ms, 3), "bitwise_equal_reference_golden": ok,
               "cpu_reference_mflups": round(eng.n_fluid * 100 / cpu_s / 1e6, 3),
               "cpu_reference_bitwise": cpu_ok, "cpu_cores": 1,
-              "note": "GPU timed via engine.run (graph); small problem: launch-latency bound"})
+              "note": "GPU timed via engine.run: one resident cooperative launch for all steps (k_resident)"})
 
 
 def c3(steps):
