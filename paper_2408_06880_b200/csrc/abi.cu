@@ -74,6 +74,7 @@ void free_engine(SlbmEngine* e) {
   if (e->own_stream) cudaStreamSynchronize(e->own_stream);
   for (auto& gx : e->graph)
     if (gx) cudaGraphExecDestroy(gx);
+  free_pair(e);
   void* ptrs[] = {e->pdf,         e->tmp,          e->idx,       e->x_flat,
                   e->cid_map,     e->ubb_slot,     e->ubb_partner, e->ubb_corr,
                   e->ghost_key,   e->frame_cids,   e->frame_bits, e->d_bad,
@@ -649,7 +650,17 @@ int slbm_run(SlbmEngine* e, int64_t n, int use_graph) {
     }
     return SLBM_OK;
   }
-  if (use_graph && n >= 2) {
+  if (use_graph && n >= 2 && pair_eligible(e)) {  // temporally blocked step pairs
+    if (e->parity == SLBM_ODD) {
+      SLBM_TRY(sweep_once(e));
+      done = 1;
+    }
+    for (; done + 2 <= n; done += 2) {
+      SLBM_TRY(launch_pair(e));
+      e->steps_done += 2;
+    }
+  }
+  if (use_graph && n - done >= 2) {
     // state key: AA -> parity; pull -> which buffer is active (pdf < tmp)
     auto key = [&]() { return e->pattern == SLBM_AA ? e->parity : (e->pdf < e->tmp ? 0 : 1); };
     const int k = key();
@@ -667,8 +678,9 @@ int slbm_run(SlbmEngine* e, int64_t n, int use_graph) {
       cudaGraphDestroy(graph);
       if (ce != cudaSuccess) return fail(SLBM_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
     }
-    for (; done + 2 <= n; done += 2) SLBM_CUDA_TRY(cudaGraphLaunch(e->graph[k], e->stream));
-    e->steps_done += done;
+    int64_t pairs = 0;
+    for (; done + 2 <= n; done += 2, pairs += 2) SLBM_CUDA_TRY(cudaGraphLaunch(e->graph[k], e->stream));
+    e->steps_done += pairs;
   }
   for (; done < n; ++done) SLBM_TRY(sweep_once(e));
   return SLBM_OK;

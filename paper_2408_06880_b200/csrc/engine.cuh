@@ -5,6 +5,10 @@
 
 #include "common.cuh"
 
+namespace slbm {
+struct PairPlan;
+}
+
 struct SlbmEngine {
   int device = 0;
   int dim = 3, q = 19;
@@ -71,6 +75,7 @@ struct SlbmEngine {
   // CUDA graphs of one step pair, keyed by starting state (0/1)
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
   int64_t steps_done = 0;
+  slbm::PairPlan* pair = nullptr;  // pair.cu: temporally blocked AA step pair
 
   int ensure_scratch(size_t bytes);
 
@@ -100,6 +105,12 @@ constexpr int64_t kResidentChunk = 1 << 12;
 bool resident_eligible(const SlbmEngine* e, int64_t n);
 int launch_resident(SlbmEngine* e, int64_t n);
 int launch_advance(SlbmEngine* e);
+// pair.cu: one AA step pair (EVEN refresh + even + odd refresh + odd) in one
+// launch, temporally blocked in L2; engines without halo slots
+bool pair_eligible(const SlbmEngine* e);
+int launch_pair(SlbmEngine* e);
+void free_pair(SlbmEngine* e);
+int pair_tune(int knob, int value);
 int launch_canonical(SlbmEngine* e, double* dev_out);  // (q, n) at current parity
 // box layout (zeros at solids must be pre-set) or compact: one value per fluid cell
 int launch_macroscopic(SlbmEngine* e, const double* dev_canon, double* dev_rho, double* dev_u,

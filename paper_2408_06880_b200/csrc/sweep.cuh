@@ -73,15 +73,25 @@ __device__ __forceinline__ bool collide_scatter(const double (&t)[L::Q], const u
   }
 }
 
+// L2-only load (ld.global.cg) for data another SM wrote during the same
+// launch (pair.cu): the reading SM's L1 may hold a stale copy of the line
+template <bool CG>
+__device__ __forceinline__ double ld_pdf(const double* p) {
+  if constexpr (CG)
+    return __ldcg(p);
+  else
+    return *p;
+}
+
 // AA odd (cell-local reversed step, sparse.py:273-282): read the opposite
 // groups, write the own groups — every access a coalesced row
-template <class L, int MODEL>
+template <class L, int MODEL, bool CG = false>
 __device__ __forceinline__ bool cell_local(double* pdf, const uint32_t* base, uint32_t c,
                                            double omega, double lam) {
   double t[L::Q];
   sfor<0, L::Q>([&](auto q) {
     constexpr int qb = L::INV[q];
-    t[q] = pdf[base[qb] + c];
+    t[q] = ld_pdf<CG>(pdf + base[qb] + c);
   });
   return collide<L, MODEL>(t, omega, lam,
                            [&](auto q, double v) { pdf[base[decltype(q)::value] + c] = v; });
@@ -96,7 +106,7 @@ __device__ __forceinline__ bool cell_local(double* pdf, const uint32_t* base, ui
 // the UBB refresh (sparse.py:301-304).  CPU restatement:
 // oracle/sparse_ref.py OracleSparseEngine._refresh_outlet (same op order).
 // `base` = device group starts; `u_store` = this entry's 3 velocity words.
-template <class L>
+template <class L, bool CG = false>
 __device__ __forceinline__ void outlet_entry(double* pdf, const uint32_t* base, uint32_t slot,
                                              uint32_t partner, uint32_t c, int qd, double rho_o,
                                              double* u_store, int parity) {
@@ -138,7 +148,7 @@ __device__ __forceinline__ void outlet_entry(double* pdf, const uint32_t* base, 
   if (parity == SLBM_EVEN)
     pdf[slot] = 2.0 * feq_sym - pdf[partner];
   else
-    pdf[partner] = 2.0 * feq_sym - pdf[slot];
+    pdf[partner] = 2.0 * feq_sym - ld_pdf<CG>(pdf + slot);
 }
 
 }  // namespace slbm
