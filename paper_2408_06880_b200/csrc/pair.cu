@@ -1,30 +1,42 @@
-// AA step pair in one launch, temporally blocked in L2 (slbm_run on sparse
-// engines without halo slots).
+// AA step pair in one launch, temporally blocked in L2 — EXPERIMENTAL,
+// off by default (slbm_set_tuning knob 5 = 1 enables it for slbm_run on
+// sparse AA engines without halo slots).  Bitwise identical to the per-step
+// path (tests/test_gpu_pair.py) but slower on the bench bed; kept with the
+// measurements below for the next attempt.
 //
-// The even step (index list, sparse.py:264-271) of cell n writes into the
-// slots of n's neighbours; the odd step (cell-local, sparse.py:273-282) of
-// cell c reads and rewrites only c's own slots.  So odd(c) may run as soon
-// as even(n) has run for every n that touches one of c's slots — in cid
-// order (z-major) those are within about one z-plane of c.  Run separately,
-// both sweeps stream the whole state through HBM (376 + 304 B/cell, D3Q19);
-// here the odd step of a tile follows the even steps it depends on by about
-// one plane + one wave of CTAs, while the values the even step wrote are
-// still in the 126 MB L2: the odd reads hit L2 and the even writes are
-// overwritten there before they are evicted.  Same per-cell bodies as the
-// two sweeps (sweep.cuh), same order per slot, hence bitwise identical.
+// Idea.  The even step (index list, sparse.py:264-271) of cell n writes into
+// the slots of n's neighbours; the odd step (cell-local, sparse.py:273-282)
+// of cell c reads and rewrites only c's own slots.  So odd(c) may run as
+// soon as even(n) has run for every n that touches one of c's slots — in
+// cid order (z-major) those lie within about one z-plane of c.  If the odd
+// step of a tile follows its writers closely enough, the values the even
+// step wrote are still in the 126 MB L2: odd reads hit L2 and the even
+// writes are overwritten there before eviction (680 -> ~376 B/cell of HBM
+// traffic per pair, D3Q19).
 //
-// Scheduling.  Work items are tiles of 128 cells, even or odd; CTAs take
-// items in a precomputed order by an atomic ticket (not blockIdx), so an
-// item is only ever handed out after every item it may wait for: an odd
-// tile waits (spinning, L2-scope acquire) only for even tiles earlier in the
-// order, which are held by running CTAs that never wait — deadlock free
-// with any residency.  Even tiles publish completion per chunk of 32 tiles
-// (monotonic counters, no reset between launches); odd tiles wait on the
-// chunk range their writers span (computed once from the index list).
-// Tiles whose writers wrap around a periodic boundary wait for all even
-// tiles and are ordered last.  The odd UBB / outlet refresh
-// (sparse.py:301-304) of an entry runs inside the odd tile of its partner
-// cell, after the wait.
+// Design.  Work items are 32-cell tiles (one warp), even or odd, in a
+// precomputed order: odd tile j after the last even tile of its writers'
+// chunks + `slack`.  Persistent warps take items by an atomic ticket (so
+// the items in flight form a window near the frontier); even tiles publish
+// per 128-tile chunk with red.release (no L1 invalidation; an acquire or
+// __threadfence() emits CCTL.IVALL, which wiped the L1 the index gathers
+// rely on: 5x slower); odd tiles poll their writer chunks (near range and
+// the far range across a periodic wrap) with relaxed L2 loads and read the
+// state with ld.global.cg.  The odd UBB / outlet refresh of an entry runs in
+// the odd tile of its partner cell.  Deadlock free: tickets increase per
+// warp, an item only waits for smaller positions, and a warp publishes its
+// pending item before it spins.
+//
+// Measured (512^3 bed, tools/pair_debug.py, profiles/r01_pair.md): the
+// ticket frontier advances ~500 tiles/us, so a few us of DRAM tail latency
+// put thousands of positions between the oldest unfinished item and the
+// newest; an odd tile only finds its writers done with slack >= ~6000
+// tiles, and then ~190K cells (~130 MB of traffic) separate a write from its
+// reuse — more than L2 holds.  Result: 24.4 GB of DRAM per pair instead of
+// 27.4 and 5.2 ms instead of 4.4 ms for the two per-step sweeps.  Per-CTA
+// items (barrier stalls) reached 16.9 GB but 5.1 ms; static round robin let
+// warps drift apart (38 ms).  A blocked cell order (short dependency
+// distance) and a bounded frontier are the next things to try.
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -39,10 +51,9 @@ namespace slbm {
 struct PairPlan {
   int64_t n_tiles = 0, n_chunks = 0, n_items = 0;
   int32_t* sched = nullptr;      // ticket -> item: t >= 0 even tile t, ~j odd tile j
-  uint32_t* dep = nullptr;       // per odd tile: first, last chunk it waits for (kAll: all)
+  uint32_t* dep = nullptr;       // per odd tile: near and far writer chunk ranges (4 words)
   uint32_t* chunk_done = nullptr;  // even tiles completed per chunk, cumulative over launches
   uint32_t* ctl = nullptr;       // [0] ticket, [1] finished items, [2] launch count
-  unsigned long long* total_done = nullptr;  // even tiles completed, cumulative
   uint32_t* ubb_perm = nullptr;  // UBB entries grouped by odd tile of the partner cell
   uint32_t* ubb_start = nullptr;  // n_tiles + 1
   uint32_t* out_perm = nullptr;
@@ -51,14 +62,16 @@ struct PairPlan {
 
 namespace {
 
-constexpr int kPT = 128;            // cells per tile = threads per CTA
-constexpr uint32_t kChunk = 32;     // tiles per completion counter
-constexpr uint32_t kWide = 256;     // chunk span above which a tile waits for all
-constexpr uint32_t kAll = 0xffffffffu;
+constexpr int kTile = 32;           // cells per tile = one warp
+constexpr int kCTA = 128;           // threads per CTA (4 worker warps)
+constexpr uint32_t kChunk = 128;    // tiles per completion counter (4096 cells)
+constexpr uint32_t kWide = 512;     // chunk span above which a tile waits for all
+constexpr uint32_t kBundle = 2;     // schedule positions per ticket
+constexpr uint32_t kNone = 0xffffffffu;
 
-int g_pair = 1;        // knob 5: 0 off
+int g_pair = 0;        // knob 5: 1 = use the pair kernel in slbm_run (experimental)
 int g_pair_slack = 0;  // knob 6: extra tiles between an odd tile's writers and it (0: one wave)
-int g_pair_persist = 1;  // knob 7: persistent CTAs (1) or one CTA per item (0)
+int g_pair_ahead = -1;  // knob 7: idx prefetch distance in tiles (-1: 4 per SM, 0: off)
 
 struct PairArgs {
   double* pdf;
@@ -72,7 +85,6 @@ struct PairArgs {
   const uint32_t* dep;
   uint32_t* chunk_done;
   uint32_t* ctl;
-  unsigned long long* total_done;
   const uint32_t* ubb_slot;
   const uint32_t* ubb_partner;
   const double* ubb_corr;
@@ -89,156 +101,172 @@ struct PairArgs {
   uint32_t ahead;  // idx prefetch distance in tiles
 };
 
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+// Completion flags.  Release: fence.release / red.release (MEMBAR.ALL.GPU,
+// no L1 invalidation — __threadfence() and every acquire operation also
+// emit CCTL.IVALL, which wipes the SM's L1 and with it the sector merging
+// the index-list gathers live on: 5x slower when done per tile).  Poll:
+// ld.relaxed.gpu (L2).  The odd tile's data loads that follow are L2 loads
+// as well (ld.global.cg, sweep.cuh ld_pdf<true>) issued after the poll
+// observed the count, and the writer's release made its stores reach L2
+// before the count: the L2 is the point of coherence for both.
+__device__ __forceinline__ uint32_t ld_poll(const uint32_t* p) {
   uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
+__device__ __forceinline__ void red_release(uint32_t* p) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
 }
 
 constexpr int kEnd = INT_MIN;  // no more items
 
-// even step of tile t (k_index_sweep<kEven> body), then publish completion
-template <class L, int MODEL>
-__device__ __forceinline__ void pair_even(const PairArgs& a, uint32_t t, unsigned long long step) {
-  const uint32_t first = t * kPT;
-  prefetch_idx_ahead<L::Q - 1, kPT>(a.idx, a.idx_pitch, nullptr, a.n_fluid, first, a.ahead);
-  const uint32_t c = first + threadIdx.x;
-  if (c < a.n_fluid) {
-    uint32_t s[L::Q];
-    double v[L::Q];
-    load_slots<L>(s, a.idx, a.idx_pitch, c);
-    gather<L>(v, a.pdf, s);
-    if (collide_scatter<L, MODEL, true>(v, s, a.pdf, a.pdf, a.base, c, a.omega, a.lam))
-      atomicMin(a.bad, step);
+// Publish the completion of the worker's previous even item: lanes' stores
+// -> __syncwarp -> lane 0 fence + counter (the cooperative-groups grid
+// barrier pattern).  Called after the NEXT item's loads are issued, so the
+// fence's wait for outstanding memory operations overlaps loads the warp
+// waits for anyway instead of stalling the warp on its own stores.
+__device__ __forceinline__ void publish(const PairArgs& a, int& pend) {
+  __syncwarp();
+  if (pend >= 0 && (threadIdx.x & 31) == 0) {
+    red_release(&a.chunk_done[uint32_t(pend) / kChunk]);
   }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    atomicAdd(&a.chunk_done[t / kChunk], 1u);
-    atomicAdd(a.total_done, 1ull);
-  }
+  pend = -1;
 }
 
-// odd step of tile j: wait for its writers, odd refresh of the boundary
-// entries of its cells, cell-local sweep (loads from L2: written this launch)
-template <class L, int MODEL>
-__device__ __forceinline__ void pair_odd(const PairArgs& a, uint32_t j, uint32_t epoch,
-                                         unsigned long long step) {
-  if (threadIdx.x < 32) {
-    const uint32_t lo = a.dep[2 * j], hi = a.dep[2 * j + 1];
-    if (lo == kAll) {
-      const unsigned long long target = (unsigned long long)(epoch + 1) * a.n_tiles;
-      if (threadIdx.x == 0)
-        while (ld_acquire(a.total_done) < target) __nanosleep(256);
-    } else {
-      for (uint32_t k0 = lo; k0 <= hi; k0 += 32) {
-        const uint32_t k = k0 + threadIdx.x;
-        if (k <= hi) {
-          const uint32_t size = min(kChunk, a.n_tiles - k * kChunk);
-          const uint32_t target = (epoch + 1) * size;
-          while (ld_acquire(&a.chunk_done[k]) < target) __nanosleep(64);
-        }
-        __syncwarp();
+__device__ __forceinline__ bool range_ready(const PairArgs& a, uint32_t lo, uint32_t hi,
+                                            uint32_t epoch) {
+  const uint32_t lane = threadIdx.x & 31;
+  bool ok = true;
+  for (uint32_t k0 = lo; k0 <= hi; k0 += 32) {
+    const uint32_t k = k0 + lane;
+    if (k <= hi) {
+      const uint32_t size = min(kChunk, a.n_tiles - k * kChunk);
+      ok &= ld_poll(&a.chunk_done[k]) >= (epoch + 1) * size;
+    }
+  }
+  return ok;
+}
+
+// true when every even tile that writes into odd tile j's slots has
+// completed: the chunks of its near writers (within kWide chunks) and of its
+// far ones (across a periodic wrap), two ranges
+__device__ __forceinline__ bool deps_ready(const PairArgs& a, uint32_t j, uint32_t epoch) {
+  const uint4 d = reinterpret_cast<const uint4*>(a.dep)[j];
+  bool ok = range_ready(a, d.x, d.y, epoch);
+  if (d.z != kNone) ok &= range_ready(a, d.z, d.w, epoch);
+  return __all_sync(0xffffffffu, ok);
+}
+
+// Persistent warps taking bundles of kBundle consecutive schedule positions
+// by an atomic ticket (the ticket for the next bundle is fetched one bundle
+// ahead, off the critical path).  Items are handed out in schedule order, so
+// the items in flight form a window about one wave wide and an odd tile's
+// writers (2 x slack positions earlier) are normally done when it starts;
+// static round robin instead lets warps drift apart without bound (measured
+// 8x slower).  Deadlock free: a warp's tickets increase, an odd item waits
+// only for smaller positions, and a warp publishes its pending item before
+// it spins.
+template <class L, int MODEL, int MINB>
+__global__ void __launch_bounds__(kCTA, MINB) k_pair(const PairArgs a) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t W = gridDim.x * (kCTA / 32);
+  const uint32_t w = blockIdx.x * (kCTA / 32) + threadIdx.x / 32;
+  const uint32_t epoch = *(volatile uint32_t*)&a.ctl[2];
+  const unsigned long long step = *(volatile unsigned long long*)a.step;
+  int pend = -1;  // even tile whose completion is not yet published
+  bool bad = false, bad_odd = false;
+  uint32_t tk = 0;  // lane 0: ticket of the next item, fetched while this one's loads fly
+  if (lane == 0) tk = atomicAdd(&a.ctl[0], 1u);
+  uint32_t i = __shfl_sync(0xffffffffu, tk, 0);
+  int item = i < a.n_items ? __ldg(a.sched + i) : kEnd;
+  while (item != kEnd) {
+    if (item >= 0) {
+      const uint32_t t = uint32_t(item);
+      if (a.ahead && lane < L::Q - 1) {  // idx rows of the tile `ahead` tiles later into L2
+        const uint32_t f = (t + a.ahead) * kTile;
+        if (f < a.n_fluid)  // normal priority: evict_last would pin idx lines the odd reuse needs
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(a.idx + size_t(lane) * a.idx_pitch + f));
       }
+      const uint32_t c = t * kTile + lane;
+      const bool valid = c < a.n_fluid;
+      uint32_t s[L::Q];
+      double v[L::Q];
+      if (valid) {
+        load_slots<L>(s, a.idx, a.idx_pitch, c);
+        gather<L>(v, a.pdf, s);
+      }
+      if (lane == 0) tk = atomicAdd(&a.ctl[0], 1u);  // overshoots at the end; reset per launch
+      publish(a, pend);
+      if (valid)
+        bad |= collide_scatter<L, MODEL, true>(v, s, a.pdf, a.pdf, a.base, c, a.omega, a.lam);
+      pend = item;
+    } else {
+      const uint32_t j = ~uint32_t(item);
+      if (!deps_ready(a, j, epoch)) {
+        publish(a, pend);
+        uint32_t spins = 0;
+        while (!deps_ready(a, j, epoch)) {
+          __nanosleep(128);
+          ++spins;
+        }
+        if (lane == 0) {  // debug statistics (slbm_debug_pair_stats)
+          atomicAdd(&a.ctl[4], 1u);
+          atomicAdd(&a.ctl[5], spins);
+          if (atomicCAS(&a.ctl[6], 0u, 1u) == 0u) {
+            a.ctl[7] = j;
+            a.ctl[8] = a.dep[4 * j];
+            a.ctl[9] = a.dep[4 * j + 1];
+            a.ctl[10] = i;
+            a.ctl[11] = w;
+          a.ctl[12] = W;
+          }
+        }
+      }
+      __syncwarp();
+      // odd refresh of the boundary entries whose partner slot is in this tile
+      for (uint32_t k = a.ubb_start[j] + lane; k < a.ubb_start[j + 1]; k += 32) {
+        const uint32_t e = a.ubb_perm[k];
+        a.pdf[a.ubb_partner[e]] = __ldcg(a.pdf + a.ubb_slot[e]) + a.ubb_corr[e];
+      }
+      if (a.out_start) {
+        for (uint32_t k = a.out_start[j] + lane; k < a.out_start[j + 1]; k += 32) {
+          const uint32_t e = a.out_perm[k];
+          outlet_entry<L, true>(a.pdf, a.base, a.out_slot[e], a.out_partner[e], a.out_cell[e],
+                                a.out_dir[e], a.out_rho[e], const_cast<double*>(a.out_u) + 3 * e,
+                                SLBM_ODD);
+        }
+      }
+      __syncwarp();
+      const uint32_t c = j * kTile + lane;
+      const bool valid = c < a.n_fluid;
+      double v[L::Q];
+      if (valid) {
+        sfor<0, L::Q>([&](auto q) {
+          constexpr int qb = L::INV[q];
+          v[q] = __ldcg(a.pdf + a.base[qb] + c);
+        });
+      }
+      if (lane == 0) tk = atomicAdd(&a.ctl[0], 1u);
+      publish(a, pend);
+      if (valid)
+        bad_odd |= collide<L, MODEL>(v, a.omega, a.lam, [&](auto q, double x) {
+          a.pdf[a.base[decltype(q)::value] + c] = x;
+        });
     }
+    i = __shfl_sync(0xffffffffu, tk, 0);
+    item = i < a.n_items ? __ldg(a.sched + i) : kEnd;
   }
-  __syncthreads();
-  for (uint32_t i = a.ubb_start[j] + threadIdx.x; i < a.ubb_start[j + 1]; i += kPT) {
-    const uint32_t e = a.ubb_perm[i];
-    a.pdf[a.ubb_partner[e]] = __ldcg(a.pdf + a.ubb_slot[e]) + a.ubb_corr[e];
-  }
-  if (a.out_start) {
-    for (uint32_t i = a.out_start[j] + threadIdx.x; i < a.out_start[j + 1]; i += kPT) {
-      const uint32_t e = a.out_perm[i];
-      outlet_entry<L, true>(a.pdf, a.base, a.out_slot[e], a.out_partner[e], a.out_cell[e],
-                            a.out_dir[e], a.out_rho[e], const_cast<double*>(a.out_u) + 3 * e,
-                            SLBM_ODD);
-    }
-  }
-  __syncthreads();
-  const uint32_t c = j * kPT + threadIdx.x;
-  if (c < a.n_fluid && cell_local<L, MODEL, true>(a.pdf, a.base, c, a.omega, a.lam))
-    atomicMin(a.bad, step + 1);
-}
-
-__device__ __forceinline__ void pair_item_done(const PairArgs& a, uint32_t epoch,
-                                               unsigned long long step) {
-  __threadfence();
-  if (atomicAdd(&a.ctl[1], 1u) == a.n_items - 1) {  // last item of the launch
-    a.ctl[2] = epoch + 1;
-    *a.step = step + 2;
+  publish(a, pend);
+  if (bad) atomicMin(a.bad, step);
+  if (bad_odd) atomicMin(a.bad, step + 1);
+  if (lane == 0) {
     __threadfence();
-  }
-}
-
-// one CTA per item
-template <class L, int MODEL, int MINB>
-__global__ void __launch_bounds__(kPT, MINB) k_pair(const PairArgs a) {
-  __shared__ int s_item;
-  __shared__ uint32_t s_epoch;
-  __shared__ unsigned long long s_step;
-  if (threadIdx.x == 0) {
-    s_item = a.sched[atomicAdd(&a.ctl[0], 1u)];
-    s_epoch = *(volatile uint32_t*)&a.ctl[2];
-    s_step = *(volatile unsigned long long*)a.step;
-  }
-  __syncthreads();
-  const int item = s_item;
-  if (item >= 0)
-    pair_even<L, MODEL>(a, uint32_t(item), s_step);
-  else
-    pair_odd<L, MODEL>(a, ~uint32_t(item), s_epoch, s_step);
-  __syncthreads();
-  if (threadIdx.x == 0) pair_item_done(a, s_epoch, s_step);
-}
-
-// persistent CTAs (one wave); thread 0 fetches the ticket two items ahead
-// and the item one ahead while the CTA works, so no item starts with a
-// dependent ticket + schedule round trip.  Per-CTA tickets increase, so a
-// waiting item only ever waits for smaller tickets held by CTAs that are
-// not waiting on it: deadlock free.
-template <class L, int MODEL, int MINB>
-__global__ void __launch_bounds__(kPT, MINB) k_pair_persist(const PairArgs a) {
-  __shared__ int s_item;
-  __shared__ uint32_t s_epoch;
-  __shared__ unsigned long long s_step;
-  uint32_t tk = 0;  // thread 0: ticket of the next item
-  if (threadIdx.x == 0) {
-    const uint32_t t0 = atomicAdd(&a.ctl[0], 1u);
-    s_item = t0 < a.n_items ? a.sched[t0] : kEnd;
-    tk = atomicAdd(&a.ctl[0], 1u);
-    s_epoch = *(volatile uint32_t*)&a.ctl[2];
-    s_step = *(volatile unsigned long long*)a.step;
-  }
-  __syncthreads();
-  const uint32_t epoch = s_epoch;
-  const unsigned long long step = s_step;
-  for (;;) {
-    const int item = s_item;
-    if (item == kEnd) break;
-    int nxt = kEnd;
-    uint32_t tk2 = 0;
-    if (threadIdx.x == 0) {
-      tk2 = atomicAdd(&a.ctl[0], 1u);  // overshoots past n_items; reset before each launch
-      if (tk < a.n_items) nxt = __ldg(a.sched + tk);
+    if (atomicAdd(&a.ctl[1], 1u) == W - 1) {  // last warp of the launch
+      a.ctl[2] = epoch + 1;
+      *a.step = step + 2;
+      __threadfence();
     }
-    if (item >= 0)
-      pair_even<L, MODEL>(a, uint32_t(item), step);
-    else
-      pair_odd<L, MODEL>(a, ~uint32_t(item), epoch, step);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      pair_item_done(a, epoch, step);
-      s_item = nxt;
-      tk = tk2;
-    }
-    __syncthreads();
   }
 }
 
@@ -264,15 +292,16 @@ __global__ void k_pair_deps(const uint32_t* idx, uint32_t pitch, uint32_t n_flui
                             Base28 pb, const uint32_t* ubb_sorted, const uint32_t* ubb_entry,
                             const uint32_t* ubb_partner, uint32_t n_ubb,
                             const uint32_t* out_sorted, const uint32_t* out_entry,
-                            const uint32_t* out_partner, uint32_t n_out, uint32_t* lo,
-                            uint32_t* hi) {
+                            const uint32_t* out_partner, uint32_t n_out, uint32_t* dep) {
   const uint32_t n = blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= n_fluid) return;
-  const uint32_t wchunk = (n / kPT) / kChunk;
-  auto add = [&](int64_t c) {
-    const uint32_t t = uint32_t(c / kPT);
-    atomicMin(lo + t, wchunk);
-    atomicMax(hi + t, wchunk);
+  const uint32_t wchunk = (n / kTile) / kChunk;
+  auto add = [&](int64_t c) {  // near range (x, y), far range (z, w) of tile c / kTile
+    const uint32_t t = uint32_t(c / kTile), tc = t / kChunk;
+    const bool near = wchunk + kWide >= tc && wchunk <= tc + kWide;
+    uint32_t* d = dep + 4 * size_t(t) + (near ? 0 : 2);
+    atomicMin(d, wchunk);
+    atomicMax(d + 1, wchunk);
   };
   add(n);
   auto lookup = [&](const uint32_t* sorted, const uint32_t* entry, const uint32_t* partner,
@@ -294,23 +323,23 @@ __global__ void k_pair_deps(const uint32_t* idx, uint32_t pitch, uint32_t n_flui
   }
 }
 
-// dep ranges (wide -> kAll) and the order key: the even tile after which
-// an odd tile is handed out
-__global__ void k_pair_keys(uint32_t* lo, uint32_t* hi, uint32_t n_tiles, uint32_t slack,
-                            uint32_t* key, uint32_t* val) {
+// order key of every odd tile: the even tile after which it is handed out
+// (its last writer chunk's end + slack)
+__global__ void k_pair_keys(const uint32_t* dep, uint32_t n_tiles, uint32_t slack, uint32_t* key,
+                            uint32_t* val) {
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n_tiles) return;
-  uint32_t l = lo[j], h = hi[j];
-  uint32_t k;
-  if (h - l > kWide) {
-    lo[j] = kAll;
-    k = n_tiles - 1;
-  } else {
-    const uint64_t last = uint64_t(h + 1) * kChunk - 1 + slack;
-    k = uint32_t(std::min<uint64_t>(last, n_tiles - 1));
-  }
-  key[j] = k;
+  uint32_t last = dep[4 * j + 1];
+  if (dep[4 * j + 2] != kNone) last = max(last, dep[4 * j + 3]);
+  const uint64_t k = uint64_t(last + 1) * kChunk - 1 + slack;
+  key[j] = uint32_t(std::min<uint64_t>(k, n_tiles - 1));
   val[j] = j;
+}
+
+__global__ void k_pair_dep_init(uint32_t* dep, uint32_t n_tiles) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n_tiles) return;
+  reinterpret_cast<uint4*>(dep)[j] = make_uint4(kNone, 0u, kNone, 0u);
 }
 
 // merge: odd item of sorted rank r goes after even tile key[r]
@@ -329,14 +358,6 @@ __global__ void k_pair_sched(const uint32_t* key_sorted, const uint32_t* odd_sor
   sched[i + l] = int32_t(i);
 }
 
-__global__ void k_pair_dep_pack(const uint32_t* lo, const uint32_t* hi, uint32_t n_tiles,
-                                uint32_t* dep) {
-  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n_tiles) return;
-  dep[2 * j] = lo[j];
-  dep[2 * j + 1] = hi[j];
-}
-
 // entries -> (tile of the partner cell, entry); slot copy for the lookup
 __global__ void k_entry_keys(const uint32_t* slot, const uint32_t* partner, uint32_t n,
                              uint32_t n_fluid, int q, Base28 pb, uint32_t* tile, uint32_t* ent,
@@ -344,7 +365,7 @@ __global__ void k_entry_keys(const uint32_t* slot, const uint32_t* partner, uint
   const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n) return;
   const int64_t c = owner_cell(pb.v, q, n_fluid, partner[e]);
-  tile[e] = c >= 0 ? uint32_t(c / kPT) : 0u;
+  tile[e] = c >= 0 ? uint32_t(c / kTile) : 0u;
   ent[e] = e;
   slot_key[e] = slot[e];
 }
@@ -359,11 +380,6 @@ __global__ void k_tile_starts(const uint32_t* tile_sorted, uint32_t n, uint32_t 
     if (tile_sorted[mid] < t) l = mid + 1; else h = mid;
   }
   start[t] = l;
-}
-
-__global__ void k_fill_u32(uint32_t* p, uint32_t n, uint32_t v) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) p[i] = v;
 }
 
 inline unsigned blocks(int64_t n, int b = 256) { return unsigned(std::max<int64_t>(1, (n + b - 1) / b)); }
@@ -420,7 +436,7 @@ int build_pair_plan(SlbmEngine* e) {
   cudaStream_t s = e->stream;
   auto* p = new PairPlan();
   e->pair = p;
-  const uint32_t n_tiles = uint32_t((e->n_fluid + kPT - 1) / kPT);
+  const uint32_t n_tiles = uint32_t((e->n_fluid + kTile - 1) / kTile);
   p->n_tiles = n_tiles;
   p->n_chunks = (n_tiles + kChunk - 1) / kChunk;
   p->n_items = 2 * int64_t(n_tiles);
@@ -434,40 +450,33 @@ int build_pair_plan(SlbmEngine* e) {
     SLBM_TRY(group_entries(e, e->out_slot, e->out_partner, e->n_out, pb, n_tiles, &p->out_perm,
                            &p->out_start, &o_sorted, &o_entry, s));
 
-  uint32_t *lo = nullptr, *hi = nullptr, *key = nullptr, *val = nullptr, *key2 = nullptr,
-           *val2 = nullptr;
+  uint32_t *key = nullptr, *val = nullptr, *key2 = nullptr, *val2 = nullptr;
   const size_t tb = size_t(n_tiles) * 4;
-  SLBM_CUDA_TRY(cudaMallocAsync(&lo, tb, s));
-  SLBM_CUDA_TRY(cudaMallocAsync(&hi, tb, s));
+  SLBM_CUDA_TRY(cudaMalloc(&p->dep, size_t(n_tiles) * 16));
   SLBM_CUDA_TRY(cudaMallocAsync(&key, tb, s));
   SLBM_CUDA_TRY(cudaMallocAsync(&val, tb, s));
   SLBM_CUDA_TRY(cudaMallocAsync(&key2, tb, s));
   SLBM_CUDA_TRY(cudaMallocAsync(&val2, tb, s));
-  k_fill_u32<<<blocks(n_tiles), 256, 0, s>>>(lo, n_tiles, UINT_MAX);
-  SLBM_CUDA_TRY(cudaMemsetAsync(hi, 0, tb, s));
+  k_pair_dep_init<<<blocks(n_tiles), 256, 0, s>>>(p->dep, n_tiles);
   k_pair_deps<<<blocks(e->n_fluid), 256, 0, s>>>(
       e->idx, uint32_t(e->idx_pitch), uint32_t(e->n_fluid), e->q, pb, u_sorted, u_entry,
       e->ubb_partner, uint32_t(e->n_ubb), o_sorted, o_entry, e->out_partner, uint32_t(e->n_out),
-      lo, hi);
+      p->dep);
   const uint32_t slack =
-      g_pair_slack > 0 ? uint32_t(g_pair_slack) : uint32_t(num_sms_pair() * 4);
-  k_pair_keys<<<blocks(n_tiles), 256, 0, s>>>(lo, hi, n_tiles, slack, key, val);
+      g_pair_slack > 0 ? uint32_t(g_pair_slack) : uint32_t(num_sms_pair() * 12);
+  k_pair_keys<<<blocks(n_tiles), 256, 0, s>>>(p->dep, n_tiles, slack, key, val);
   size_t tmpb = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tmpb, key, key2, val, val2, int(n_tiles), 0, 32, s);
   void* tmp = nullptr;
   SLBM_CUDA_TRY(cudaMallocAsync(&tmp, tmpb, s));
   cub::DeviceRadixSort::SortPairs(tmp, tmpb, key, key2, val, val2, int(n_tiles), 0, 32, s);
   SLBM_CUDA_TRY(cudaMalloc(&p->sched, size_t(p->n_items) * 4));
-  SLBM_CUDA_TRY(cudaMalloc(&p->dep, size_t(n_tiles) * 8));
   k_pair_sched<<<blocks(n_tiles), 256, 0, s>>>(key2, val2, n_tiles, p->sched);
-  k_pair_dep_pack<<<blocks(n_tiles), 256, 0, s>>>(lo, hi, n_tiles, p->dep);
   SLBM_CUDA_TRY(cudaMalloc(&p->chunk_done, size_t(p->n_chunks) * 4));
-  SLBM_CUDA_TRY(cudaMalloc(&p->ctl, 4 * 4));
-  SLBM_CUDA_TRY(cudaMalloc(&p->total_done, 8));
+  SLBM_CUDA_TRY(cudaMalloc(&p->ctl, 16 * 4));
   SLBM_CUDA_TRY(cudaMemsetAsync(p->chunk_done, 0, size_t(p->n_chunks) * 4, s));
-  SLBM_CUDA_TRY(cudaMemsetAsync(p->ctl, 0, 16, s));
-  SLBM_CUDA_TRY(cudaMemsetAsync(p->total_done, 0, 8, s));
-  for (void* q : {(void*)lo, (void*)hi, (void*)key, (void*)val, (void*)key2, (void*)val2, tmp,
+  SLBM_CUDA_TRY(cudaMemsetAsync(p->ctl, 0, 64, s));
+  for (void* q : {(void*)key, (void*)val, (void*)key2, (void*)val2, tmp,
                   (void*)u_sorted, (void*)u_entry})
     SLBM_CUDA_TRY(cudaFreeAsync(q, s));
   if (o_sorted) SLBM_CUDA_TRY(cudaFreeAsync(o_sorted, s));
@@ -480,17 +489,15 @@ int build_pair_plan(SlbmEngine* e) {
 template <class L, int MODEL>
 void pair_launch(const PairArgs& a, cudaStream_t s) {
   constexpr int MINB = L::Q == 9 ? 8 : 4;
-  if (g_pair_persist) {
-    static int per_sm = 0;
-    if (!per_sm) {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pair_persist<L, MODEL, MINB>, kPT, 0);
-      per_sm = std::max(per_sm, 1);
-    }
-    const int64_t grid = std::min<int64_t>(a.n_items, int64_t(per_sm) * num_sms_pair());
-    k_pair_persist<L, MODEL, MINB><<<unsigned(grid), kPT, 0, s>>>(a);
-  } else {
-    k_pair<L, MODEL, MINB><<<a.n_items, kPT, 0, s>>>(a);
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pair<L, MODEL, MINB>, kCTA, 0);
+    per_sm = std::max(per_sm, 1);
   }
+  // one wave: every warp resident (the deadlock-freedom condition)
+  const int64_t grid = std::min<int64_t>((a.n_items + kCTA / 32 - 1) / (kCTA / 32),
+                                         int64_t(per_sm) * num_sms_pair());
+  k_pair<L, MODEL, MINB><<<unsigned(std::max<int64_t>(grid, 1)), kCTA, 0, s>>>(a);
 }
 
 }  // namespace
@@ -498,7 +505,7 @@ void pair_launch(const PairArgs& a, cudaStream_t s) {
 int pair_tune(int knob, int value) {
   if (knob == 5) g_pair = value;
   else if (knob == 6) g_pair_slack = value;
-  else g_pair_persist = value;
+  else g_pair_ahead = value;
   return SLBM_OK;
 }
 
@@ -511,7 +518,7 @@ void free_pair(SlbmEngine* e) {
   if (!e->pair) return;
   PairPlan* p = e->pair;
   for (void* q : {(void*)p->sched, (void*)p->dep, (void*)p->chunk_done, (void*)p->ctl,
-                  (void*)p->total_done, (void*)p->ubb_perm, (void*)p->ubb_start,
+                  (void*)p->ubb_perm, (void*)p->ubb_start,
                   (void*)p->out_perm, (void*)p->out_start})
     if (q) cudaFree(q);
   delete p;
@@ -524,7 +531,7 @@ int launch_pair(SlbmEngine* e) {
   if (!e->pair) SLBM_TRY(build_pair_plan(e));
   SLBM_TRY(launch_refresh(e, SLBM_EVEN));
   PairPlan* p = e->pair;
-  SLBM_CUDA_TRY(cudaMemsetAsync(p->ctl, 0, 2 * sizeof(uint32_t), e->stream));  // ticket, finished
+  SLBM_CUDA_TRY(cudaMemsetAsync(p->ctl, 0, 2 * sizeof(uint32_t), e->stream));  // finished warps
   PairArgs a{};
   a.pdf = e->pdf;
   a.idx = e->idx;
@@ -541,7 +548,6 @@ int launch_pair(SlbmEngine* e) {
   a.dep = p->dep;
   a.chunk_done = p->chunk_done;
   a.ctl = p->ctl;
-  a.total_done = p->total_done;
   a.ubb_slot = e->ubb_slot;
   a.ubb_partner = e->ubb_partner;
   a.ubb_corr = e->ubb_corr;
@@ -555,7 +561,7 @@ int launch_pair(SlbmEngine* e) {
   a.out_u = e->out_u;
   a.out_perm = p->out_perm;
   a.out_start = p->out_start;
-  a.ahead = uint32_t(num_sms_pair());
+  a.ahead = g_pair_ahead >= 0 ? uint32_t(g_pair_ahead) : uint32_t(num_sms_pair() * 4);
   if (e->q == 9)
     e->model == SLBM_SRT ? pair_launch<LatD2Q9, SLBM_SRT>(a, e->stream)
                          : pair_launch<LatD2Q9, SLBM_TRT>(a, e->stream);
@@ -573,3 +579,11 @@ int launch_pair(SlbmEngine* e) {
 }
 
 }  // namespace slbm
+
+// debug: the pair plan's wait statistics of the last launches (not in the header)
+extern "C" int slbm_debug_pair_stats(SlbmEngine* e, uint32_t* out16) {
+  if (!e || !e->pair || !out16) return 1;
+  cudaStreamSynchronize(e->stream);
+  cudaMemcpy(out16, e->pair->ctl, 64, cudaMemcpyDeviceToHost);
+  return 0;
+}

@@ -1,4 +1,4 @@
-"""The temporally blocked AA step pair (pair.cu k_pair: engine.run on
+"""The experimental temporally blocked AA step pair (pair.cu k_pair, knob 5; engine.run on
 sparse AA engines without halo slots) against the per-step path (refresh +
 sweep + step counter per step, pinned to the goldens and the oracle):
 bit-identical states, counters and first-unstable-step on the fuzz
@@ -32,7 +32,7 @@ def knobs(gpu_lib):
 
     yield pair_path
     lib.slbm_set_tuning(RESIDENT_CAP, 1 << 19)
-    lib.slbm_set_tuning(PAIR, 1)
+    lib.slbm_set_tuning(PAIR, 0)
 
 
 def _engines(fl, st, p, seed, **kw):

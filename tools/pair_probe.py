@@ -23,7 +23,6 @@ def main():
     ap.add_argument("--model", default="trt")
     ap.add_argument("--stencil", default="d3q19")
     ap.add_argument("--porosity", type=float, default=0.3)
-    ap.add_argument("--persist", type=int, nargs="*", default=[1, 0])
     args = ap.parse_args()
     import hashlib
 
@@ -66,20 +65,18 @@ def main():
     n = eng.n_fluid
     out = {"edge": args.edge, "n_fluid": n, "model": args.model, "stencil": args.stencil}
     bpc = {19: 680, 27: 968}[st.q]
-    variants = [("per_step", 0, 0, 0)] + [("pair", 1, sl, pe) for pe in args.persist
-                                          for sl in args.slack]
-    for label, pair, slack, persist in variants:
+    variants = [("per_step", 0, 0)] + [("pair", 1, sl) for sl in args.slack]
+    for label, pair, slack in variants:
         lib.slbm_set_tuning(5, pair)
         if True:
             lib.slbm_set_tuning(6, slack)
-            lib.slbm_set_tuning(7, persist)
             if pair and eng._h is not None:
                 eng.close()
                 eng = SparseEngine(fl, st, p, "aa", device=0, check="deferred")
             eng.init_equilibrium(1.0, np.array([0.01, 0.0, 0.0]))
             timed(eng, 3)
             ms = timed(eng, args.pairs)
-            key = label if not pair else f"pair_p{persist}_s{slack}"
+            key = label if not pair else f"pair_s{slack}"
             out[key + "_ms_per_pair"] = round(ms / args.pairs, 4)
             out[key + "_mflups"] = round(2 * n * args.pairs / (ms / 1e3) / 1e6, 1)
             out[key + "_algorithmic_gbs"] = round(bpc * n / (ms / args.pairs / 1e3) / 1e9, 1)
@@ -88,9 +85,8 @@ def main():
             eng.run(10)
             out[key + "_digest"] = digest(eng)
             print(json.dumps(out), flush=True)
-    lib.slbm_set_tuning(5, 1)
+    lib.slbm_set_tuning(5, 0)
     lib.slbm_set_tuning(6, 0)
-    lib.slbm_set_tuning(7, 1)
 
 
 if __name__ == "__main__":
