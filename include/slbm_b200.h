@@ -281,6 +281,11 @@ int slbm_graph_destroy(void* graph_exec);
  *   1  cell-local sweep variant (0: 3 CTAs/SM, 2: 4 CTAs/SM)
  *   2  idx L2 prefetch distance in quarter waves (default 1)
  *   3  ... in CTAs, overriding knob 2 when > 0
+ *   4  slbm_run: resident multi-step kernel up to this many fluid cells
+ *      (default 2^19, 0 = off)
+ *   5  slbm_run: experimental temporally blocked AA pair kernel (default 0)
+ *   6  ... its schedule slack in 32-cell tiles (0 = default)
+ *   7  ... its index-list prefetch distance in tiles (-1 = default, 0 = off)
  *   10 host staging chunk in MiB, 11 host staging threads                   */
 int slbm_set_tuning(int knob, int value);
 
