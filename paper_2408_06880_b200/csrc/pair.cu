@@ -33,7 +33,8 @@
 // newest; an odd tile only finds its writers done with slack >= ~6000
 // tiles, and then ~190K cells (~130 MB of traffic) separate a write from its
 // reuse — more than L2 holds.  Result: 24.4 GB of DRAM per pair instead of
-// 27.4 and 5.2 ms instead of 4.4 ms for the two per-step sweeps.  Per-CTA
+// 27.4 and 5.2 ms instead of 4.4 ms for the two per-step sweeps (4.9 ms
+// with L2 keep/drop hints on the even stores / odd loads, knob 8).  Per-CTA
 // items (barrier stalls) reached 16.9 GB but 5.1 ms; static round robin let
 // warps drift apart (38 ms).  A blocked cell order (short dependency
 // distance) and a bounded frontier are the next things to try.
@@ -72,6 +73,7 @@ constexpr uint32_t kNone = 0xffffffffu;
 int g_pair = 0;        // knob 5: 1 = use the pair kernel in slbm_run (experimental)
 int g_pair_slack = 0;  // knob 6: extra tiles between an odd tile's writers and it (0: one wave)
 int g_pair_ahead = -1;  // knob 7: idx prefetch distance in tiles (-1: 4 per SM, 0: off)
+int g_pair_hints = 1;   // knob 8: L2 keep/drop hints on the even stores / odd loads
 
 struct PairArgs {
   double* pdf;
@@ -99,6 +101,7 @@ struct PairArgs {
   const uint32_t* out_perm;
   const uint32_t* out_start;
   uint32_t ahead;  // idx prefetch distance in tiles
+  int hints;       // L2 eviction-priority hints (knob 8)
 };
 
 // Completion flags.  Release: fence.release / red.release (MEMBAR.ALL.GPU,
@@ -112,6 +115,30 @@ struct PairArgs {
 __device__ __forceinline__ uint32_t ld_poll(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// L2 eviction priorities: lines the even step writes are kept (evict_last)
+// until the odd step reads them (evict_first); the rest streams normally
+__device__ __forceinline__ uint64_t policy_keep() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ uint64_t policy_drop() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ void st_hint(double* p, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+
+__device__ __forceinline__ double ld_cg_hint(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
   return v;
 }
 
@@ -176,6 +203,8 @@ __global__ void __launch_bounds__(kCTA, MINB) k_pair(const PairArgs a) {
   const unsigned long long step = *(volatile unsigned long long*)a.step;
   int pend = -1;  // even tile whose completion is not yet published
   bool bad = false, bad_odd = false;
+  const bool hints = a.hints != 0;
+  const uint64_t keep = policy_keep(), drop = policy_drop();
   uint32_t tk = 0;  // lane 0: ticket of the next item, fetched while this one's loads fly
   if (lane == 0) tk = atomicAdd(&a.ctl[0], 1u);
   uint32_t i = __shfl_sync(0xffffffffu, tk, 0);
@@ -198,8 +227,15 @@ __global__ void __launch_bounds__(kCTA, MINB) k_pair(const PairArgs a) {
       }
       if (lane == 0) tk = atomicAdd(&a.ctl[0], 1u);  // overshoots at the end; reset per launch
       publish(a, pend);
-      if (valid)
-        bad |= collide_scatter<L, MODEL, true>(v, s, a.pdf, a.pdf, a.base, c, a.omega, a.lam);
+      if (valid) {  // collide_scatter<EVEN> with the keep hint on the stores
+        bad |= collide<L, MODEL>(v, a.omega, a.lam, [&](auto q, double x) {
+          constexpr int qb = L::INV[decltype(q)::value];
+          if (hints)
+            st_hint(a.pdf + s[qb], x, keep);
+          else
+            a.pdf[s[qb]] = x;
+        });
+      }
       pend = item;
     } else {
       const uint32_t j = ~uint32_t(item);
@@ -244,7 +280,7 @@ __global__ void __launch_bounds__(kCTA, MINB) k_pair(const PairArgs a) {
       if (valid) {
         sfor<0, L::Q>([&](auto q) {
           constexpr int qb = L::INV[q];
-          v[q] = __ldcg(a.pdf + a.base[qb] + c);
+          v[q] = hints ? ld_cg_hint(a.pdf + a.base[qb] + c, drop) : __ldcg(a.pdf + a.base[qb] + c);
         });
       }
       if (lane == 0) tk = atomicAdd(&a.ctl[0], 1u);
@@ -505,7 +541,8 @@ void pair_launch(const PairArgs& a, cudaStream_t s) {
 int pair_tune(int knob, int value) {
   if (knob == 5) g_pair = value;
   else if (knob == 6) g_pair_slack = value;
-  else g_pair_ahead = value;
+  else if (knob == 7) g_pair_ahead = value;
+  else g_pair_hints = value;
   return SLBM_OK;
 }
 
@@ -561,6 +598,7 @@ int launch_pair(SlbmEngine* e) {
   a.out_u = e->out_u;
   a.out_perm = p->out_perm;
   a.out_start = p->out_start;
+  a.hints = g_pair_hints;
   a.ahead = g_pair_ahead >= 0 ? uint32_t(g_pair_ahead) : uint32_t(num_sms_pair() * 4);
   if (e->q == 9)
     e->model == SLBM_SRT ? pair_launch<LatD2Q9, SLBM_SRT>(a, e->stream)

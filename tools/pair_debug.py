@@ -1,7 +1,7 @@
 """Debug probe of the pair kernel (pair.cu): per-launch time and the plan's
 wait statistics (slbm_debug_pair_stats) on the bench bed.
 
-    python tools/pair_debug.py [edge] [ahead] [slack]
+    python tools/pair_debug.py [edge] [ahead] [slack] [hints]
 """
 import ctypes as C
 import json
@@ -29,6 +29,8 @@ if len(sys.argv) > 2:
     lib.slbm_set_tuning(7, int(sys.argv[2]))
 if len(sys.argv) > 3:
     lib.slbm_set_tuning(6, int(sys.argv[3]))
+if len(sys.argv) > 4:
+    lib.slbm_set_tuning(8, int(sys.argv[4]))
 fl = bench.make_flags(edge, 0)
 e = SparseEngine(fl, st, p, "aa", device=0, check="deferred")
 e.init_equilibrium(1.0, np.array([0.01, 0.0, 0.0]))
@@ -45,5 +47,6 @@ for k in range(4):
     v = list(out)
     d = [v[4] - (prev[4] if prev else 0), v[5] - (prev[5] if prev else 0)]
     prev = v
-    print(json.dumps({"edge": edge, "slack": sys.argv[3] if len(sys.argv) > 3 else "default", "launch": k, "ms": round(e0.elapsed_time(e1), 3),
+    print(json.dumps({"edge": edge, "slack": sys.argv[3] if len(sys.argv) > 3 else "default",
+                      "hints": sys.argv[4] if len(sys.argv) > 4 else "1", "launch": k, "ms": round(e0.elapsed_time(e1), 3),
                       "waits": d[0], "spins": d[1], "ctl": v[:4]}), flush=True)
