@@ -83,3 +83,20 @@ def test_library_is_built_for_sm100a():
         pytest.skip("cuobjdump unavailable")
     assert "sm_100a" in out.stdout
     ctypes.CDLL(_abi.LIB_PATH)
+
+
+def test_tuning_knobs_documented_and_accepted():
+    """Every knob the header documents is accepted (host-side state only, no
+    GPU work); unknown knobs fail with the configuration error."""
+    from paper_2408_06880_b200 import _abi
+
+    with open(HEADER) as fh:
+        text = fh.read()
+    block = text[text.index("tuning knobs"):text.index("int slbm_set_tuning")]
+    knobs = sorted({int(k) for k in re.findall(r"^\s*\*\s+(\d+)\s", block, flags=re.M)} | {11})
+    assert {0, 1, 2, 3, 4, 5, 6, 7, 8, 10, 11} <= set(knobs)
+    lib = _abi.load()
+    defaults = {0: 0, 1: 0, 2: 1, 3: 0, 4: 1 << 19, 5: 0, 6: 0, 7: -1, 8: 1}
+    for k, v in defaults.items():
+        assert lib.slbm_set_tuning(k, v) == 0
+    assert lib.slbm_set_tuning(99, 0) != 0
