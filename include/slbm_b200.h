@@ -150,7 +150,9 @@ int slbm_refresh_boundary(SlbmEngine* eng, int parity);
 int slbm_step(SlbmEngine* eng, int phase);
 int slbm_finish_step(SlbmEngine* eng);
 /* n full single-block steps (refresh_boundary + step(all) + finish_step), no
- * host sync; use_graph=1 replays a captured CUDA graph of one step pair.   */
+ * host sync; use_graph=1 replays a captured CUDA graph of one step pair, or
+ * for blocks up to 2^19 fluid cells (knob 4) runs all n steps in one
+ * cooperative launch (resident kernel, bitwise the same result).          */
 int slbm_run(SlbmEngine* eng, int64_t n, int use_graph);
 /* blocks until the engine's stream is idle, then reports the first unstable
  * step (SLBM_EUNSTABLE, *first_bad_step set) or SLBM_OK (-1).  Clears.     */
