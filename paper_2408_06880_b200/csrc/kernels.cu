@@ -263,6 +263,9 @@ __global__ void __launch_bounds__(kIB, MINB) k_resident(const SweepArgs a, const
       for (uint32_t c = tid; c < a.n_fluid; c += nth) {
         uint32_t s[L::Q];
         double t[L::Q];
+        // idx rows of this warp's next cells into L2 (as the sweep kernels do)
+        const uint32_t lane = threadIdx.x & 31, nxt = c - lane + nth;
+        if (lane < L::Q - 1 && nxt < a.n_fluid) prefetch_l2(a.idx + size_t(lane) * a.idx_pitch + nxt);
         load_slots<L>(s, a.idx, a.idx_pitch, c);
         gather<L>(t, cur, s);
         bad |= r.pull ? collide_scatter<L, MODEL, false>(t, s, cur, oth, a.base, c, a.omega, a.lam)

@@ -28,9 +28,9 @@ def main():
     from paper_2408_06880_b200.lattice import make_stencil
 
     lib = _abi.load()
-    for name, model in (("d3q19", "srt"), ("d3q19", "trt"), ("d3q27", "cumulant")):
+    for name, model in (("d3q19", "trt"), ("d3q27", "cumulant")):
         st = make_stencil(name)
-        for n in (32, 48, 64, 80, 96, 128, 160):
+        for n in ([32, 64, 96, 128, 160, 192] if name == "d3q19" else [64, 96, 128]):
             fl = geometry.packed_bed_flags((n, n, n), 0.5, n / 10.0, 1, channel=False)
             for pattern in ("aa", "pull"):
                 if pattern == "pull" and name != "d3q19":
