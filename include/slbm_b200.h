@@ -289,6 +289,7 @@ int slbm_graph_destroy(void* graph_exec);
  *   6  ... its schedule slack in 32-cell tiles (0 = default)
  *   7  ... its index-list prefetch distance in tiles (-1 = default, 0 = off)
  *   8  ... its L2 keep/drop hints (default 1)
+ *   9  dense engines: lean whole-block odd sweep k_dense_odd (default 1)
  *   10 host staging chunk in MiB, 11 host staging threads                   */
 int slbm_set_tuning(int knob, int value);
 

@@ -34,6 +34,7 @@ namespace slbm {
 namespace {
 
 constexpr uint32_t kSolid = 0xffffffffu;
+int g_dense_lean_odd = 1;  // knob 9: lean whole-block odd sweep (k_dense_odd)
 constexpr uint32_t kHasUbb = 0x80000000u;
 constexpr uint8_t kFluidT = 0, kUbbT = 2, kExchT = 3, kOutT = 4;
 
@@ -212,6 +213,44 @@ __global__ void __launch_bounds__(128, 4) k_dense(const DenseArgs a, uint32_t ah
     }
   }
   if (bad) atomicMin(a.bad, *a.step);
+}
+
+// Lean AA odd (cell-local) sweep for whole-block phases: the same per-cell
+// arithmetic as k_dense<KIND 2>, addressing every group through a table of
+// 32-bit group starts (q * npad) that the compiler folds into the load
+// instructions — k_dense<2> computes q * npad + p per direction and needs
+// 122 registers at 4 CTAs/SM (80 + 128 B of spills at 6); this fits 80
+// registers without spills, 6 CTAs/SM.
+struct DenseOddArgs {
+  double* pdf;
+  const uint32_t* mask;
+  uint32_t X, Y, PX, PY, offz;
+  uint32_t base[28];  // q * npad
+  double omega, lam;
+  unsigned long long* bad;
+  const unsigned long long* step;
+};
+
+template <class L, int MODEL>
+__global__ void __launch_bounds__(128, L::Q == 27 ? 5 : 6) k_dense_odd(const DenseOddArgs a) {
+  const uint32_t chunks = (a.X + 127) / 128;
+  const uint32_t row = blockIdx.x / chunks, chunk = blockIdx.x - row * chunks;
+  const uint32_t x = chunk * 128 + threadIdx.x;
+  if (x >= a.X) return;
+  const uint32_t y = row % a.Y, z = row / a.Y;
+  const uint32_t p = ((z + a.offz) * a.PY + y + 1) * a.PX + x + 1;
+  double t[L::Q];
+  sfor<0, L::Q>([&](auto q) {
+    constexpr int qb = L::INV[q];
+    t[q] = a.pdf[a.base[qb] + p];
+  });
+  // a solid cell's loads above were harmless reads; its results are dropped
+  // (predicated stores: an early return here costs 128 B of spills)
+  const bool fluid = a.mask[row * a.X + x] != kSolid;
+  if (collide<L, MODEL>(t, a.omega, a.lam, [&](auto q, double v) {
+        if (fluid) a.pdf[a.base[decltype(q)::value] + p] = v;
+      }) && fluid)
+    atomicMin(a.bad, *a.step);
 }
 
 // fold mask per box cell and the number of UBB folds (for the entry list)
@@ -446,6 +485,19 @@ int dense_step(SlbmEngine* e, int phase) {
   const uint32_t ahead = uint32_t(sms);  // ~ a quarter wave of 128-thread CTAs
   // speculative loads pay off when few box cells are solid
   const bool spec = double(e->n_fluid) >= 0.75 * double(e->geo.n_cells());
+  DenseOddArgs oa{};
+  oa.pdf = a.pdf;
+  oa.mask = a.mask;
+  oa.X = uint32_t(e->geo.n[0]);
+  oa.Y = uint32_t(e->geo.n[1]);
+  oa.PX = uint32_t(e->geo.p[0]);
+  oa.PY = uint32_t(e->geo.p[1]);
+  oa.offz = uint32_t(e->geo.off[2]);
+  for (int q = 0; q < 28 && q < e->q; ++q) oa.base[q] = uint32_t(q) * uint32_t(a.npad);
+  oa.omega = a.omega;
+  oa.lam = a.lam;
+  oa.bad = a.bad;
+  oa.step = a.step;
   with_lattice(e->q, [&](auto lat) {
     using L = decltype(lat);
     auto go = [&](auto model) {
@@ -456,6 +508,8 @@ int dense_step(SlbmEngine* e, int phase) {
           k_dense<L, M, 0, S><<<grid, 128, 0, e->stream>>>(a, ahead);
         else if (kind == 1)
           k_dense<L, M, 1, S><<<grid, 128, 0, e->stream>>>(a, ahead);
+        else if (phase == SLBM_PHASE_ALL && g_dense_lean_odd)
+          k_dense_odd<L, M><<<grid, 128, 0, e->stream>>>(oa);
         else
           k_dense<L, M, 2, S><<<grid, 128, 0, e->stream>>>(a, ahead);
       };
@@ -494,6 +548,11 @@ int dense_canonical(SlbmEngine* e, double* dev_values) {
   k_dense_gather<<<grid_of(e->n_fluid, 256), 256, 0, e->stream>>>(
       e->pdf, e->x_flat, e->n_fluid, e->geo.n_padded(), e->dirs, odd, dev_values);
   SLBM_CUDA_TRY(cudaGetLastError());
+  return SLBM_OK;
+}
+
+int dense_tune(int value) {
+  g_dense_lean_odd = value;
   return SLBM_OK;
 }
 

@@ -111,6 +111,7 @@ bool pair_eligible(const SlbmEngine* e);
 int launch_pair(SlbmEngine* e);
 void free_pair(SlbmEngine* e);
 int pair_tune(int knob, int value);
+int dense_tune(int value);  // knob 9: lean dense odd sweep on/off
 int launch_canonical(SlbmEngine* e, double* dev_out);  // (q, n) at current parity
 // box layout (zeros at solids must be pre-set) or compact: one value per fluid cell
 int launch_macroscopic(SlbmEngine* e, const double* dev_canon, double* dev_rho, double* dev_u,

@@ -1,7 +1,7 @@
 """Dense (direct-addressing) sweeps on a box of porosity PHI: per-kernel
 times (CUDA events per step) and the fraction of the measured copy peak.
 
-    python tools/dense_probe.py [edge] [phi] [steps]
+    python tools/dense_probe.py [edge] [phi] [steps] [lean odd 1|0]
 
 Measured (384^3, phi 1.0): even 0.89, odd 0.85 of the copy peak; 5 or 6
 CTAs/SM for the odd sweep (96 / 80 registers, spills) were slower (0.84 /
@@ -26,8 +26,12 @@ from paper_2408_06880_b200.lattice import make_stencil  # noqa: E402
 edge = int(sys.argv[1]) if len(sys.argv) > 1 else 384
 phi = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
 steps = int(sys.argv[3]) if len(sys.argv) > 3 else 40
+lean = int(sys.argv[4]) if len(sys.argv) > 4 else 1
 
 torch.cuda.set_device(0)
+from paper_2408_06880_b200 import _abi  # noqa: E402
+
+_abi.load().slbm_set_tuning(9, lean)
 
 st = make_stencil("d3q19")
 p = CollisionParams(bench.OMEGA, "trt", bench.magic_lambda(bench.OMEGA))
@@ -53,6 +57,6 @@ odd = statistics.mean(t for t, q in zip(per, par) if q == 1)
 cells = edge ** 3
 peak = bench.measured_peak_gbs() if hasattr(bench, "measured_peak_gbs") else 6549.1
 gbs = lambda ms: cells * 304 / (ms / 1e3) / 1e9  # noqa: E731
-print(json.dumps({"edge": edge, "phi": phi, "even_ms": round(even, 4), "odd_ms": round(odd, 4),
+print(json.dumps({"edge": edge, "phi": phi, "lean_odd": lean, "even_ms": round(even, 4), "odd_ms": round(odd, 4),
                   "even_frac": round(gbs(even) / peak, 3), "odd_frac": round(gbs(odd) / peak, 3),
                   "mflups": round(cells * steps / (sum(per) / 1e3) / 1e6, 1)}))
