@@ -5,8 +5,11 @@ times (CUDA events per step) and the fraction of the measured copy peak.
 
 Measured (384^3, phi 1.0): even 0.89, odd 0.85 of the copy peak; 5 or 6
 CTAs/SM for the odd sweep (96 / 80 registers, spills) were slower (0.84 /
-0.79).  The odd sweep's gap to the sparse one (1.03) is the padded box
-layout: every warp row starts 8 B past a line boundary (x + 1).
+0.79).  The lean odd kernel (k_dense_odd, knob 9) then reached 0.97.  A lean
+combined (even) step in the same style — per-direction constant offsets
+recomputed at the store, predicated solid cells — compiled to 84 registers
+without spills but ran at 0.60 (vs 0.85): the per-direction face-wrap
+branches break up the batch of 19 loads.  Not kept.
 """
 import json
 import os
