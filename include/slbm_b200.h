@@ -290,7 +290,9 @@ int slbm_graph_destroy(void* graph_exec);
  *   7  ... its index-list prefetch distance in tiles (-1 = default, 0 = off)
  *   8  ... its L2 keep/drop hints (default 1)
  *   9  dense engines: lean whole-block odd sweep k_dense_odd (default 1)
- *   10 host staging chunk in MiB, 11 host staging threads                   */
+ *   10 host staging chunk in MiB, 11 host staging threads
+ *   12 slbm_macroscopic into pinned buffers: 0 = HBM staging + DMA copy
+ *      (default), 1 = field kernel writes mapped host memory             */
 int slbm_set_tuning(int knob, int value);
 
 const char* slbm_last_error(void);

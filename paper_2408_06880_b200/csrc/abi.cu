@@ -527,11 +527,25 @@ int slbm_macroscopic(SlbmEngine* e, double* rho, double* u) {
   if (odd) SLBM_TRY(launch_refresh(e, SLBM_ODD));
   const int64_t cells = e->geo.n_cells();
   if (!e->layout) {
-    // pinned destinations: the kernel writes the fields straight into them
-    // over PCIe (no device staging buffer, no separate DMA)
     void* drho = mapped_device_ptr(rho);
     void* du = mapped_device_ptr(u);
-    if (drho && du) return launch_macroscopic_box(e, (double*)drho, (double*)du);
+    if (drho && du) {
+      // pinned destinations
+      if (mapped_out_enabled())  // the kernel writes straight into them over PCIe
+        return launch_macroscopic_box(e, (double*)drho, (double*)du);
+      // box fields into HBM (zeros at solids written by the kernel), then
+      // one DMA copy each at the link rate
+      SLBM_TRY(e->ensure_scratch(size_t(cells) * (1 + e->dim) * sizeof(double)));
+      double* d_rho = e->d_scratch;
+      double* d_u = e->d_scratch + cells;
+      SLBM_TRY(launch_macroscopic_box(e, d_rho, d_u));
+      SLBM_CUDA_TRY(cudaMemcpyAsync(rho, d_rho, size_t(cells) * sizeof(double),
+                                    cudaMemcpyDeviceToHost, e->stream));
+      SLBM_CUDA_TRY(cudaMemcpyAsync(u, d_u, size_t(cells) * e->dim * sizeof(double),
+                                    cudaMemcpyDeviceToHost, e->stream));
+      SLBM_CUDA_TRY(cudaStreamSynchronize(e->stream));
+      return SLBM_OK;
+    }
   }
   const size_t nq = e->layout ? size_t(e->q) * e->n_fluid : 0;
   SLBM_TRY(e->ensure_scratch((size_t(cells) * (1 + e->dim) + nq) * sizeof(double)));

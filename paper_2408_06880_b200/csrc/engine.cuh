@@ -140,7 +140,8 @@ void* mapped_device_ptr(void* host);  // pinned host buffer -> device address, e
 // macroscopic fields of every box cell written straight into (mapped) host
 // memory: zeros at solids, no device staging
 int launch_macroscopic_box(SlbmEngine* e, double* rho, double* u);
-int hostcopy_tune(int knob, int value);  // 10: chunk MiB, 11: max threads
+int hostcopy_tune(int knob, int value);  // 10: chunk MiB, 11: max threads, 12: mapped out
+bool mapped_out_enabled();
 
 // builder.cu
 int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,

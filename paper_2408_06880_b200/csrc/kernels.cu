@@ -464,7 +464,7 @@ int set_tuning(int knob, int value) {
   else if (knob == 4) g_resident_cap = value;
   else if (knob >= 5 && knob <= 8) return pair_tune(knob, value);
   else if (knob == 9) return dense_tune(value);
-  else if (knob == 10 || knob == 11) return hostcopy_tune(knob, value);
+  else if (knob == 10 || knob == 11 || knob == 12) return hostcopy_tune(knob, value);
   else return fail(SLBM_ECONFIG, "unknown tuning knob");
   return SLBM_OK;
 }
