@@ -9,7 +9,9 @@ CTAs/SM for the odd sweep (96 / 80 registers, spills) were slower (0.84 /
 combined (even) step in the same style — per-direction constant offsets
 recomputed at the store, predicated solid cells — compiled to 84 registers
 without spills but ran at 0.60 (vs 0.85): the per-direction face-wrap
-branches break up the batch of 19 loads.  Not kept.
+branches break up the batch of 19 loads.  An interior-only variant with
+straight-line loads (face cells left to k_dense<1> in a frame pass) was
+bitwise equal but also slower (0.59 vs 0.71 at phi 0.8).  Not kept.
 """
 import json
 import os
@@ -60,6 +62,9 @@ odd = statistics.mean(t for t, q in zip(per, par) if q == 1)
 cells = edge ** 3
 peak = bench.measured_peak_gbs() if hasattr(bench, "measured_peak_gbs") else 6549.1
 gbs = lambda ms: cells * 304 / (ms / 1e3) / 1e9  # noqa: E731
-print(json.dumps({"edge": edge, "phi": phi, "lean_odd": lean, "even_ms": round(even, 4), "odd_ms": round(odd, 4),
+import hashlib  # noqa: E402
+
+digest = hashlib.sha256(eng.canonical_state().tobytes()).hexdigest()[:16]
+print(json.dumps({"edge": edge, "phi": phi, "lean_odd": lean, "state_sha": digest, "even_ms": round(even, 4), "odd_ms": round(odd, 4),
                   "even_frac": round(gbs(even) / peak, 3), "odd_frac": round(gbs(odd) / peak, 3),
                   "mflups": round(cells * steps / (sum(per) / 1e3) / 1e6, 1)}))
