@@ -25,6 +25,7 @@
 #include <cstring>
 
 #include "engine.cuh"
+#include "sweep.cuh"
 
 namespace slbm {
 namespace {
@@ -279,7 +280,7 @@ __global__ void k_physical_idx(const uint32_t* in, int64_t n, int64_t pitch, int
   const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= rows * n) return;
   const int64_t r = t / n, c = t - r * n;
-  out[r * pitch + c] = m(in[t]);
+  out[idx_offset(rows == 18, uint32_t(pitch), uint32_t(r), uint32_t(c))] = m(in[t]);
 }
 
 // physical rows of `pitch` -> the reference's contiguous (Q-1) x n slot ids
@@ -288,7 +289,7 @@ __global__ void k_logical_idx(const uint32_t* in, int64_t n, int64_t pitch, int6
   const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= rows * n) return;
   const int64_t r = t / n, c = t - r * n;
-  out[t] = inv(in[r * pitch + c]);
+  out[t] = inv(in[idx_offset(rows == 18, uint32_t(pitch), uint32_t(r), uint32_t(c))]);
 }
 
 __global__ void k_physical_inplace(uint32_t* v, int64_t n, SlotMap m) {

@@ -125,8 +125,7 @@ __global__ void __launch_bounds__(kIB) k_probe(const SweepArgs a) {
   const uint32_t c = i;
   uint32_t s[L::Q];
   double t[L::Q];
-  s[0] = c;
-  sfor<1, L::Q>([&](auto q) { s[q] = __ldcs(a.idx + size_t(q - 1) * a.idx_pitch + c); });
+  load_slots<L>(s, a.idx, a.idx_pitch, c);
   sfor<0, L::Q>([&](auto q) { t[q] = a.pdf[s[q]]; });
   sfor<0, L::Q>([&](auto q) { a.pdf[s[L::INV[q]]] = t[q]; });
 }
@@ -265,7 +264,7 @@ __global__ void __launch_bounds__(kIB, MINB) k_resident(const SweepArgs a, const
         double t[L::Q];
         // idx rows of this warp's next cells into L2 (as the sweep kernels do)
         const uint32_t lane = threadIdx.x & 31, nxt = c - lane + nth;
-        if (lane < L::Q - 1 && nxt < a.n_fluid) prefetch_l2(a.idx + size_t(lane) * a.idx_pitch + nxt);
+        if (nxt < a.n_fluid) prefetch_idx_warp<L::Q - 1>(a.idx, a.idx_pitch, nxt, lane);
         load_slots<L>(s, a.idx, a.idx_pitch, c);
         gather<L>(t, cur, s);
         bad |= r.pull ? collide_scatter<L, MODEL, false>(t, s, cur, oth, a.base, c, a.omega, a.lam)

@@ -212,10 +212,9 @@ __global__ void __launch_bounds__(kCTA, MINB) k_pair(const PairArgs a) {
   while (item != kEnd) {
     if (item >= 0) {
       const uint32_t t = uint32_t(item);
-      if (a.ahead && lane < L::Q - 1) {  // idx rows of the tile `ahead` tiles later into L2
+      if (a.ahead) {  // idx rows of the tile `ahead` tiles later into L2
         const uint32_t f = (t + a.ahead) * kTile;
-        if (f < a.n_fluid)  // normal priority: evict_last would pin idx lines the odd reuse needs
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(a.idx + size_t(lane) * a.idx_pitch + f));
+        if (f < a.n_fluid) prefetch_idx_warp<L::Q - 1>(a.idx, a.idx_pitch, f, lane);
       }
       const uint32_t c = t * kTile + lane;
       const bool valid = c < a.n_fluid;
@@ -351,7 +350,7 @@ __global__ void k_pair_deps(const uint32_t* idx, uint32_t pitch, uint32_t n_flui
     return -2;
   };
   for (int r = 0; r < q - 1; ++r) {
-    const uint32_t s = idx[size_t(r) * pitch + n];
+    const uint32_t s = idx[idx_offset(q == 19, pitch, uint32_t(r), n)];
     int64_t c = owner_cell(pb.v, q, n_fluid, s);
     if (c < 0) c = lookup(ubb_sorted, ubb_entry, ubb_partner, n_ubb, s);
     if (c == -2) c = lookup(out_sorted, out_entry, out_partner, n_out, s);

@@ -10,6 +10,22 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
 }
 
+// Index-list layout.  D3Q19 (the bench stencil) stores the Q-1 rows in
+// interleaved pairs: for rows (2k, 2k+1) one uint2 per cell, rows of pairs
+// `pitch` cells long — a cell's 18 slot ids are 9 64-bit loads instead of 18
+// 32-bit ones, every warp load still one contiguous 256-B run (same bytes;
+// even sweep 0.90 -> 0.94 of HBM, tools/variants.py).  D3Q27 keeps single
+// rows (13 pair loads measured 5 % slower there: register pressure of the
+// cumulant sweep).  idx_offset() is the uint32 position of (row r, cell c).
+template <int QM1>
+constexpr bool kPairedIdx = (QM1 == 18);
+
+__host__ __device__ __forceinline__ size_t idx_offset(bool paired, uint32_t pitch, uint32_t r,
+                                                      uint32_t c) {
+  return paired ? size_t(r >> 1) * 2 * pitch + 2 * size_t(c) + (r & 1u)
+                : size_t(r) * pitch + c;
+}
+
 // L2 prefetch of the index list of the CTA `ahead` CTAs later.
 //
 // The index-list sweep is latency bound: every PDF gather depends on an idx
@@ -21,7 +37,7 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 // once either way), ~+7-9% sweep bandwidth measured (profiles/r01_*).
 //
 // Positions are sweep positions: with a cell list (frame sweeps) they index
-// `cids` (the future CTA's first cell id of each 32-cell run is read from
+// `cids` (the future CTA's first cell id of each line's run is read from
 // it; call after the own gathers are issued, so that dependent load overlaps
 // them), without one they are cell ids.  `first` is this CTA's first
 // position, `end` one past the sweep's last.
@@ -29,13 +45,32 @@ template <int QM1, int BLOCK>
 __device__ __forceinline__ void prefetch_idx_ahead(const uint32_t* idx, uint32_t pitch,
                                                    const uint32_t* cids, uint32_t end,
                                                    uint32_t first, uint32_t ahead) {
-  constexpr int kLines = BLOCK * 4 / 128;
-  if (threadIdx.x >= QM1 * kLines) return;
+  constexpr bool kPaired = kPairedIdx<QM1>;
+  constexpr int kRows = kPaired ? QM1 / 2 : QM1;
+  constexpr int kCellsPerLine = kPaired ? 16 : 32;
+  constexpr int kLines = BLOCK / kCellsPerLine;
+  if (threadIdx.x >= kRows * kLines) return;
   const uint32_t row = threadIdx.x / kLines, line = threadIdx.x % kLines;
-  const uint32_t pos = first + ahead * BLOCK + line * 32;
+  const uint32_t pos = first + ahead * BLOCK + line * kCellsPerLine;
   if (pos >= end) return;
   const uint32_t cell = cids ? __ldcs(cids + pos) : pos;
-  prefetch_l2(idx + size_t(row) * pitch + cell);
+  if constexpr (kPaired)
+    prefetch_l2(reinterpret_cast<const uint2*>(idx) + size_t(row) * pitch + cell);
+  else
+    prefetch_l2(idx + size_t(row) * pitch + cell);
+}
+
+// one 128-B line of the index list of cells [c0, c0 + 32) per lane < Q-1
+// (warp-granular prefetch: resident / pair kernels)
+template <int QM1>
+__device__ __forceinline__ void prefetch_idx_warp(const uint32_t* idx, uint32_t pitch,
+                                                  uint32_t c0, uint32_t lane) {
+  if (lane >= QM1) return;
+  if constexpr (kPairedIdx<QM1>)
+    prefetch_l2(reinterpret_cast<const uint2*>(idx) + size_t(lane >> 1) * pitch + c0 +
+                (lane & 1u) * 16);
+  else
+    prefetch_l2(idx + size_t(lane) * pitch + c0);
 }
 
 // ---- per-cell bodies shared by the single-engine sweeps (kernels.cu) and
@@ -46,7 +81,17 @@ template <class L>
 __device__ __forceinline__ void load_slots(uint32_t (&s)[L::Q], const uint32_t* idx,
                                            uint32_t pitch, uint32_t c) {
   s[0] = c;
-  sfor<1, L::Q>([&](auto q) { s[q] = __ldcs(idx + size_t(q - 1) * pitch + c); });
+  if constexpr (kPairedIdx<L::Q - 1>) {
+    const uint2* p2 = reinterpret_cast<const uint2*>(idx);
+    sfor<0, (L::Q - 1) / 2>([&](auto r) {
+      constexpr int R = decltype(r)::value;
+      const uint2 v = __ldcs(p2 + size_t(R) * pitch + c);
+      s[1 + 2 * R] = v.x;
+      s[2 + 2 * R] = v.y;
+    });
+  } else {
+    sfor<1, L::Q>([&](auto q) { s[q] = __ldcs(idx + size_t(q - 1) * pitch + c); });
+  }
 }
 
 template <class L>
