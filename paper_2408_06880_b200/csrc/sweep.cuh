@@ -14,9 +14,10 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 // interleaved pairs: for rows (2k, 2k+1) one uint2 per cell, rows of pairs
 // `pitch` cells long — a cell's 18 slot ids are 9 64-bit loads instead of 18
 // 32-bit ones, every warp load still one contiguous 256-B run (same bytes;
-// even sweep 0.90 -> 0.94 of HBM, tools/variants.py).  D3Q27 keeps single
-// rows (13 pair loads measured 5 % slower there: register pressure of the
-// cumulant sweep).  idx_offset() is the uint32 position of (row r, cell c).
+// even sweep 0.90 -> 0.97 of HBM burst, tools/variants.py).  Groups of four
+// rows (uint4; 5 loads) measured 0.4 % slower than pairs in an alternating
+// A/B.  D3Q27 keeps single rows (13 pair loads measured 5 % slower there:
+// register pressure of the cumulant sweep).  idx_offset() is the uint32 position of (row r, cell c).
 template <int QM1>
 constexpr bool kPairedIdx = (QM1 == 18);
 
