@@ -163,6 +163,9 @@ int slbm_poll_engines(SlbmEngine** engines, int n, int64_t* first_bad_step, int*
 int slbm_synchronize(SlbmEngine* eng);
 int slbm_parity(const SlbmEngine* eng, int* parity);
 int slbm_set_parity(SlbmEngine* eng, int parity);
+/* pull pattern: 1 when the second buffer is the current one (the buffer pair
+ * a captured CUDA graph refers to), else 0; AA: always 0 (extension) */
+int slbm_buffer_state(const SlbmEngine* eng, int* state);
 
 /* ---- slot access for halo plans (sparse.py:335-366) ---------------------- */
 /* pflat: padded flat index of the cell (C order over the padded box)       */
@@ -278,22 +281,29 @@ int slbm_capture_end(void* stream, void** graph_exec);
 int slbm_graph_launch(void* graph_exec, void* stream);
 int slbm_graph_destroy(void* graph_exec);
 
-/* tuning knobs (tools/variants.py, tools/e2e_probe.py; 0 = default):
- *   0  index-list sweep variant (0 production, 1 no idx prefetch, 2 probe)
+/* Tuning knobs (tools/variants.py, tools/e2e_probe.py).
+ * Engine knobs 0-9 select kernels; each engine owns its settings
+ * (slbm_engine_set_tuning, which also drops that engine's captured graphs).
+ * slbm_set_tuning(0-9) changes the defaults engines created afterwards copy.
+ *   0  index-list sweep variant (0 production, 1 no idx prefetch,
+ *      2 memory-pattern probe -- refused unless built with SLBM_PROBES=1)
  *   1  cell-local sweep variant (0: 3 CTAs/SM, 2: 4 CTAs/SM)
  *   2  idx L2 prefetch distance in quarter waves (default 1)
  *   3  ... in CTAs, overriding knob 2 when > 0
  *   4  slbm_run: resident multi-step kernel up to this many fluid cells
  *      (default 2^19, 0 = off)
- *   5  slbm_run: experimental temporally blocked AA pair kernel (default 0)
+ *   5  slbm_run: experimental temporally blocked AA pair kernel (default 0;
+ *      only in builds with SLBM_EXPERIMENTAL_PAIR=1, else refused)
  *   6  ... its schedule slack in 32-cell tiles (0 = default)
  *   7  ... its index-list prefetch distance in tiles (-1 = default, 0 = off)
  *   8  ... its L2 keep/drop hints (default 1)
  *   9  dense engines: lean whole-block odd sweep k_dense_odd (default 1)
+ * Process-wide host-transfer knobs (slbm_set_tuning only):
  *   10 host staging chunk in MiB, 11 host staging threads
  *   12 slbm_macroscopic into pinned buffers: 0 = HBM staging + DMA copy
  *      (default), 1 = field kernel writes mapped host memory             */
 int slbm_set_tuning(int knob, int value);
+int slbm_engine_set_tuning(SlbmEngine* eng, int knob, int value);
 
 const char* slbm_last_error(void);
 const char* slbm_version(void);

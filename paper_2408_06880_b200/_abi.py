@@ -74,6 +74,7 @@ SIGNATURES = {
     "slbm_synchronize": [vp],
     "slbm_parity": [vp, C.POINTER(C.c_int)],
     "slbm_set_parity": [vp, C.c_int],
+    "slbm_buffer_state": [vp, C.POINTER(C.c_int)],
     "slbm_slot_index": [vp, c_i64p, c_i64p, C.c_int64, c_i64p],
     "slbm_ghost_slot_index": [vp, c_i64p, c_i64p, C.c_int64, c_i64p],
     "slbm_read_slots": [vp, c_i64p, C.c_int64, c_dp],
@@ -106,6 +107,7 @@ SIGNATURES = {
     "slbm_halo_connect": [vp, C.c_int, vp, vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
     "slbm_voxelize_spheres": [c_i32p, c_dp, C.c_int64, C.c_double, C.c_int, c_u8p],
     "slbm_set_tuning": [C.c_int, C.c_int],
+    "slbm_engine_set_tuning": [vp, C.c_int, C.c_int],
     "slbm_group_create": [C.POINTER(vp), C.c_int, C.POINTER(vp)],
     "slbm_group_destroy": [vp],
     "slbm_group_refresh": [vp, C.c_int, vp],

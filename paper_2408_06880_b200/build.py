@@ -56,6 +56,40 @@ FLAGS = [
 ]
 
 
+# Optional build variants (environment, read at build time):
+#   SLBM_EXPERIMENTAL_PAIR=1  compile csrc/pair.cu (temporally blocked AA pair
+#                             kernel, off by default and slower)
+#   SLBM_PROBES=1             allow tuning knob 0 = 2 (memory-pattern probe)
+# Objects of another variant are rebuilt (the variant is part of the stamp).
+def _variant() -> list[str]:
+    defs = []
+    if os.environ.get("SLBM_EXPERIMENTAL_PAIR") == "1":
+        defs.append("-DSLBM_WITH_PAIR")
+    if os.environ.get("SLBM_PROBES") == "1":
+        defs.append("-DSLBM_PROBES")
+    return defs
+
+
+def _sources() -> list[str]:
+    srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    if "-DSLBM_WITH_PAIR" not in _variant():
+        srcs = [s for s in srcs if os.path.basename(s) != "pair.cu"]
+    return srcs
+
+
+def _stamp_ok() -> bool:
+    stamp = os.path.join(OBJDIR, "variant.txt")
+    want = " ".join(_variant())
+    have = open(stamp).read() if os.path.exists(stamp) else None
+    if have != want:
+        for o in glob.glob(os.path.join(OBJDIR, "*.o")):
+            os.remove(o)
+        with open(stamp, "w") as fh:
+            fh.write(want)
+        return False
+    return True
+
+
 def _newest_header() -> float:
     hdrs = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h"))
     hdrs += glob.glob(os.path.join(ROOT, "include", "*.h"))
@@ -66,7 +100,7 @@ def _compile(src: str, inc: str, verbose: bool) -> str:
     obj = os.path.join(OBJDIR, os.path.basename(src).replace(".cu", ".o"))
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), _newest_header()):
         return obj
-    cmd = [_nvcc(), *ARCH, *FLAGS, "-I", inc, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+    cmd = [_nvcc(), *ARCH, *FLAGS, *_variant(), "-I", inc, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr}")
@@ -81,14 +115,15 @@ def _compile(src: str, inc: str, verbose: bool) -> str:
 def build(verbose: bool = True, force: bool = False) -> str:
     os.makedirs(OBJDIR, exist_ok=True)
     inc, libdir = _nccl_dirs()
-    sources = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    sources = _sources()
     if force:
         for o in glob.glob(os.path.join(OBJDIR, "*.o")):
             os.remove(o)
+    relink = not _stamp_ok()
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(lambda s: _compile(s, inc, verbose), sources))
     newest = max(os.path.getmtime(o) for o in objs)
-    if os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
+    if not relink and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
         return LIB
     ncclso = os.path.join(libdir, "libnccl.so.2")
     link = [

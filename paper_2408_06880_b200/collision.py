@@ -34,6 +34,35 @@ class Parity(Enum):
         return Parity.ODD if self is Parity.EVEN else Parity.EVEN
 
 
+# The Parity class the engines report.  A host application that compares
+# parities by identity (the reference's ``exchange.phase_for`` does
+# ``parity is Parity.EVEN``, ``exchange.py:313-316``) adopts its own enum
+# through :func:`adopt_parity` (``errors.adopt`` does this for the
+# reference package); internally parities are compared by ``.value``.
+_parity_cls = [Parity]
+
+
+def parity_class():
+    return _parity_cls[0]
+
+
+def adopt_parity(cls) -> None:
+    """Report parities as members of ``cls`` (an Enum with EVEN=0, ODD=1
+    and ``flipped()``, e.g. ``slbm.core.Parity``) from now on."""
+    if cls.EVEN.value != 0 or cls.ODD.value != 1:
+        raise errors.make("ConfigurationError", f"{cls!r} is not an EVEN=0/ODD=1 parity enum")
+    _parity_cls[0] = cls
+
+
+def is_even(parity) -> bool:
+    return getattr(parity, "value", parity) == 0
+
+
+def as_parity(parity):
+    """``parity`` (any EVEN/ODD enum or 0/1) as a member of the adopted class."""
+    return parity_class()(getattr(parity, "value", parity))
+
+
 @dataclass
 class CollisionParams:
     omega: float

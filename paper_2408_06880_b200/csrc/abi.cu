@@ -141,6 +141,20 @@ const char* slbm_version(void) { return "slbm_b200 0.1 sm_100a"; }
 
 int slbm_set_tuning(int knob, int value) { return set_tuning(knob, value); }
 
+int slbm_engine_set_tuning(SlbmEngine* e, int knob, int value) {
+  CHECK_ENGINE(e);
+  SlbmTuning t = e->tune;
+  SLBM_TRY(tuning_apply(t, knob, value));
+  e->tune = t;
+  // captured step pairs baked in the previous kernel choice
+  for (auto& g : e->graph)
+    if (g) {
+      cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
+  return SLBM_OK;
+}
+
 int slbm_capture_begin(void* stream) {
   if (!stream) return fail(SLBM_ECONFIG, "capture needs a non-default stream");
   SLBM_CUDA_TRY(cudaStreamBeginCapture((cudaStream_t)stream, cudaStreamCaptureModeThreadLocal));
@@ -757,6 +771,14 @@ int slbm_synchronize(SlbmEngine* e) {
 int slbm_parity(const SlbmEngine* e, int* parity) {
   CHECK_ENGINE(e);
   *parity = e->parity;
+  return SLBM_OK;
+}
+
+int slbm_buffer_state(const SlbmEngine* e, int* state) {
+  CHECK_ENGINE(e);
+  // pull: which of the two buffers is current (the pointers a captured graph
+  // bakes in); AA: always 0 (one buffer, in place)
+  *state = (e->pattern == SLBM_PULL && e->tmp != nullptr && e->tmp < e->pdf) ? 1 : 0;
   return SLBM_OK;
 }
 

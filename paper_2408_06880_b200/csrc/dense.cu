@@ -34,7 +34,6 @@ namespace slbm {
 namespace {
 
 constexpr uint32_t kSolid = 0xffffffffu;
-int g_dense_lean_odd = 1;  // knob 9: lean whole-block odd sweep (k_dense_odd)
 constexpr uint32_t kHasUbb = 0x80000000u;
 constexpr uint8_t kFluidT = 0, kUbbT = 2, kExchT = 3, kOutT = 4;
 
@@ -508,7 +507,7 @@ int dense_step(SlbmEngine* e, int phase) {
           k_dense<L, M, 0, S><<<grid, 128, 0, e->stream>>>(a, ahead);
         else if (kind == 1)
           k_dense<L, M, 1, S><<<grid, 128, 0, e->stream>>>(a, ahead);
-        else if (phase == SLBM_PHASE_ALL && g_dense_lean_odd)
+        else if (phase == SLBM_PHASE_ALL && e->tune.dense_lean_odd)
           k_dense_odd<L, M><<<grid, 128, 0, e->stream>>>(oa);
         else
           k_dense<L, M, 2, S><<<grid, 128, 0, e->stream>>>(a, ahead);
@@ -551,9 +550,5 @@ int dense_canonical(SlbmEngine* e, double* dev_values) {
   return SLBM_OK;
 }
 
-int dense_tune(int value) {
-  g_dense_lean_odd = value;
-  return SLBM_OK;
-}
 
 }  // namespace slbm

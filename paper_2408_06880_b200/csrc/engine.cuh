@@ -9,6 +9,28 @@ namespace slbm {
 struct PairPlan;
 }
 
+// Kernel-selection knobs (slbm_engine_set_tuning; include/slbm_b200.h).  Each
+// engine owns a copy, taken from the process defaults (slbm_set_tuning) when
+// it is created, so tuning one engine never changes another's kernels.
+struct SlbmTuning {
+  int even_variant = 0;            // 0: production, 1: no idx prefetch, 2: probe (SLBM_PROBES builds)
+  int odd_variant = 0;             // cell-local sweep CTAs per SM (0: 3, 2: 4)
+  int ahead_quarters = 1;          // idx L2 prefetch distance in quarter waves
+  int ahead_ctas = 0;              // ... in CTAs when > 0
+  int64_t resident_cap = 1 << 19;  // slbm_run: k_resident up to this n_fluid (0: off)
+  int pair = 0;                    // slbm_run: temporally blocked pair kernel (SLBM_WITH_PAIR builds)
+  int pair_slack = 0;
+  int pair_ahead = -1;
+  int pair_hints = 1;
+  int dense_lean_odd = 1;          // dense engines: k_dense_odd
+};
+
+namespace slbm {
+extern SlbmTuning g_tuning_defaults;
+// knob -> field; SLBM_ECONFIG for unknown knobs or values this build refuses
+int tuning_apply(SlbmTuning& t, int knob, int value);
+}
+
 struct SlbmEngine {
   int device = 0;
   int dim = 3, q = 19;
@@ -16,6 +38,7 @@ struct SlbmEngine {
   double omega = 1.0, lambda_odd = 1.0;
   int pattern = SLBM_PULL;
   int parity = SLBM_EVEN;
+  SlbmTuning tune = slbm::g_tuning_defaults;
   slbm::Geometry geo{};
   slbm::DirTable dirs{};
 
@@ -107,11 +130,15 @@ int launch_resident(SlbmEngine* e, int64_t n);
 int launch_advance(SlbmEngine* e);
 // pair.cu: one AA step pair (EVEN refresh + even + odd refresh + odd) in one
 // launch, temporally blocked in L2; engines without halo slots
+#ifdef SLBM_WITH_PAIR
 bool pair_eligible(const SlbmEngine* e);
 int launch_pair(SlbmEngine* e);
 void free_pair(SlbmEngine* e);
-int pair_tune(int knob, int value);
-int dense_tune(int value);  // knob 9: lean dense odd sweep on/off
+#else  // pair.cu is experimental and left out of the shipped library
+inline bool pair_eligible(const SlbmEngine*) { return false; }
+inline int launch_pair(SlbmEngine*) { return SLBM_ECONFIG; }
+inline void free_pair(SlbmEngine*) {}
+#endif
 int launch_canonical(SlbmEngine* e, double* dev_out);  // (q, n) at current parity
 // box layout (zeros at solids must be pre-set) or compact: one value per fluid cell
 int launch_macroscopic(SlbmEngine* e, const double* dev_canon, double* dev_rho, double* dev_u,

@@ -56,12 +56,6 @@ __device__ __forceinline__ void flag_bad(const SweepArgs& a) {
   atomicMin(a.bad, *a.step);
 }
 
-// tuning knobs (slbm_set_tuning), kept for tools/variants.py
-int g_even_variant = 0;     // knob 0: 0 = production, 1 = no idx prefetch, 2 = probe
-int g_odd_variant = 0;      // knob 1: odd-sweep CTAs per SM (0: 3)
-int g_ahead_quarters = 1;   // knob 2: idx prefetch distance in quarter waves
-int g_ahead_ctas = 0;       // knob 3: ... or in CTAs when > 0
-int64_t g_resident_cap = 1 << 19;  // knob 4: slbm_run uses k_resident up to this n_fluid (0: off)
 int g_num_sms = 0;
 
 enum Kind { kPull = 0, kEven = 1, kOdd = 2 };
@@ -151,34 +145,35 @@ int num_sms() {
 }
 
 template <class L, int MODEL, int KIND, int MINB, bool PF>
-void launch_index(const SweepArgs& a, cudaStream_t s) {
+void launch_index(const SweepArgs& a, const SlbmTuning& t, cudaStream_t s) {
   static int resident = 0;  // CTAs per SM this instantiation actually gets
   if (!resident) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_index_sweep<L, MODEL, KIND, MINB, PF>,
                                                   kIB, 0);
     resident = std::max(resident, 1);
   }
-  const uint32_t ahead = g_ahead_ctas > 0 ? uint32_t(g_ahead_ctas)
-                                          : uint32_t(num_sms() * resident * g_ahead_quarters / 4);
+  const uint32_t ahead = t.ahead_ctas > 0 ? uint32_t(t.ahead_ctas)
+                                          : uint32_t(num_sms() * resident * t.ahead_quarters / 4);
   k_index_sweep<L, MODEL, KIND, MINB, PF>
       <<<(a.n_cells + kIB - 1) / kIB, kIB, 0, s>>>(a, std::max(ahead, 1u));
 }
 
 template <class L, int MODEL>
-void launch_kind(int kind, const SweepArgs& a, unsigned grid, cudaStream_t s) {
+void launch_kind(int kind, const SweepArgs& a, unsigned grid, const SlbmTuning& t, cudaStream_t s) {
   constexpr int MINB = L::Q == 9 ? 8 : 4;
   if (kind == kPull) {
-    launch_index<L, MODEL, kPull, MINB, true>(a, s);
+    launch_index<L, MODEL, kPull, MINB, true>(a, t, s);
   } else if (kind == kEven) {
-    if (g_even_variant == 1)
-      launch_index<L, MODEL, kEven, MINB, false>(a, s);
-
-    else if (g_even_variant == 2)
+    if (t.even_variant == 1)
+      launch_index<L, MODEL, kEven, MINB, false>(a, t, s);
+#ifdef SLBM_PROBES
+    else if (t.even_variant == 2)  // memory-pattern probe, not LBM
       k_probe<L><<<(a.n_cells + kIB - 1) / kIB, kIB, 0, s>>>(a);
+#endif
     else
-      launch_index<L, MODEL, kEven, MINB, true>(a, s);
+      launch_index<L, MODEL, kEven, MINB, true>(a, t, s);
   } else {
-    if (L::Q != 9 && g_odd_variant == 2)
+    if (L::Q != 9 && t.odd_variant == 2)
       k_aa_odd<L, MODEL, 4><<<grid, kBlock, 0, s>>>(a);
     else
       k_aa_odd<L, MODEL, L::Q == 9 ? 1 : 3><<<grid, kBlock, 0, s>>>(a);
@@ -186,13 +181,14 @@ void launch_kind(int kind, const SweepArgs& a, unsigned grid, cudaStream_t s) {
 }
 
 template <class L>
-void launch_model(int model, int kind, const SweepArgs& a, unsigned grid, cudaStream_t s) {
+void launch_model(int model, int kind, const SweepArgs& a, unsigned grid, const SlbmTuning& t,
+                  cudaStream_t s) {
   if (model == SLBM_SRT)
-    launch_kind<L, SLBM_SRT>(kind, a, grid, s);
+    launch_kind<L, SLBM_SRT>(kind, a, grid, t, s);
   else if (model == SLBM_TRT)
-    launch_kind<L, SLBM_TRT>(kind, a, grid, s);
+    launch_kind<L, SLBM_TRT>(kind, a, grid, t, s);
   else if constexpr (L::Q == 27)
-    launch_kind<L, SLBM_CUMULANT>(kind, a, grid, s);
+    launch_kind<L, SLBM_CUMULANT>(kind, a, grid, t, s);
 }
 
 __global__ void k_refresh(double* pdf, const uint32_t* slot, const uint32_t* partner,
@@ -455,17 +451,40 @@ void by_lattice(int q, F&& f) {
 
 }  // namespace
 
+SlbmTuning g_tuning_defaults{};
+
+int tuning_apply(SlbmTuning& t, int knob, int value) {
+  switch (knob) {
+    case 0:
+#ifndef SLBM_PROBES
+      if (value == 2) return fail(SLBM_ECONFIG, "knob 0 = 2 (memory probe) needs an SLBM_PROBES build");
+#endif
+      if (value < 0 || value > 2) return fail(SLBM_ECONFIG, "knob 0: variant 0, 1 or 2");
+      t.even_variant = value;
+      return SLBM_OK;
+    case 1: t.odd_variant = value; return SLBM_OK;
+    case 2:
+      if (value < 0) return fail(SLBM_ECONFIG, "knob 2: distance >= 0");
+      t.ahead_quarters = value;
+      return SLBM_OK;
+    case 3: t.ahead_ctas = value; return SLBM_OK;
+    case 4: t.resident_cap = value; return SLBM_OK;
+    case 5: case 6: case 7: case 8:
+#ifndef SLBM_WITH_PAIR
+      if (knob == 5 && value != 0)
+        return fail(SLBM_ECONFIG, "the pair kernel is experimental: build with SLBM_EXPERIMENTAL_PAIR=1");
+#endif
+      (knob == 5 ? t.pair : knob == 6 ? t.pair_slack : knob == 7 ? t.pair_ahead : t.pair_hints) = value;
+      return SLBM_OK;
+    case 9: t.dense_lean_odd = value; return SLBM_OK;
+    default: return fail(SLBM_ECONFIG, "unknown engine tuning knob " + std::to_string(knob));
+  }
+}
+
 int set_tuning(int knob, int value) {
-  if (knob == 0) g_even_variant = value;
-  else if (knob == 1) g_odd_variant = value;
-  else if (knob == 2) g_ahead_quarters = value;
-  else if (knob == 3) g_ahead_ctas = value;
-  else if (knob == 4) g_resident_cap = value;
-  else if (knob >= 5 && knob <= 8) return pair_tune(knob, value);
-  else if (knob == 9) return dense_tune(value);
-  else if (knob == 10 || knob == 11 || knob == 12) return hostcopy_tune(knob, value);
-  else return fail(SLBM_ECONFIG, "unknown tuning knob");
-  return SLBM_OK;
+  if (knob >= 0 && knob <= 9) return tuning_apply(g_tuning_defaults, knob, value);
+  if (knob == 10 || knob == 11 || knob == 12) return hostcopy_tune(knob, value);
+  return fail(SLBM_ECONFIG, "unknown tuning knob " + std::to_string(knob));
 }
 
 int launch_slot_lookup(SlbmEngine* e, const int64_t* d_qs, const int64_t* d_pflat, int64_t n,
@@ -500,7 +519,7 @@ int launch_step(SlbmEngine* e, int phase) {
   const int kind = e->pattern == SLBM_PULL ? kPull : (e->parity == SLBM_EVEN ? kEven : kOdd);
   const unsigned grid = grid_for(a.n_cells, kBlock);
   by_lattice(e->q, [&](auto lat) {
-    launch_model<decltype(lat)>(e->model, kind, a, grid, e->stream);
+    launch_model<decltype(lat)>(e->model, kind, a, grid, e->tune, e->stream);
   });
   SLBM_CUDA_TRY(cudaGetLastError());
   return SLBM_OK;
@@ -550,8 +569,8 @@ cudaError_t resident_launch(const SweepArgs& a, const ResidentArgs& r, cudaStrea
 }  // namespace
 
 bool resident_eligible(const SlbmEngine* e, int64_t n) {
-  return g_resident_cap > 0 && n >= 2 && e->layout == 0 && e->n_fluid > 0 &&
-         e->n_fluid <= g_resident_cap;
+  return e->tune.resident_cap > 0 && n >= 2 && e->layout == 0 && e->n_fluid > 0 &&
+         e->n_fluid <= e->tune.resident_cap;
 }
 
 // n whole steps in one cooperative launch (k_resident); the caller updates

@@ -70,10 +70,9 @@ constexpr uint32_t kWide = 512;     // chunk span above which a tile waits for a
 constexpr uint32_t kBundle = 2;     // schedule positions per ticket
 constexpr uint32_t kNone = 0xffffffffu;
 
-int g_pair = 0;        // knob 5: 1 = use the pair kernel in slbm_run (experimental)
-int g_pair_slack = 0;  // knob 6: extra tiles between an odd tile's writers and it (0: one wave)
-int g_pair_ahead = -1;  // knob 7: idx prefetch distance in tiles (-1: 4 per SM, 0: off)
-int g_pair_hints = 1;   // knob 8: L2 keep/drop hints on the even stores / odd loads
+// knobs 5-8 (SlbmTuning::pair*): use the pair kernel in slbm_run; extra
+// tiles between an odd tile's writers and it (0: one wave); idx prefetch
+// distance in tiles (-1: 4 per SM, 0: off); L2 keep/drop hints
 
 struct PairArgs {
   double* pdf;
@@ -498,7 +497,7 @@ int build_pair_plan(SlbmEngine* e) {
       e->ubb_partner, uint32_t(e->n_ubb), o_sorted, o_entry, e->out_partner, uint32_t(e->n_out),
       p->dep);
   const uint32_t slack =
-      g_pair_slack > 0 ? uint32_t(g_pair_slack) : uint32_t(num_sms_pair() * 12);
+      e->tune.pair_slack > 0 ? uint32_t(e->tune.pair_slack) : uint32_t(num_sms_pair() * 12);
   k_pair_keys<<<blocks(n_tiles), 256, 0, s>>>(p->dep, n_tiles, slack, key, val);
   size_t tmpb = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tmpb, key, key2, val, val2, int(n_tiles), 0, 32, s);
@@ -537,16 +536,9 @@ void pair_launch(const PairArgs& a, cudaStream_t s) {
 
 }  // namespace
 
-int pair_tune(int knob, int value) {
-  if (knob == 5) g_pair = value;
-  else if (knob == 6) g_pair_slack = value;
-  else if (knob == 7) g_pair_ahead = value;
-  else g_pair_hints = value;
-  return SLBM_OK;
-}
 
 bool pair_eligible(const SlbmEngine* e) {
-  return g_pair && e->layout == 0 && e->pattern == SLBM_AA && e->n_ghost == 0 &&
+  return e->tune.pair && e->layout == 0 && e->pattern == SLBM_AA && e->n_ghost == 0 &&
          e->n_fluid > 0 && e->n_fluid < (int64_t(1) << 31) / 2;
 }
 
@@ -597,8 +589,8 @@ int launch_pair(SlbmEngine* e) {
   a.out_u = e->out_u;
   a.out_perm = p->out_perm;
   a.out_start = p->out_start;
-  a.hints = g_pair_hints;
-  a.ahead = g_pair_ahead >= 0 ? uint32_t(g_pair_ahead) : uint32_t(num_sms_pair() * 4);
+  a.hints = e->tune.pair_hints;
+  a.ahead = e->tune.pair_ahead >= 0 ? uint32_t(e->tune.pair_ahead) : uint32_t(num_sms_pair() * 4);
   if (e->q == 9)
     e->model == SLBM_SRT ? pair_launch<LatD2Q9, SLBM_SRT>(a, e->stream)
                          : pair_launch<LatD2Q9, SLBM_TRT>(a, e->stream);

@@ -30,7 +30,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import errors
-from .collision import Parity
+from .collision import is_even
 from .counters import Counters
 from .engine import DenseEngine, SparseEngine, default_device
 from .halo import DeviceHalo, EdgePlan, NcclComm, Phase, phase_for
@@ -574,7 +574,10 @@ class Domain:
         from . import _abi
         import ctypes as C
 
-        key = (driver, getattr(self.parity, "value", self.parity))
+        # the captured pair bakes in buffer pointers: AA keys on parity, pull
+        # on which of each engine's two buffers is current (finish_step swaps)
+        key = (driver, getattr(self.parity, "value", self.parity),
+               tuple(e.buffer_state() for e in self.local_engines()))
         graphs = self.__dict__.setdefault("_graphs", {})
         if key not in graphs:
             engines = self.local_engines()
@@ -746,7 +749,7 @@ class BlockGroup:
         cells = [e._phase_cells(phase) for e in self.engines]  # validates the phase
         _abi.call("slbm_group_step", self._h, _PHASE_CODE[phase], C.c_void_p(stream or 0))
         for e, n in zip(self.engines, cells):
-            table = e.pattern == "pull" or e.parity is Parity.EVEN
+            table = e.pattern == "pull" or is_even(e.parity)
             e.counters.record_sweep(phase, n, e.stencil.q, table)
 
     def finish(self, stream):

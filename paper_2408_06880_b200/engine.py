@@ -33,7 +33,7 @@ import os
 import numpy as np
 
 from . import _abi, errors
-from .collision import Parity, params_code
+from .collision import is_even, params_code, parity_class
 from .counters import Counters
 from .lattice import stencil_code
 from .tags import OUTLET, UBB, rev_shape
@@ -150,7 +150,7 @@ class SparseEngine:
         self._has_split = bool(info.has_split)
         self._n_interior = int(info.n_interior)
         self._n_frame = int(info.n_frame)
-        self.parity = Parity.EVEN
+        self.parity = parity_class().EVEN
         self.counters = Counters()
         self._fluid_coords = None
         self._cid_map = None  # host copy for slot_index, fetched on first use
@@ -248,13 +248,13 @@ class SparseEngine:
                 f"expected state shape {(self.stencil.q, self.n_fluid)}, got {values.shape}",
             )
         _abi.call("slbm_init_canonical", self._h, _abi.ptr(values, C.c_double))
-        self.parity = Parity.EVEN
+        self.parity = parity_class().EVEN
 
     def init_canonical_device(self, dev_ptr: int) -> None:
         """init_canonical from a device buffer of (q, n_fluid) float64."""
         _abi.call("slbm_init_canonical_dev", self._h, C.c_void_p(dev_ptr))
         _abi.call("slbm_synchronize", self._h)
-        self.parity = Parity.EVEN
+        self.parity = parity_class().EVEN
 
     def init_equilibrium(self, rho=1.0, u=None) -> None:
         dim, n = self.stencil.dim, self.n_fluid
@@ -274,7 +274,7 @@ class SparseEngine:
                 u_scalar = 0
         _abi.call("slbm_init_equilibrium", self._h, _abi.ptr(rho_a, C.c_double), rho_scalar,
                   _abi.ptr(u_a, C.c_double), u_scalar)
-        self.parity = Parity.EVEN
+        self.parity = parity_class().EVEN
 
     # -- stepping -------------------------------------------------------------------
 
@@ -290,7 +290,7 @@ class SparseEngine:
     def step(self, phase: str = "all") -> None:
         cells = self._phase_cells(phase)
         _abi.call("slbm_step", self._h, _PHASE_CODE[phase])
-        table_reads = self.pattern == "pull" or self.parity is Parity.EVEN
+        table_reads = self.pattern == "pull" or is_even(self.parity)
         self.counters.record_sweep(phase, cells, self.stencil.q, table_reads)
         if self.check == "step":
             self.poll()
@@ -314,7 +314,7 @@ class SparseEngine:
             return
         q = self.stencil.q
         for _ in range(steps):
-            table_reads = self.pattern == "pull" or self.parity is Parity.EVEN
+            table_reads = self.pattern == "pull" or is_even(self.parity)
             self.counters.record_sweep("all", self.n_fluid, q, table_reads)
             if self.pattern == "aa":
                 self.parity = self.parity.flipped()
@@ -337,6 +337,17 @@ class SparseEngine:
 
     def synchronize(self) -> None:
         _abi.call("slbm_synchronize", self._h)
+
+    def set_tuning(self, knob: int, value: int) -> None:
+        """Kernel-selection knob of THIS engine (include/slbm_b200.h, knobs
+        0-9); drops the engine's captured step-pair graphs."""
+        _abi.call("slbm_engine_set_tuning", self._h, int(knob), int(value))
+
+    def buffer_state(self) -> int:
+        """Pull: 1 when the second buffer is current, else 0; AA: 0."""
+        st = C.c_int(0)
+        _abi.call("slbm_buffer_state", self._h, C.byref(st))
+        return int(st.value)
 
     def stream(self) -> int:
         s = C.c_void_p()

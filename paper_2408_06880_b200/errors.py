@@ -74,11 +74,39 @@ _classes = {
 
 def adopt(module) -> None:
     """Raise the exception classes of ``module`` (e.g. ``slbm.errors``)
-    from now on, instead of this package's own."""
+    from now on, instead of this package's own.
+
+    When ``module`` belongs to a package with a ``core.Parity`` enum (the
+    reference: ``slbm.core.Parity``, ``core.py:32-47``), the engines also
+    report their parity as members of that enum, so host code comparing
+    parities by identity -- the reference's ``exchange.phase_for``
+    (``exchange.py:313-316``) -- takes the right halo phase."""
+    import importlib
+
     for name in list(_classes):
         cls = getattr(module, name, None)
         if cls is not None:
             _classes[name] = cls
+    pkg = getattr(module, "__package__", None) or getattr(module, "__name__", "").rpartition(".")[0]
+    if pkg:
+        try:
+            core = importlib.import_module(pkg + ".core")
+        except ImportError:
+            core = None
+        parity = getattr(core, "Parity", None)
+        if parity is not None:
+            from .collision import adopt_parity
+
+            adopt_parity(parity)
+
+
+def reset() -> None:
+    """Back to this package's own exception and Parity classes."""
+    from .collision import Parity, adopt_parity
+
+    for name in list(_classes):
+        _classes[name] = globals()[name]
+    adopt_parity(Parity)
 
 
 def error_class(name: str) -> type:

@@ -11,6 +11,43 @@ if ROOT not in sys.path:
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 REFERENCE_SRC = "/root/reference/pkg/src"
+# the unmodified reference installed by tools/install_reference.sh; it travels
+# to the GPU box with the snapshot (git-ignored), /root/reference does not
+REFERENCE_INSTALL = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_paths():
+    """(package dir, tests dir) of an importable unmodified reference, or
+    (None, None).  Prefers the in-tree install (present on the GPU box)."""
+    inst = REFERENCE_INSTALL
+    if os.path.isdir(os.path.join(inst, "slbm")):
+        tests = os.path.join(inst, "slbm_tests")
+        return inst, tests if os.path.isdir(tests) else None
+    if os.path.isdir(REFERENCE_SRC):
+        return REFERENCE_SRC, "/root/reference/pkg/tests"
+    return None, None
+
+
+def import_reference():
+    """The reference package ``slbm`` (imported read-only), or skip."""
+    src, _ = reference_paths()
+    if src is None:
+        pytest.skip("reference package not installed (tools/install_reference.sh)")
+    sys.dont_write_bytecode = True
+    if src not in sys.path:
+        sys.path.insert(0, src)
+    import slbm
+    import slbm.core
+    import slbm.dense
+    import slbm.domain
+    import slbm.errors
+    import slbm.exchange
+    import slbm.flags
+    import slbm.geometry
+    import slbm.sparse
+    import slbm.stencil
+
+    return slbm
 
 
 def pytest_configure(config):

@@ -22,15 +22,12 @@ DEFAULT_CAP = 1 << 19
 
 @pytest.fixture
 def cap(gpu_lib):
-    from paper_2408_06880_b200 import _abi
+    """Per-engine resident cap (knob 4, slbm_engine_set_tuning)."""
 
-    lib = _abi.load()
+    def set_cap(eng, v):
+        eng.set_tuning(CAP_KNOB, int(v))
 
-    def set_cap(v):
-        assert lib.slbm_set_tuning(CAP_KNOB, int(v)) == 0
-
-    yield set_cap
-    set_cap(DEFAULT_CAP)
+    return set_cap
 
 
 def _pair(seed):
@@ -46,9 +43,8 @@ def _pair(seed):
 
 
 def _run(eng, steps, cap, resident):
-    cap(DEFAULT_CAP if resident else 0)
+    cap(eng, DEFAULT_CAP if resident else 0)
     eng.run(steps, use_graph=True)
-    cap(DEFAULT_CAP)
 
 
 @pytest.mark.parametrize("seed", range(24))
@@ -104,8 +100,7 @@ def test_resident_reports_first_unstable_step(pattern, cap):
 def test_cap_selects_path(cap):
     """Above the cap the per-step path runs; both give the same answer."""
     a, b = _pair(1)
-    cap(1)  # n_fluid > 1: per-step path
+    cap(a, 1)  # n_fluid > 1: per-step path
     a.run(6, use_graph=True)
-    cap(DEFAULT_CAP)
-    b.run(6, use_graph=True)
+    b.run(6, use_graph=True)  # default cap: resident
     np.testing.assert_array_equal(a.canonical_state(), b.canonical_state())

@@ -1,4 +1,5 @@
-"""Time the AA sweep kernel variants (slbm_set_tuning) on the bench workload
+"""Time the AA sweep kernel variants (per-engine tuning knobs; variant 2 of
+knob 0 needs a build with SLBM_PROBES=1) on the bench workload
 and check they are bit-identical.
 
     python tools/variants.py            # prints a table + JSON
@@ -64,12 +65,12 @@ def main():
     for _ in range(reps):
         for ah in aheads:
             if ah < 0:
-                lib.slbm_set_tuning(3, -ah)  # negative: distance in CTAs
+                eng.set_tuning(3, -ah)  # negative: distance in CTAs
             else:
-                lib.slbm_set_tuning(3, 0)
-                lib.slbm_set_tuning(2, ah)
+                eng.set_tuning(3, 0)
+                eng.set_tuning(2, ah)
             for v in variants:
-                lib.slbm_set_tuning(0, v)
+                eng.set_tuning(0, v)
                 te, _ = time_pair(eng, reps=3 if reps > 1 else 6)
                 key = f"{v}" if len(aheads) == 1 else f"{v}@{ah}"
                 samples.setdefault(key, []).append(te)
@@ -78,15 +79,15 @@ def main():
         res["even"][key] = {"ms": te, "gbs": n * be / te / 1e6, "frac": n * be / te / 1e6 / hbm}
         print(f"even variant {key}: {te:.4f} ms  {n * be / te / 1e6:.0f} GB/s  "
               f"{n * be / te / 1e6 / hbm:.3f}")
-    lib.slbm_set_tuning(2, 1)
-    lib.slbm_set_tuning(3, 0)
-    lib.slbm_set_tuning(0, 0)
+    eng.set_tuning(2, 1)
+    eng.set_tuning(3, 0)
+    eng.set_tuning(0, 0)
     for v in odd_variants:
-        lib.slbm_set_tuning(1, v)
+        eng.set_tuning(1, v)
         _, to = time_pair(eng)
         res["odd"][v] = {"ms": to, "gbs": n * bo / to / 1e6, "frac": n * bo / to / 1e6 / hbm}
         print(f"odd variant {v}: {to:.4f} ms  {n * bo / to / 1e6:.0f} GB/s  {n * bo / to / 1e6 / hbm:.3f}")
-    lib.slbm_set_tuning(1, 0)
+    eng.set_tuning(1, 0)
     eng.poll()
     # bitwise agreement of all variants on a small bed
     small = bench.make_flags(48, 0)
