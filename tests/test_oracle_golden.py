@@ -14,6 +14,9 @@ from oracle.sparse_ref import OracleInstability, OracleSparseEngine, build_lists
 
 ENGINE = golden_files("engine")
 BED = golden_files("bed")
+# the oracle steps the beds up to C1's 64^3 here; the C2 law at 128^3 / 256^3
+# is pinned on the GPU only (tests/test_gpu_engine.py), the CPU suite stays fast
+BED_CPU = [p for p in BED if int(np.prod(np.load(p)["dims"])) <= 64 ** 3]
 
 
 def _id(p):
@@ -59,7 +62,7 @@ def _sha(a):
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
 
-@pytest.mark.parametrize("path", BED, ids=_id)
+@pytest.mark.parametrize("path", BED_CPU, ids=_id)
 def test_oracle_bed_runs_match_reference(path):
     """C1 (64^3 channel bed, 100 steps) and the C2 law at 48^3: bitwise via
     SHA-256 of the full canonical state."""

@@ -285,5 +285,211 @@ def main():
     print("trt magic lambda", lam316, trt)
 
 
+def _state_digest(prefix, arr, mask_flat, rng, n_sample=4000):
+    """SHA-256 + per-direction fsums + sampled values of a (q,)+box array
+    (zeros at non-fluid cells) at random fluid positions."""
+    import math
+
+    q = arr.shape[0]
+    flat = arr.reshape(q, -1)
+    cells = np.flatnonzero(mask_flat)
+    sq = rng.integers(0, q, n_sample)
+    sc = cells[rng.integers(0, cells.size, n_sample)]
+    return {
+        f"{prefix}_sha": np.array(sha(arr)),
+        f"{prefix}_sums": np.array([math.fsum(r) for r in flat]),
+        f"{prefix}_sample_q": sq,
+        f"{prefix}_sample_cell": sc,
+        f"{prefix}_sample_v": flat[sq, sc],
+    }
+
+
+def config_domain_case(name, fl, block, stname, model, omega, lam, steps, recipe, seed=7,
+                       pattern="aa", driver="overlapped", workers=8):
+    """BASELINE config at reduced scale through the reference's own Domain
+    (domain.py:69-268) and driver (exchange.py:330-374).  ``recipe`` records
+    how the geometry is rebuilt on the GPU box (tests/test_gpu_configs.py);
+    the tag box itself is pinned by its SHA.  Outputs are digests."""
+    import math
+
+    core, domain, exchange, flags, geometry, sparse, stencil = _ref()
+    st = stencil.make_stencil(stname)
+    p = core.CollisionParams(omega=omega, model=model, lambda_odd=lam)
+    d = domain.Domain(fl, block, st, p, pattern=pattern, frame_width=1)
+    d.init_random(seed)
+    rng = np.random.default_rng(12345)
+    mask = (fl.tags[tuple(slice(1, -1) for _ in fl.dims)] == 0).reshape(-1)
+    rec = {
+        "kind": np.array("config_domain"),
+        "stencil": np.array(stname),
+        "model": np.array(model),
+        "omega": np.array(omega),
+        "lambda_odd": np.array(lam if lam is not None else np.nan),
+        "dims": np.array(fl.dims),
+        "periodic": np.array(fl.periodic),
+        "block": np.array(block),
+        "seed": np.array(seed),
+        "steps": np.array(steps),
+        "pattern": np.array(pattern),
+        "driver": np.array(driver),
+        "recipe": np.array(json_dumps(recipe)),
+        "tags_sha": np.array(sha(fl.tags)),
+        "ubb_sha": np.array(sha(np.where((fl.tags == 2)[..., None], fl.ubb_u, 0.0))),
+        "n_fluid": np.array(d.total_fluid()),
+        "blocks": np.array(sorted(d.blocks), dtype=np.int64),
+        "block_fluid": np.array([d.blocks[b].n_fluid for b in sorted(d.blocks)], dtype=np.int64),
+        "n_edges": np.array(len(d.edge_plans)),
+        "edge_wire": np.array([sum(pp.n_wire for pp in pl.phases.values()) for pl in d.edge_plans],
+                              dtype=np.int64),
+    }
+    if workers and len(d.blocks) > 1:
+        asg = d.balance(workers)
+        rec["balance_bids"] = np.array(sorted(asg), dtype=np.int64)
+        rec["balance_workers"] = np.array([asg[b] for b in sorted(asg)], dtype=np.int64)
+    rec.update(_state_digest("init", d.gather_canonical(), mask, rng))
+    d.run(steps, driver=driver)
+    final = d.gather_canonical()
+    rec.update(_state_digest("final", final, mask, rng))
+    rec["mass"] = np.array(math.fsum(final.ravel()))
+    rho, u = d.gather_macroscopics()
+    rec["rho_sha"] = np.array(sha(rho))
+    rec["u_sha"] = np.array(sha(u))
+    c = d.counters()
+    rec["counters"] = np.array(
+        [c.steps, c.cells_visited, c.cells_visited_interior, c.cells_visited_frame,
+         c.pdf_accesses, c.idx_reads, c.values_exchanged, c.messages], dtype=np.int64)
+    np.savez_compressed(os.path.join(OUT, f"config_{name}.npz"), **rec)
+    print("config", name, "n_fluid", d.total_fluid(), "blocks", len(d.blocks),
+          "edges", len(d.edge_plans), flush=True)
+
+
+def config_engine_case(name, fl, stname, model, omega, lam, steps, recipe, seed=11,
+                       layouts=("sparse", "dense"), patterns=("aa", "pull")):
+    """One block through the reference's SparseEngine / DenseEngine
+    (sparse.py:48-383, dense.py:53-342) with the conftest drive loop."""
+    core, domain, exchange, flags, geometry, sparse, stencil = _ref()
+    from slbm import dense
+
+    st = stencil.make_stencil(stname)
+    p = core.CollisionParams(omega=omega, model=model, lambda_odd=lam)
+    values = seed_values(fl, st, seed, core)
+    rec = {
+        "kind": np.array("config_engine"),
+        "stencil": np.array(stname),
+        "model": np.array(model),
+        "omega": np.array(omega),
+        "lambda_odd": np.array(lam if lam is not None else np.nan),
+        "dims": np.array(fl.dims),
+        "periodic": np.array(fl.periodic),
+        "seed": np.array(seed),
+        "steps": np.array(steps),
+        "recipe": np.array(json_dumps(recipe)),
+        "tags_sha": np.array(sha(fl.tags)),
+        "values0_sha": np.array(sha(values)),
+        "layouts": np.array(list(layouts)),
+        "patterns": np.array(list(patterns)),
+    }
+    first = None
+    for layout in layouts:
+        cls = sparse.SparseEngine if layout == "sparse" else dense.DenseEngine
+        for pattern in patterns:
+            e = cls(fl, st, p, pattern=pattern)
+            if layout == "sparse":
+                rec["n_fluid"] = np.array(e.n_fluid)
+                rec["idx_sha"] = np.array(sha(e.idx))
+                rec["base"] = e.base
+            e.init_canonical(values)
+            drive(e, steps)
+            final = e.canonical_state()
+            rho, u = e.macroscopic_fields()
+            key = f"{layout}_{pattern}"
+            rec[f"{key}_final_sha"] = np.array(sha(final))
+            rec[f"{key}_rho_sha"] = np.array(sha(rho))
+            rec[f"{key}_u_sha"] = np.array(sha(u))
+            rec[f"{key}_counters"] = np.array([e.counters.steps, e.counters.cells_visited,
+                                               e.counters.pdf_accesses, e.counters.idx_reads],
+                                              dtype=np.int64)
+            if first is None:
+                first = final
+                rng = np.random.default_rng(99)
+                rec["sample_q"] = rng.integers(0, st.q, 3000)
+                rec["sample_c"] = rng.integers(0, final.shape[1], 3000)
+            rec[f"{key}_sample_v"] = final[rec["sample_q"], rec["sample_c"]]
+    np.savez_compressed(os.path.join(OUT, f"config_{name}.npz"), **rec)
+    print("config", name, "n_fluid", int(rec["n_fluid"]), flush=True)
+
+
+def json_dumps(obj):
+    import json
+
+    return json.dumps(obj, sort_keys=True)
+
+
+def _sphere_solid(dims, diameter, porosity, seed, geometry, fill_dims=None):
+    """Overlapping spheres through the reference's voxelize (geometry.py:
+    150-178); centres drawn over ``fill_dims`` (default dims) grown by one
+    radius per side (the law of bench.py / paper_2408_06880_b200.geometry)."""
+    import math
+
+    fill = tuple(fill_dims or dims)
+    vol = math.pi * diameter**3 / 6.0
+    grown = np.asarray(fill, dtype=np.float64) + diameter
+    count = int(round(-math.log(porosity) * float(np.prod(grown)) / vol))
+    rng = np.random.default_rng(seed)
+    centers = rng.random((count, 3)) * grown - diameter / 2.0
+    pack = geometry.SpherePack(tuple(float(d) for d in dims), diameter, centers, seed)
+    return geometry.voxelize(pack).solid
+
+
+def configs_main(which):
+    """BASELINE configs pinned at reduced scale (VERDICT r01 next #1)."""
+    os.makedirs(OUT, exist_ok=True)
+    core, domain, exchange, flags, geometry, sparse, stencil = _ref()
+    FK, FS = flags.FaceKind, flags.FaceSpec
+    P, W = FS(FK.PERIODIC), FS(FK.WALL)
+    lam316 = 1.0 / (3.0 / 16.0 / (1.0 / 1.2 - 0.5) + 0.5)
+    if "c2" in which:
+        # C2 law (d = 16, porosity 0.30, fully periodic, TRT AA) at 128^3 and 256^3
+        for edge in (128, 256):
+            bed_case(f"c2_{edge}_trt_aa", (edge,) * 3, 0.3, 16.0, 1, "d3q19", "trt", 1.2, lam316,
+                     20, "aa", channel=False)
+    if "c5" in which:
+        # C5 porosity sweep: obstacle_flags (geometry.py:250-260, 315-320), sparse and dense
+        for phi in (0.05, 0.3, 0.6, 1.0):
+            fl = geometry.obstacle_flags((96, 96, 96), phi, 1)
+            config_engine_case(f"c5_96_phi{int(round(phi * 100)):03d}", fl, "d3q19", "trt", 1.2,
+                               lam316, 6,
+                               {"kind": "obstacle", "dims": [96, 96, 96], "porosity": phi,
+                                "seed": 1})
+    if "c3" in which:
+        # C3 riverbed at 64^3 per block, 2x2x1 blocks, D3Q27 TRT, overlapped driver
+        dims = (128, 128, 64)
+        solid = _sphere_solid(dims, 16.0, 0.35, 3, geometry, fill_dims=(128, 128, 32))
+        lid = FS(FK.WALL, velocity=(0.02, 0.0, 0.0))
+        fl = flags.make_flags(dims, [(P, P), (P, P), (W, lid)], solid=solid)
+        config_domain_case("c3_2x2x1_d3q27_trt", fl, (64, 64, 64), "d3q27", "trt", 1.6, 1.1, 8,
+                           {"kind": "riverbed", "dims": list(dims), "diameter": 16.0,
+                            "porosity": 0.35, "seed": 3, "fill": [128, 128, 32],
+                            "lid": [0.02, 0.0, 0.0]})
+    if "c4" in which:
+        # C4 artery, quarter scale (128^3 box, radii / 4), 32^3 blocks, UBB inlet, no outlet
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        if root not in sys.path:
+            sys.path.insert(0, root)
+        from paper_2408_06880_b200 import geometry as mine  # the generator (unpinned, F13)
+
+        dims = (128, 128, 128)
+        fluid = mine.artery_tree(dims, seed=0, r_root=10.0, r_min=3.5)
+        inlet = FS(FK.WALL, velocity=(0.02, 0.0, 0.0))
+        fl = flags.make_flags(dims, [(inlet, W), (W, W), (W, W)], solid=~fluid)
+        config_domain_case("c4_quarter_artery", fl, (32, 32, 32), "d3q19", "trt", 1.7,
+                           1.0 / (3.0 / 16.0 / (1.0 / 1.7 - 0.5) + 0.5), 10,
+                           {"kind": "artery", "dims": list(dims), "seed": 0, "r_root": 10.0,
+                            "r_min": 3.5, "inlet": [0.02, 0.0, 0.0]})
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "--configs":
+        configs_main(sys.argv[2:] or ["c2", "c3", "c4", "c5"])
+    else:
+        main()
