@@ -280,6 +280,10 @@ int slbm_capture_begin(void* stream);
 int slbm_capture_end(void* stream, void** graph_exec);
 int slbm_graph_launch(void* graph_exec, void* stream);
 int slbm_graph_destroy(void* graph_exec);
+/* number of this library's kernels launched in the process so far (every
+ * launch site counts itself; a graph replay counts the library kernels it
+ * captured; cub / NCCL kernels are not included) -- bench.py's gpu_launches */
+int slbm_launch_count(int64_t* count);
 
 /* Tuning knobs (tools/variants.py, tools/e2e_probe.py).
  * Engine knobs 0-9 select kernels; each engine owns its settings

@@ -108,6 +108,7 @@ SIGNATURES = {
     "slbm_voxelize_spheres": [c_i32p, c_dp, C.c_int64, C.c_double, C.c_int, c_u8p],
     "slbm_set_tuning": [C.c_int, C.c_int],
     "slbm_engine_set_tuning": [vp, C.c_int, C.c_int],
+    "slbm_launch_count": [C.POINTER(C.c_int64)],
     "slbm_group_create": [C.POINTER(vp), C.c_int, C.POINTER(vp)],
     "slbm_group_destroy": [vp],
     "slbm_group_refresh": [vp, C.c_int, vp],
@@ -156,3 +157,11 @@ def ptr(arr, ctype):
     if arr is None:
         return None
     return arr.ctypes.data_as(C.POINTER(ctype))
+
+
+def launch_count() -> int:
+    """Kernels of this library launched so far in the process
+    (slbm_launch_count; graph replays included)."""
+    n = C.c_int64(0)
+    call("slbm_launch_count", C.byref(n))
+    return int(n.value)

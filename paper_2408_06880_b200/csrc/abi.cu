@@ -3,11 +3,18 @@
 #include <climits>
 #include <cmath>
 #include <cstring>
+#include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "engine.cuh"
 
 namespace slbm {
+
+std::atomic<long long> g_launches{0};
+static thread_local long long t_capture_mark = 0;
+static std::mutex g_graph_mu;
+static std::unordered_map<void*, long long> g_graph_kernels;  // exec -> kernels per replay
 
 static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
@@ -158,11 +165,14 @@ int slbm_engine_set_tuning(SlbmEngine* e, int knob, int value) {
 int slbm_capture_begin(void* stream) {
   if (!stream) return fail(SLBM_ECONFIG, "capture needs a non-default stream");
   SLBM_CUDA_TRY(cudaStreamBeginCapture((cudaStream_t)stream, cudaStreamCaptureModeThreadLocal));
+  t_capture_mark = g_launches.load();
   return SLBM_OK;
 }
 
 int slbm_capture_end(void* stream, void** graph_exec) {
   if (!stream || !graph_exec) return fail(SLBM_ECONFIG, "null argument");
+  const long long captured = g_launches.load() - t_capture_mark;
+  g_launches.fetch_sub(captured);  // recorded, not launched: counted per replay
   cudaGraph_t graph = nullptr;
   SLBM_CUDA_TRY(cudaStreamEndCapture((cudaStream_t)stream, &graph));
   cudaGraphExec_t exec = nullptr;
@@ -170,6 +180,10 @@ int slbm_capture_end(void* stream, void** graph_exec) {
   cudaGraphDestroy(graph);
   if (err != cudaSuccess)
     return fail(SLBM_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(err));
+  {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    g_graph_kernels[(void*)exec] = captured;
+  }
   *graph_exec = (void*)exec;
   return SLBM_OK;
 }
@@ -177,11 +191,24 @@ int slbm_capture_end(void* stream, void** graph_exec) {
 int slbm_graph_launch(void* graph_exec, void* stream) {
   if (!graph_exec) return fail(SLBM_ECONFIG, "null graph");
   SLBM_CUDA_TRY(cudaGraphLaunch((cudaGraphExec_t)graph_exec, (cudaStream_t)stream));
+  std::lock_guard<std::mutex> lk(g_graph_mu);
+  auto it = g_graph_kernels.find(graph_exec);
+  if (it != g_graph_kernels.end()) count_launch(it->second);
+  return SLBM_OK;
+}
+
+int slbm_launch_count(int64_t* count) {
+  if (!count) return fail(SLBM_ECONFIG, "null argument");
+  *count = g_launches.load();
   return SLBM_OK;
 }
 
 int slbm_graph_destroy(void* graph_exec) {
-  if (graph_exec) cudaGraphExecDestroy((cudaGraphExec_t)graph_exec);
+  if (graph_exec) {
+    cudaGraphExecDestroy((cudaGraphExec_t)graph_exec);
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    g_graph_kernels.erase(graph_exec);
+  }
   return SLBM_OK;
 }
 
@@ -695,8 +722,11 @@ int slbm_run(SlbmEngine* e, int64_t n, int use_graph) {
     if (!e->graph[k]) {
       cudaGraph_t graph = nullptr;
       SLBM_CUDA_TRY(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+      const long long mark = g_launches.load();
       int st = sweep_once(e);
       if (st == SLBM_OK) st = sweep_once(e);
+      e->graph_kernels[k] = g_launches.load() - mark;
+      g_launches.fetch_sub(e->graph_kernels[k]);
       cudaError_t ce = cudaStreamEndCapture(e->stream, &graph);
       // the captured pair leaves the state where it started
       e->steps_done -= 2;
@@ -707,7 +737,10 @@ int slbm_run(SlbmEngine* e, int64_t n, int use_graph) {
       if (ce != cudaSuccess) return fail(SLBM_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
     }
     int64_t pairs = 0;
-    for (; done + 2 <= n; done += 2, pairs += 2) SLBM_CUDA_TRY(cudaGraphLaunch(e->graph[k], e->stream));
+    for (; done + 2 <= n; done += 2, pairs += 2) {
+      SLBM_CUDA_TRY(cudaGraphLaunch(e->graph[k], e->stream));
+      count_launch(e->graph_kernels[k]);
+    }
     e->steps_done += pairs;
   }
   for (; done < n; ++done) SLBM_TRY(sweep_once(e));

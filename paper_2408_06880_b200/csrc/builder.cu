@@ -427,7 +427,7 @@ int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
                                 cudaMemcpyDeviceToDevice, s));
   SLBM_TRY(dalloc(e, &e->cid_map, n_pad));
   SLBM_CUDA_TRY(cudaMemsetAsync(e->cid_map, 0xff, n_pad * sizeof(int32_t), s));
-  k_cid_map<<<grid_for(n, 256), 256, 0, s>>>(e->x_flat, n, e->cid_map);
+  { k_cid_map<<<grid_for(n, 256), 256, 0, s>>>(e->x_flat, n, e->cid_map); slbm::count_launch(); }
 
   // -- pass 1: counts --
   Upwind up{g, d};
@@ -441,7 +441,7 @@ int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, e->device);
     unsigned blocks = std::min<unsigned>(grid_for(n, 256), unsigned(dev_sms) * 8);
-    k_count<<<blocks, 256, 0, s>>>(d_tags, e->cid_map, e->x_flat, n, up, d_counts, d_err);
+    { k_count<<<blocks, 256, 0, s>>>(d_tags, e->cid_map, e->x_flat, n, up, d_counts, d_err); slbm::count_launch(); }
   }
   unsigned long long h_counts[kCounters];
   int h_err = 0;
@@ -500,7 +500,7 @@ int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
 
   // -- pass 2: index list --
   SLBM_TRY(dalloc(e, &e->idx, int64_t(d.q - 1) * n));
-  k_fill<<<grid_for(n, 256), 256, 0, s>>>(d_tags, e->cid_map, e->x_flat, n, up, bases, e->idx);
+  { k_fill<<<grid_for(n, 256), 256, 0, s>>>(d_tags, e->cid_map, e->x_flat, n, up, bases, e->idx); slbm::count_launch(); }
 
   SLBM_TRY(dalloc(e, &e->ubb_slot, e->n_ubb));
   SLBM_TRY(dalloc(e, &e->ubb_partner, e->n_ubb));
@@ -520,10 +520,10 @@ int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
     int64_t cnt = 0;
     SLBM_TRY(select_if(thrust::counting_iterator<uint32_t>(0), sel_buf, n,
                        ReadsTag{d_tags, e->x_flat, up, q, kUbb}, &cnt, s));
-    k_ubb_assign<<<grid_for(cnt, 256), 256, 0, s>>>(
+    { k_ubb_assign<<<grid_for(cnt, 256), 256, 0, s>>>(
         sel_buf, cnt, q, e->x_flat, n, up, bases, d_wall_flat, d_wall_u,
         int64_t(wall_flat.size()), e->idx, e->ubb_slot + e->ubb_off[q],
-        e->ubb_partner + e->ubb_off[q], e->ubb_corr + e->ubb_off[q], d_err);
+        e->ubb_partner + e->ubb_off[q], e->ubb_corr + e->ubb_off[q], d_err); slbm::count_launch(); }
   }
 
   SLBM_TRY(dalloc(e, &e->ghost_key, e->n_ghost));
@@ -541,7 +541,7 @@ int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
       int64_t cnt = 0;
       SLBM_TRY(select_if(thrust::counting_iterator<uint32_t>(0), sel_buf, n,
                          ReadsTag{d_tags, e->x_flat, up, q, kExchange}, &cnt, s));
-      k_ghost_keys<<<grid_for(cnt, 256), 256, 0, s>>>(sel_buf, cnt, q, e->x_flat, up, k_in);
+      { k_ghost_keys<<<grid_for(cnt, 256), 256, 0, s>>>(sel_buf, cnt, q, e->x_flat, up, k_in); slbm::count_launch(); }
       size_t tmp_bytes = 0;
       SLBM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k_in, k_out, sel_buf,
                                                     c_out, cnt, 0, 37, s));
@@ -551,7 +551,7 @@ int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
                                                     cnt, 0, 37, s));
       SLBM_CUDA_TRY(cudaFreeAsync(tmp, s));
       uint32_t first = uint32_t(e->base[q] + n + e->n_ubb_q[q]);
-      k_ghost_assign<<<grid_for(cnt, 256), 256, 0, s>>>(c_out, cnt, q, n, first, e->idx);
+      { k_ghost_assign<<<grid_for(cnt, 256), 256, 0, s>>>(c_out, cnt, q, n, first, e->idx); slbm::count_launch(); }
       SLBM_CUDA_TRY(cudaMemcpyAsync(e->ghost_key + e->ghost_off[q], k_out,
                                     cnt * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
     }
@@ -578,10 +578,10 @@ int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
                        ReadsTag{d_tags, e->x_flat, up, q, kOutlet}, &cnt, s));
     const uint32_t first = uint32_t(e->base[q] + n + e->n_ubb_q[q] + e->n_ghost_q[q]);
     const int64_t off = e->out_off[q];
-    k_outlet_assign<<<grid_for(cnt, 256), 256, 0, s>>>(
+    { k_outlet_assign<<<grid_for(cnt, 256), 256, 0, s>>>(
         sel_buf, cnt, q, e->x_flat, n, up, bases, first, d_wall_flat, d_wall_u,
         int64_t(wall_flat.size()), e->idx, e->out_slot + off, e->out_partner + off,
-        e->out_cell + off, e->out_dir + off, e->out_rho + off, d_err);
+        e->out_cell + off, e->out_dir + off, e->out_rho + off, d_err); slbm::count_launch(); }
   }
 
   // -- ownership uniqueness (sparse.py:182-185) --
@@ -591,8 +591,8 @@ int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
     SLBM_CUDA_TRY(cudaMalloc(&bits, words * sizeof(unsigned int)));
     SLBM_CUDA_TRY(cudaMemsetAsync(bits, 0, words * sizeof(unsigned int), s));
     int64_t entries = int64_t(d.q) * n;
-    k_unique<<<grid_for(entries, 256), 256, 0, s>>>(e->idx, n, d.q, uint64_t(total), bits,
-                                                     d_err);
+    { k_unique<<<grid_for(entries, 256), 256, 0, s>>>(e->idx, n, d.q, uint64_t(total), bits,
+                                                     d_err); slbm::count_launch(); }
     SLBM_CUDA_TRY(cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
     SLBM_CUDA_TRY(cudaStreamSynchronize(s));
     cudaFree(bits);
@@ -638,15 +638,15 @@ int build_lists(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
     e->device_bytes -= int64_t(d.q - 1) * n * 4;  // the logical list is freed below
     const int64_t entries = int64_t(d.q - 1) * n;
     if (entries)
-      k_physical_idx<<<grid_for(entries, 256), 256, 0, s>>>(logical, n, e->idx_pitch, d.q - 1, m,
-                                                            e->idx);
+      { k_physical_idx<<<grid_for(entries, 256), 256, 0, s>>>(logical, n, e->idx_pitch, d.q - 1, m,
+                                                            e->idx); slbm::count_launch(); }
     if (e->n_ubb) {
-      k_physical_inplace<<<grid_for(e->n_ubb, 256), 256, 0, s>>>(e->ubb_slot, e->n_ubb, m);
-      k_physical_inplace<<<grid_for(e->n_ubb, 256), 256, 0, s>>>(e->ubb_partner, e->n_ubb, m);
+      { k_physical_inplace<<<grid_for(e->n_ubb, 256), 256, 0, s>>>(e->ubb_slot, e->n_ubb, m); slbm::count_launch(); }
+      { k_physical_inplace<<<grid_for(e->n_ubb, 256), 256, 0, s>>>(e->ubb_partner, e->n_ubb, m); slbm::count_launch(); }
     }
     if (e->n_out) {
-      k_physical_inplace<<<grid_for(e->n_out, 256), 256, 0, s>>>(e->out_slot, e->n_out, m);
-      k_physical_inplace<<<grid_for(e->n_out, 256), 256, 0, s>>>(e->out_partner, e->n_out, m);
+      { k_physical_inplace<<<grid_for(e->n_out, 256), 256, 0, s>>>(e->out_slot, e->n_out, m); slbm::count_launch(); }
+      { k_physical_inplace<<<grid_for(e->n_out, 256), 256, 0, s>>>(e->out_partner, e->n_out, m); slbm::count_launch(); }
     }
     SLBM_CUDA_TRY(cudaGetLastError());
     SLBM_CUDA_TRY(cudaStreamSynchronize(s));
@@ -705,7 +705,7 @@ int build_split(SlbmEngine* e, const int32_t* lo_w, const int32_t* hi_w, uint32_
   } else {
     e->interior_lo = -1;
     SLBM_TRY(dalloc(e, &e->frame_bits, (n + 31) / 32));
-    k_frame_bits<<<grid_for(n, 256), 256, 0, s>>>(fr, n, e->frame_bits);
+    { k_frame_bits<<<grid_for(n, 256), 256, 0, s>>>(fr, n, e->frame_bits); slbm::count_launch(); }
     SLBM_CUDA_TRY(cudaGetLastError());
   }
   SLBM_CUDA_TRY(cudaStreamSynchronize(s));
@@ -732,8 +732,8 @@ int export_idx_logical(SlbmEngine* e, uint32_t* host) {
   }
   uint32_t* tmp = nullptr;
   SLBM_CUDA_TRY(cudaMallocAsync(&tmp, size_t(rows * n) * 4, e->stream));
-  k_logical_idx<<<grid_for(rows * n, 256), 256, 0, e->stream>>>(e->idx, n, e->idx_pitch, rows, inv,
-                                                                tmp);
+  { k_logical_idx<<<grid_for(rows * n, 256), 256, 0, e->stream>>>(e->idx, n, e->idx_pitch, rows, inv,
+                                                                tmp); slbm::count_launch(); }
   SLBM_CUDA_TRY(cudaGetLastError());
   SLBM_TRY(copy_d2h(host, tmp, size_t(rows * n) * 4, e->device, e->stream));
   SLBM_CUDA_TRY(cudaFreeAsync(tmp, e->stream));

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 #include <type_traits>
 
@@ -11,6 +12,14 @@
 #include "lattice_tables.h"
 
 namespace slbm {
+
+// ---- launch accounting (slbm_launch_count) ---------------------------------
+// Every kernel launch site of the library calls count_launch() right after the
+// launch; a stream capture takes its launches back out and the graph adds
+// them again on every replay, so the counter is the number of this library's
+// kernels that reached the GPU (cub / NCCL kernels are not counted).
+extern std::atomic<long long> g_launches;
+inline void count_launch(long long n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 // ---- error plumbing -------------------------------------------------------
 void set_error(const std::string& msg);

@@ -407,8 +407,8 @@ int build_dense(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
   SLBM_CUDA_TRY(cudaMalloc(&d_err, sizeof(int)));
   SLBM_CUDA_TRY(cudaMemsetAsync(d_cnt, 0, 2 * sizeof(unsigned long long), s));
   SLBM_CUDA_TRY(cudaMemsetAsync(d_err, 0, sizeof(int), s));
-  k_dense_mask<<<grid_of(cells, 256), 256, 0, s>>>(d_tags, g, e->dirs, e->dense_mask, d_cnt,
-                                                    d_err);
+  { k_dense_mask<<<grid_of(cells, 256), 256, 0, s>>>(d_tags, g, e->dirs, e->dense_mask, d_cnt,
+                                                    d_err); slbm::count_launch(); }
   unsigned long long n_ubb = 0;
   int h_err = 0;
   SLBM_CUDA_TRY(cudaMemcpyAsync(&n_ubb, d_cnt, sizeof(n_ubb), cudaMemcpyDeviceToHost, s));
@@ -433,9 +433,9 @@ int build_dense(SlbmEngine* e, const uint8_t* tags_pad, const double* ubb_u_pad,
     SLBM_CUDA_TRY(cudaMalloc(&corr, n_ubb * 8));
     SLBM_CUDA_TRY(cudaMalloc(&e->dense_ubb_key, n_ubb * 8));
     SLBM_CUDA_TRY(cudaMalloc(&e->dense_ubb_corr, n_ubb * 8));
-    k_dense_ubb<<<grid_of(cells, 256), 256, 0, s>>>(d_tags, g, e->dirs, e->dense_mask, d_wf, d_wu,
+    { k_dense_ubb<<<grid_of(cells, 256), 256, 0, s>>>(d_tags, g, e->dirs, e->dense_mask, d_wf, d_wu,
                                                      int64_t(wall_flat.size()), d_cnt + 1, keys,
-                                                     corr);
+                                                     corr); slbm::count_launch(); }
     size_t tmp_bytes = 0;
     SLBM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, e->dense_ubb_key, corr,
                                                   e->dense_ubb_corr, int64_t(n_ubb), 0, 64, s));
@@ -504,13 +504,13 @@ int dense_step(SlbmEngine* e, int phase) {
       auto launch = [&](auto sp) {
         constexpr bool S = decltype(sp)::value;
         if (kind == 0)
-          k_dense<L, M, 0, S><<<grid, 128, 0, e->stream>>>(a, ahead);
+          { k_dense<L, M, 0, S><<<grid, 128, 0, e->stream>>>(a, ahead); slbm::count_launch(); }
         else if (kind == 1)
-          k_dense<L, M, 1, S><<<grid, 128, 0, e->stream>>>(a, ahead);
+          { k_dense<L, M, 1, S><<<grid, 128, 0, e->stream>>>(a, ahead); slbm::count_launch(); }
         else if (phase == SLBM_PHASE_ALL && e->tune.dense_lean_odd)
-          k_dense_odd<L, M><<<grid, 128, 0, e->stream>>>(oa);
+          { k_dense_odd<L, M><<<grid, 128, 0, e->stream>>>(oa); slbm::count_launch(); }
         else
-          k_dense<L, M, 2, S><<<grid, 128, 0, e->stream>>>(a, ahead);
+          { k_dense<L, M, 2, S><<<grid, 128, 0, e->stream>>>(a, ahead); slbm::count_launch(); }
       };
       if (spec)
         launch(std::true_type{});
@@ -533,10 +533,10 @@ int dense_init(SlbmEngine* e, const double* dev_values) {
   const int64_t npad = e->geo.n_padded();
   SLBM_TRY(launch_fill(e->pdf, e->total_slots, NAN, e->stream));
   if (e->tmp) SLBM_TRY(launch_fill(e->tmp, e->total_slots, NAN, e->stream));
-  k_dense_weights<<<grid_of(e->geo.n_cells(), 256), 256, 0, e->stream>>>(e->pdf, e->geo, npad,
-                                                                          e->dirs);
-  k_dense_scatter<<<grid_of(e->n_fluid, 256), 256, 0, e->stream>>>(e->pdf, e->x_flat, e->n_fluid,
-                                                                    npad, e->q, dev_values);
+  { k_dense_weights<<<grid_of(e->geo.n_cells(), 256), 256, 0, e->stream>>>(e->pdf, e->geo, npad,
+                                                                          e->dirs); slbm::count_launch(); }
+  { k_dense_scatter<<<grid_of(e->n_fluid, 256), 256, 0, e->stream>>>(e->pdf, e->x_flat, e->n_fluid,
+                                                                    npad, e->q, dev_values); slbm::count_launch(); }
   SLBM_CUDA_TRY(cudaGetLastError());
   e->parity = SLBM_EVEN;
   return SLBM_OK;
@@ -544,8 +544,8 @@ int dense_init(SlbmEngine* e, const double* dev_values) {
 
 int dense_canonical(SlbmEngine* e, double* dev_values) {
   const int odd = (e->pattern == SLBM_AA && e->parity == SLBM_ODD) ? 1 : 0;
-  k_dense_gather<<<grid_of(e->n_fluid, 256), 256, 0, e->stream>>>(
-      e->pdf, e->x_flat, e->n_fluid, e->geo.n_padded(), e->dirs, odd, dev_values);
+  { k_dense_gather<<<grid_of(e->n_fluid, 256), 256, 0, e->stream>>>(
+      e->pdf, e->x_flat, e->n_fluid, e->geo.n_padded(), e->dirs, odd, dev_values); slbm::count_launch(); }
   SLBM_CUDA_TRY(cudaGetLastError());
   return SLBM_OK;
 }

@@ -97,6 +97,7 @@ struct SlbmEngine {
 
   // CUDA graphs of one step pair, keyed by starting state (0/1)
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
+  long long graph_kernels[2] = {0, 0};  // library kernels per replay (slbm_launch_count)
   int64_t steps_done = 0;
   slbm::PairPlan* pair = nullptr;  // pair.cu: temporally blocked AA step pair
 

@@ -57,8 +57,8 @@ extern "C" int slbm_voxelize_spheres(const int32_t* dims, const double* centers,
   if (n) {
     SLBM_CUDA_TRY(cudaMalloc(&d_c, n * 3 * sizeof(double)));
     SLBM_CUDA_TRY(cudaMemcpy(d_c, centers, n * 3 * sizeof(double), cudaMemcpyHostToDevice));
-    k_voxelize<<<unsigned(n), 256>>>(d_c, n, diameter / 2.0, make_int3(dims[0], dims[1], dims[2]),
-                                     d_solid);
+    { k_voxelize<<<unsigned(n), 256>>>(d_c, n, diameter / 2.0, make_int3(dims[0], dims[1], dims[2]),
+                                     d_solid); slbm::count_launch(); }
     SLBM_CUDA_TRY(cudaGetLastError());
   }
   SLBM_CUDA_TRY(cudaMemcpy(solid, d_solid, cells, cudaMemcpyDeviceToHost));

@@ -317,16 +317,16 @@ int slbm_group_refresh(SlbmGroup* g, int parity, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   if (g->n_ubb) {
     const int flip = g->pattern == SLBM_PULL ? g->flip : 0;
-    k_group_refresh<<<unsigned((g->n_ubb + 255) / 256), 256, 0, s>>>(
-        g->table[0][flip], g->ubb_eng, g->ubb_slot, g->ubb_partner, g->ubb_corr, g->n_ubb, parity);
+    { k_group_refresh<<<unsigned((g->n_ubb + 255) / 256), 256, 0, s>>>(
+        g->table[0][flip], g->ubb_eng, g->ubb_slot, g->ubb_partner, g->ubb_corr, g->n_ubb, parity); slbm::count_launch(); }
     SLBM_CUDA_TRY(cudaGetLastError());
   }
   if (g->n_out) {  // every outlet entry of every block: one launch
     const int flip = g->pattern == SLBM_PULL ? g->flip : 0;
     on_lattice(g->q, [&](auto lat) {
       using L = decltype(lat);
-      k_group_outlet<L><<<unsigned((g->n_out + 127) / 128), 128, 0, s>>>(
-          g->table[0][flip], g->out_tab, g->out_eng, g->out_idx, g->n_out, parity);
+      { k_group_outlet<L><<<unsigned((g->n_out + 127) / 128), 128, 0, s>>>(
+          g->table[0][flip], g->out_tab, g->out_eng, g->out_idx, g->n_out, parity); slbm::count_launch(); }
     });
     SLBM_CUDA_TRY(cudaGetLastError());
   }
@@ -354,14 +354,14 @@ int slbm_group_step(SlbmGroup* g, int phase, void* stream) {
     auto go = [&](auto mc) {
       constexpr int M = decltype(mc)::value;
       if (kind == 0)
-        k_group<L, M, 0><<<g->n_cta[phase], kGB, 0, s>>>(tab, g->cta_start[phase], n, g->omega, g->lam,
-                                                           ahead);
+        { k_group<L, M, 0><<<g->n_cta[phase], kGB, 0, s>>>(tab, g->cta_start[phase], n, g->omega, g->lam,
+                                                           ahead); slbm::count_launch(); }
       else if (kind == 1)
-        k_group<L, M, 1><<<g->n_cta[phase], kGB, 0, s>>>(tab, g->cta_start[phase], n, g->omega, g->lam,
-                                                           ahead);
+        { k_group<L, M, 1><<<g->n_cta[phase], kGB, 0, s>>>(tab, g->cta_start[phase], n, g->omega, g->lam,
+                                                           ahead); slbm::count_launch(); }
       else
-        k_group<L, M, 2><<<g->n_cta[phase], kGB, 0, s>>>(tab, g->cta_start[phase], n, g->omega, g->lam,
-                                                           ahead);
+        { k_group<L, M, 2><<<g->n_cta[phase], kGB, 0, s>>>(tab, g->cta_start[phase], n, g->omega, g->lam,
+                                                           ahead); slbm::count_launch(); }
     };
     if (g->model == SLBM_SRT)
       go(std::integral_constant<int, SLBM_SRT>{});
@@ -387,7 +387,7 @@ int slbm_group_finish(SlbmGroup* g, void* stream) {
   }
   if (g->pattern == SLBM_PULL) g->flip ^= 1;
   const int n = int(g->engines.size());
-  k_group_advance<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(g->steps, n);
+  { k_group_advance<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(g->steps, n); slbm::count_launch(); }
   SLBM_CUDA_TRY(cudaGetLastError());
   return SLBM_OK;
 }

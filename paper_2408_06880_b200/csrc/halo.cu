@@ -277,20 +277,20 @@ int peer_start(SlbmHalo* h, PhaseProg& p, int phase) {
     const FlagPtrs acks = flag_ptrs(h, p.send_peer, false, kMaxPeers);  // their acks to us
     for (size_t i = 0; i < p.send_peer.size(); ++i) {
       if (!p.remote_dst[i]) return fail(SLBM_ECONFIG, "peer transport: halo not connected");
-      k_pack_signal<<<grid_for(p.send_cnt[i]), 256, 0, s>>>(
+      { k_pack_signal<<<grid_for(p.send_cnt[i]), 256, 0, s>>>(
           t, p.d_pe + p.send_off[i], p.d_ps + p.send_off[i], p.send_cnt[i], p.remote_dst[i],
-          h->d_done + phase * kMaxPeers + i, data.p[i], acks.p[i], h->d_epoch);
+          h->d_done + phase * kMaxPeers + i, data.p[i], acks.p[i], h->d_epoch); slbm::count_launch(); }
     }
     SLBM_CUDA_TRY(cudaGetLastError());
   }
   SLBM_TRY(slbm_halo_local(h, phase));
   if (!p.recv_peer.empty()) {
-    k_unpack_ack<<<grid_for(p.n_unpack), 256, 0, s>>>(
+    { k_unpack_ack<<<grid_for(p.n_unpack), 256, 0, s>>>(
         t, p.d_upos, p.d_ue, p.d_us, p.n_unpack, h->d_recv, flag_ptrs(h, p.recv_peer, false, 0),
         flag_ptrs(h, p.recv_peer, true, kMaxPeers), h->d_done + 2 * kMaxPeers + phase,
-        h->d_epoch);
+        h->d_epoch); slbm::count_launch(); }
   } else {
-    k_epoch_advance<<<1, 1, 0, s>>>(h->d_epoch);
+    { k_epoch_advance<<<1, 1, 0, s>>>(h->d_epoch); slbm::count_launch(); }
   }
   SLBM_CUDA_TRY(cudaGetLastError());
   SLBM_CUDA_TRY(cudaEventRecord(h->ev_done, s));
@@ -472,8 +472,8 @@ int slbm_halo_local(SlbmHalo* h, int phase) {
   if (!h->committed) return fail(SLBM_ECONFIG, "halo not committed");
   PhaseProg& p = h->ph[phase];
   if (p.n_local) {
-    k_local<<<grid_for(p.n_local), 256, 0, h->comm>>>(h->table(), p.d_lse, p.d_lss, p.d_lde,
-                                                       p.d_lds, p.n_local);
+    { k_local<<<grid_for(p.n_local), 256, 0, h->comm>>>(h->table(), p.d_lse, p.d_lss, p.d_lde,
+                                                       p.d_lds, p.n_local); slbm::count_launch(); }
     SLBM_CUDA_TRY(cudaGetLastError());
   }
   SLBM_CUDA_TRY(cudaEventRecord(h->ev_done, h->comm));
@@ -486,8 +486,8 @@ int slbm_halo_local_on(SlbmHalo* h, int phase, void* stream) {
   cudaSetDevice(h->device);
   PhaseProg& p = h->ph[phase];
   if (p.n_local) {
-    k_local<<<grid_for(p.n_local), 256, 0, (cudaStream_t)stream>>>(h->table(), p.d_lse, p.d_lss,
-                                                                    p.d_lde, p.d_lds, p.n_local);
+    { k_local<<<grid_for(p.n_local), 256, 0, (cudaStream_t)stream>>>(h->table(), p.d_lse, p.d_lss,
+                                                                    p.d_lde, p.d_lds, p.n_local); slbm::count_launch(); }
     SLBM_CUDA_TRY(cudaGetLastError());
   }
   return SLBM_OK;
@@ -524,7 +524,7 @@ int slbm_halo_start(SlbmHalo* h, int phase, void* after_stream) {
 namespace {
 int nccl_start(SlbmHalo* h, PhaseProg& p, int phase, const PdfTable& t) {
   if (p.n_pack) {
-    k_pack<<<grid_for(p.n_pack), 256, 0, h->comm>>>(t, p.d_pe, p.d_ps, p.n_pack, h->d_send);
+    { k_pack<<<grid_for(p.n_pack), 256, 0, h->comm>>>(t, p.d_pe, p.d_ps, p.n_pack, h->d_send); slbm::count_launch(); }
     SLBM_CUDA_TRY(cudaGetLastError());
   }
   SLBM_TRY(slbm_halo_local(h, phase));
@@ -540,8 +540,8 @@ int nccl_start(SlbmHalo* h, PhaseProg& p, int phase, const PdfTable& t) {
     NCCL_TRY(ncclGroupEnd());
   }
   if (p.n_unpack) {
-    k_unpack<<<grid_for(p.n_unpack), 256, 0, h->comm>>>(t, p.d_upos, p.d_ue, p.d_us, p.n_unpack,
-                                                         h->d_recv);
+    { k_unpack<<<grid_for(p.n_unpack), 256, 0, h->comm>>>(t, p.d_upos, p.d_ue, p.d_us, p.n_unpack,
+                                                         h->d_recv); slbm::count_launch(); }
     SLBM_CUDA_TRY(cudaGetLastError());
   }
   SLBM_CUDA_TRY(cudaEventRecord(h->ev_done, h->comm));
@@ -593,8 +593,8 @@ int slbm_halo_pack_host(SlbmHalo* h, int phase, int peer, double* host_out) {
   const size_t i = size_t(it - p.send_peer.begin());
   const int64_t off = p.send_off[i], cnt = p.send_cnt[i];
   if (cnt == 0) return SLBM_OK;
-  k_pack<<<grid_for(cnt), 256, 0, h->comm>>>(h->table(), p.d_pe + off, p.d_ps + off, cnt,
-                                              h->d_send + off);
+  { k_pack<<<grid_for(cnt), 256, 0, h->comm>>>(h->table(), p.d_pe + off, p.d_ps + off, cnt,
+                                              h->d_send + off); slbm::count_launch(); }
   SLBM_CUDA_TRY(cudaGetLastError());
   SLBM_CUDA_TRY(cudaMemcpyAsync(host_out, h->d_send + off, cnt * sizeof(double),
                                 cudaMemcpyDeviceToHost, h->comm));
@@ -616,8 +616,8 @@ int slbm_halo_unpack_host(SlbmHalo* h, int phase, int peer, const double* host_i
     SLBM_CUDA_TRY(cudaMemcpyAsync(h->d_recv + roff, host_in, rcnt * sizeof(double),
                                   cudaMemcpyHostToDevice, h->comm));
   if (ucnt) {
-    k_unpack<<<grid_for(ucnt), 256, 0, h->comm>>>(h->table(), p.d_upos + uoff, p.d_ue + uoff,
-                                                   p.d_us + uoff, ucnt, h->d_recv);
+    { k_unpack<<<grid_for(ucnt), 256, 0, h->comm>>>(h->table(), p.d_upos + uoff, p.d_ue + uoff,
+                                                   p.d_us + uoff, ucnt, h->d_recv); slbm::count_launch(); }
     SLBM_CUDA_TRY(cudaGetLastError());
   }
   SLBM_CUDA_TRY(cudaStreamSynchronize(h->comm));

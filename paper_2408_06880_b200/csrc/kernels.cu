@@ -154,8 +154,8 @@ void launch_index(const SweepArgs& a, const SlbmTuning& t, cudaStream_t s) {
   }
   const uint32_t ahead = t.ahead_ctas > 0 ? uint32_t(t.ahead_ctas)
                                           : uint32_t(num_sms() * resident * t.ahead_quarters / 4);
-  k_index_sweep<L, MODEL, KIND, MINB, PF>
-      <<<(a.n_cells + kIB - 1) / kIB, kIB, 0, s>>>(a, std::max(ahead, 1u));
+  { k_index_sweep<L, MODEL, KIND, MINB, PF>
+      <<<(a.n_cells + kIB - 1) / kIB, kIB, 0, s>>>(a, std::max(ahead, 1u)); slbm::count_launch(); }
 }
 
 template <class L, int MODEL>
@@ -168,15 +168,15 @@ void launch_kind(int kind, const SweepArgs& a, unsigned grid, const SlbmTuning& 
       launch_index<L, MODEL, kEven, MINB, false>(a, t, s);
 #ifdef SLBM_PROBES
     else if (t.even_variant == 2)  // memory-pattern probe, not LBM
-      k_probe<L><<<(a.n_cells + kIB - 1) / kIB, kIB, 0, s>>>(a);
+      { k_probe<L><<<(a.n_cells + kIB - 1) / kIB, kIB, 0, s>>>(a); slbm::count_launch(); }
 #endif
     else
       launch_index<L, MODEL, kEven, MINB, true>(a, t, s);
   } else {
     if (L::Q != 9 && t.odd_variant == 2)
-      k_aa_odd<L, MODEL, 4><<<grid, kBlock, 0, s>>>(a);
+      { k_aa_odd<L, MODEL, 4><<<grid, kBlock, 0, s>>>(a); slbm::count_launch(); }
     else
-      k_aa_odd<L, MODEL, L::Q == 9 ? 1 : 3><<<grid, kBlock, 0, s>>>(a);
+      { k_aa_odd<L, MODEL, L::Q == 9 ? 1 : 3><<<grid, kBlock, 0, s>>>(a); slbm::count_launch(); }
   }
 }
 
@@ -492,9 +492,9 @@ int launch_slot_lookup(SlbmEngine* e, const int64_t* d_qs, const int64_t* d_pfla
   if (n == 0) return SLBM_OK;
   SweepArgs a = sweep_args(e);  // slot ids: the reference's layout, not the device one
   for (int q = 0; q <= e->q && q < 28; ++q) a.base[q] = uint32_t(e->base[q]);
-  k_slot_lookup<<<grid_for(n, 256), 256, 0, e->stream>>>(d_qs, d_pflat, n, e->cid_map,
+  { k_slot_lookup<<<grid_for(n, 256), 256, 0, e->stream>>>(d_qs, d_pflat, n, e->cid_map,
                                                           e->geo.n_padded(), a, e->q, d_out,
-                                                          d_err);
+                                                          d_err); slbm::count_launch(); }
   SLBM_CUDA_TRY(cudaGetLastError());
   return SLBM_OK;
 }
@@ -527,17 +527,17 @@ int launch_step(SlbmEngine* e, int phase) {
 
 int launch_refresh(SlbmEngine* e, int parity) {
   if (e->n_ubb) {
-    k_refresh<<<grid_for(e->n_ubb, 256), 256, 0, e->stream>>>(
-        e->pdf, e->ubb_slot, e->ubb_partner, e->ubb_corr, uint32_t(e->n_ubb), parity);
+    { k_refresh<<<grid_for(e->n_ubb, 256), 256, 0, e->stream>>>(
+        e->pdf, e->ubb_slot, e->ubb_partner, e->ubb_corr, uint32_t(e->n_ubb), parity); slbm::count_launch(); }
     SLBM_CUDA_TRY(cudaGetLastError());
   }
   if (e->n_out) {
     SweepArgs a = sweep_args(e);
     by_lattice(e->q, [&](auto lat) {
       using L = decltype(lat);
-      k_outlet<L><<<grid_for(e->n_out, 128), 128, 0, e->stream>>>(
+      { k_outlet<L><<<grid_for(e->n_out, 128), 128, 0, e->stream>>>(
           e->pdf, a, e->out_slot, e->out_partner, e->out_cell, e->out_dir, e->out_rho, e->out_u,
-          uint32_t(e->n_out), parity);
+          uint32_t(e->n_out), parity); slbm::count_launch(); }
     });
     SLBM_CUDA_TRY(cudaGetLastError());
   }
@@ -545,7 +545,7 @@ int launch_refresh(SlbmEngine* e, int parity) {
 }
 
 int launch_advance(SlbmEngine* e) {
-  k_advance<<<1, 1, 0, e->stream>>>(e->d_step);
+  { k_advance<<<1, 1, 0, e->stream>>>(e->d_step); slbm::count_launch(); }
   SLBM_CUDA_TRY(cudaGetLastError());
   return SLBM_OK;
 }
@@ -564,7 +564,9 @@ cudaError_t resident_launch(const SweepArgs& a, const ResidentArgs& r, cudaStrea
   const int64_t need = (int64_t(a.n_fluid) + kIB - 1) / kIB;
   const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(need, int64_t(per_sm) * num_sms())));
   void* args[] = {const_cast<SweepArgs*>(&a), const_cast<ResidentArgs*>(&r)};
-  return cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kIB), args, 0, s);
+  const cudaError_t err = cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kIB), args, 0, s);
+  if (err == cudaSuccess) count_launch();
+  return err;
 }
 }  // namespace
 
@@ -623,8 +625,8 @@ int launch_macroscopic(SlbmEngine* e, const double* canonical, double* dev_rho, 
   SLBM_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int), e->stream));
   by_lattice(e->q, [&](auto lat) {
     using L = decltype(lat);
-    k_macro<L><<<grid_for(e->n_fluid, 256), 256, 0, e->stream>>>(
-        src, a, odd, e->geo, compact ? nullptr : e->x_flat, dev_rho, dev_u, bad);
+    { k_macro<L><<<grid_for(e->n_fluid, 256), 256, 0, e->stream>>>(
+        src, a, odd, e->geo, compact ? nullptr : e->x_flat, dev_rho, dev_u, bad); slbm::count_launch(); }
   });
   int h_bad = 0;
   SLBM_CUDA_TRY(cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, e->stream));
@@ -642,8 +644,8 @@ int launch_macroscopic_box(SlbmEngine* e, double* rho, double* u) {
   SLBM_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int), e->stream));
   by_lattice(e->q, [&](auto lat) {
     using L = decltype(lat);
-    k_macro_box<L><<<grid_for(e->geo.n_cells(), kMacroBlock), kMacroBlock, 0, e->stream>>>(
-        e->pdf, a, odd, e->geo, e->cid_map, rho, u, bad);
+    { k_macro_box<L><<<grid_for(e->geo.n_cells(), kMacroBlock), kMacroBlock, 0, e->stream>>>(
+        e->pdf, a, odd, e->geo, e->cid_map, rho, u, bad); slbm::count_launch(); }
   });
   SLBM_CUDA_TRY(cudaGetLastError());
   int h_bad = 0;
@@ -659,8 +661,8 @@ int launch_equilibrium(SlbmEngine* e, const double* rho, int rho_scalar, const d
   SweepArgs a = sweep_args(e);
   by_lattice(e->q, [&](auto lat) {
     using L = decltype(lat);
-    k_equilibrium<L><<<grid_for(e->n_fluid, 256), 256, 0, e->stream>>>(e->pdf, a, rho,
-                                                                         rho_scalar, u, u_scalar);
+    { k_equilibrium<L><<<grid_for(e->n_fluid, 256), 256, 0, e->stream>>>(e->pdf, a, rho,
+                                                                         rho_scalar, u, u_scalar); slbm::count_launch(); }
   });
   SLBM_CUDA_TRY(cudaGetLastError());
   return SLBM_OK;
@@ -673,8 +675,8 @@ int launch_equilibrium_qn(SlbmEngine* e, const double* rho, int rho_scalar, cons
   for (int q = 0; q < 28; ++q) a.base[q] = uint32_t(q) * uint32_t(e->n_fluid);
   by_lattice(e->q, [&](auto lat) {
     using L = decltype(lat);
-    k_equilibrium<L><<<grid_for(e->n_fluid, 256), 256, 0, e->stream>>>(out, a, rho, rho_scalar,
-                                                                         u, u_scalar);
+    { k_equilibrium<L><<<grid_for(e->n_fluid, 256), 256, 0, e->stream>>>(out, a, rho, rho_scalar,
+                                                                         u, u_scalar); slbm::count_launch(); }
   });
   SLBM_CUDA_TRY(cudaGetLastError());
   return SLBM_OK;
@@ -683,7 +685,7 @@ int launch_equilibrium_qn(SlbmEngine* e, const double* rho, int rho_scalar, cons
 int launch_gather(const double* src, const uint32_t* slots, int64_t n, double* out,
                   cudaStream_t s) {
   if (n == 0) return SLBM_OK;
-  k_gather<<<grid_for(n, 256), 256, 0, s>>>(src, slots, n, out);
+  { k_gather<<<grid_for(n, 256), 256, 0, s>>>(src, slots, n, out); slbm::count_launch(); }
   SLBM_CUDA_TRY(cudaGetLastError());
   return SLBM_OK;
 }
@@ -691,7 +693,7 @@ int launch_gather(const double* src, const uint32_t* slots, int64_t n, double* o
 int launch_scatter(double* dst, const uint32_t* slots, int64_t n, const double* in,
                    cudaStream_t s) {
   if (n == 0) return SLBM_OK;
-  k_scatter<<<grid_for(n, 256), 256, 0, s>>>(dst, slots, n, in);
+  { k_scatter<<<grid_for(n, 256), 256, 0, s>>>(dst, slots, n, in); slbm::count_launch(); }
   SLBM_CUDA_TRY(cudaGetLastError());
   return SLBM_OK;
 }
@@ -700,7 +702,7 @@ int launch_fill(double* p, int64_t n, double v, cudaStream_t s) {
   if (n == 0) return SLBM_OK;
   unsigned g = grid_for(n, 256);
   if (g > 148 * 32) g = 148 * 32;
-  k_fill<<<g, 256, 0, s>>>(p, n, v);
+  { k_fill<<<g, 256, 0, s>>>(p, n, v); slbm::count_launch(); }
   SLBM_CUDA_TRY(cudaGetLastError());
   return SLBM_OK;
 }

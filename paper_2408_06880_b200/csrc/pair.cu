@@ -445,8 +445,8 @@ int group_entries(SlbmEngine* e, const uint32_t* slot, const uint32_t* partner, 
   SLBM_CUDA_TRY(cudaMallocAsync(slot_sorted, nb, s));
   SLBM_CUDA_TRY(cudaMallocAsync(slot_entry, nb, s));
   if (n > 0) {
-    k_entry_keys<<<blocks(n), 256, 0, s>>>(slot, partner, uint32_t(n), uint32_t(e->n_fluid), e->q,
-                                           pb, tile, ent, skey);
+    { k_entry_keys<<<blocks(n), 256, 0, s>>>(slot, partner, uint32_t(n), uint32_t(e->n_fluid), e->q,
+                                           pb, tile, ent, skey); slbm::count_launch(); }
     size_t tb = 0, tb2 = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tb, tile, tile2, ent, *perm, int(n), 0, 32, s);
     cub::DeviceRadixSort::SortPairs(nullptr, tb2, skey, *slot_sorted, ent, ent2, int(n), 0, 32, s);
@@ -456,7 +456,7 @@ int group_entries(SlbmEngine* e, const uint32_t* slot, const uint32_t* partner, 
     cub::DeviceRadixSort::SortPairs(tmp, tb2, skey, *slot_sorted, ent, *slot_entry, int(n), 0, 32, s);
     SLBM_CUDA_TRY(cudaFreeAsync(tmp, s));
   }
-  k_tile_starts<<<blocks(n_tiles + 1), 256, 0, s>>>(tile2, uint32_t(n), n_tiles, *start);
+  { k_tile_starts<<<blocks(n_tiles + 1), 256, 0, s>>>(tile2, uint32_t(n), n_tiles, *start); slbm::count_launch(); }
   SLBM_CUDA_TRY(cudaFreeAsync(tile, s));
   SLBM_CUDA_TRY(cudaFreeAsync(tile2, s));
   SLBM_CUDA_TRY(cudaFreeAsync(ent, s));
@@ -491,21 +491,21 @@ int build_pair_plan(SlbmEngine* e) {
   SLBM_CUDA_TRY(cudaMallocAsync(&val, tb, s));
   SLBM_CUDA_TRY(cudaMallocAsync(&key2, tb, s));
   SLBM_CUDA_TRY(cudaMallocAsync(&val2, tb, s));
-  k_pair_dep_init<<<blocks(n_tiles), 256, 0, s>>>(p->dep, n_tiles);
-  k_pair_deps<<<blocks(e->n_fluid), 256, 0, s>>>(
+  { k_pair_dep_init<<<blocks(n_tiles), 256, 0, s>>>(p->dep, n_tiles); slbm::count_launch(); }
+  { k_pair_deps<<<blocks(e->n_fluid), 256, 0, s>>>(
       e->idx, uint32_t(e->idx_pitch), uint32_t(e->n_fluid), e->q, pb, u_sorted, u_entry,
       e->ubb_partner, uint32_t(e->n_ubb), o_sorted, o_entry, e->out_partner, uint32_t(e->n_out),
-      p->dep);
+      p->dep); slbm::count_launch(); }
   const uint32_t slack =
       e->tune.pair_slack > 0 ? uint32_t(e->tune.pair_slack) : uint32_t(num_sms_pair() * 12);
-  k_pair_keys<<<blocks(n_tiles), 256, 0, s>>>(p->dep, n_tiles, slack, key, val);
+  { k_pair_keys<<<blocks(n_tiles), 256, 0, s>>>(p->dep, n_tiles, slack, key, val); slbm::count_launch(); }
   size_t tmpb = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tmpb, key, key2, val, val2, int(n_tiles), 0, 32, s);
   void* tmp = nullptr;
   SLBM_CUDA_TRY(cudaMallocAsync(&tmp, tmpb, s));
   cub::DeviceRadixSort::SortPairs(tmp, tmpb, key, key2, val, val2, int(n_tiles), 0, 32, s);
   SLBM_CUDA_TRY(cudaMalloc(&p->sched, size_t(p->n_items) * 4));
-  k_pair_sched<<<blocks(n_tiles), 256, 0, s>>>(key2, val2, n_tiles, p->sched);
+  { k_pair_sched<<<blocks(n_tiles), 256, 0, s>>>(key2, val2, n_tiles, p->sched); slbm::count_launch(); }
   SLBM_CUDA_TRY(cudaMalloc(&p->chunk_done, size_t(p->n_chunks) * 4));
   SLBM_CUDA_TRY(cudaMalloc(&p->ctl, 16 * 4));
   SLBM_CUDA_TRY(cudaMemsetAsync(p->chunk_done, 0, size_t(p->n_chunks) * 4, s));
@@ -531,7 +531,7 @@ void pair_launch(const PairArgs& a, cudaStream_t s) {
   // one wave: every warp resident (the deadlock-freedom condition)
   const int64_t grid = std::min<int64_t>((a.n_items + kCTA / 32 - 1) / (kCTA / 32),
                                          int64_t(per_sm) * num_sms_pair());
-  k_pair<L, MODEL, MINB><<<unsigned(std::max<int64_t>(grid, 1)), kCTA, 0, s>>>(a);
+  { k_pair<L, MODEL, MINB><<<unsigned(std::max<int64_t>(grid, 1)), kCTA, 0, s>>>(a); slbm::count_launch(); }
 }
 
 }  // namespace

@@ -409,3 +409,40 @@ def make_stencil_d3q19():
     from paper_2408_06880_b200.lattice import make_stencil
 
     return make_stencil("d3q19")
+
+
+def test_launch_count_is_graph_aware(gpu_lib):
+    """slbm_launch_count (bench.py's gpu_launches): eager steps count their
+    kernels, a CUDA-graph replay counts the kernels it captured, the
+    resident path one cooperative launch; engine and domain graphs."""
+    from paper_2408_06880_b200 import _abi, geometry
+    from paper_2408_06880_b200.collision import CollisionParams
+    from paper_2408_06880_b200.domain import Domain
+    from paper_2408_06880_b200.lattice import make_stencil
+
+    st = make_stencil("d3q19")
+    p = CollisionParams(1.3, "trt", 0.9)
+    fl = geometry.riverbed_flags((24, 16, 16), (8, 8, 8), 0.5, 7, 0.03)
+    eng = _engine(fl, st, p, "aa")
+    eng.set_tuning(4, 0)  # no resident kernel
+    eng.init_equilibrium()
+    c0 = _abi.launch_count()
+    drive(eng, 2)
+    eager = _abi.launch_count() - c0
+    assert eager >= 4  # refresh + sweep + step counter per step (lid: refresh launches)
+    c0 = _abi.launch_count()
+    eng.run(10, use_graph=True)
+    assert _abi.launch_count() - c0 == 5 * eager
+    eng.set_tuning(4, 1 << 19)  # resident: n steps in one cooperative launch
+    c0 = _abi.launch_count()
+    eng.run(10, use_graph=True)
+    assert _abi.launch_count() - c0 == 1
+    dom = Domain(fl, (8, 8, 8), st, p, pattern="aa", frame_width=1, check="deferred")
+    dom.init_equilibrium()
+    c0 = _abi.launch_count()
+    dom.run(2, driver="overlapped")
+    eager = _abi.launch_count() - c0
+    dom.run(2, driver="overlapped", use_graph=True)  # capture + first replay
+    c0 = _abi.launch_count()
+    dom.run(4, driver="overlapped", use_graph=True)
+    assert _abi.launch_count() - c0 == 2 * eager > 0
