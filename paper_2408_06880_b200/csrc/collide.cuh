@@ -132,13 +132,13 @@ __device__ __forceinline__ void feq_pair(const Moments<L>& m, double& fe, double
   feb = wr * (((1.0 - a) + b) - c);
 }
 
-// returns true when the cell is unstable (the values are still produced)
+// SRT / TRT relaxation given the cell's moments; true when unstable
 template <class L, int MODEL, class TV, class Sink>
-__device__ __forceinline__ bool collide(const TV& t, double omega, double lam, Sink&& sink) {
-  if constexpr (MODEL == SLBM_CUMULANT) {
-    return cumulant_collide<L>(t, omega, sink);
-  } else {
-    const Moments<L> m = moments<L>(t);
+__device__ __forceinline__ bool relax(const TV& t, const Moments<L>& m, double omega, double lam,
+                                      Sink&& sink) {
+  static_assert(MODEL != SLBM_CUMULANT, "cumulant relaxes in moment space (cumulant.cuh)");
+  {
+    const double ho = 0.5 * omega, hl = 0.5 * lam;  // TRT: exact halvings
     // rest direction: cu = 0, so poly = (1 + 0) - 1.5usq exactly, and the
     // TRT form reduces to the SRT form (sym = t0, asym = +0) bit for bit
     {
@@ -160,18 +160,30 @@ __device__ __forceinline__ bool collide(const TV& t, double omega, double lam, S
           // asym, asym_eq are exact negations, so
           //   out_q  = (t_q  - A) - B,   out_qb = (t_qb - A) + B
           // with A = we (sym - sym_eq), B = wo (asym - asym_eq).
-          const double sym = 0.5 * (t[q] + t[qb]);
-          const double asym = 0.5 * (t[q] - t[qb]);
-          const double sym_eq = 0.5 * (fe + feb);
-          const double asym_eq = 0.5 * (fe - feb);
-          const double A = omega * (sym - sym_eq);
-          const double B = lam * (asym - asym_eq);
+          // Halving is exact and commutes with round-to-nearest, so
+          //   we * (0.5 S - 0.5 Se) == (0.5 we) * (S - Se)
+          // bit for bit (S = t_q + t_qb, Se = fe + feb, same for the
+          // differences): 4 fp64 multiplies fewer per pair.  (Exact unless
+          // S - Se is subnormal, which a difference of two PDFs >= 2^-970
+          // in magnitude cannot be.)
+          const double A = ho * ((t[q] + t[qb]) - (fe + feb));
+          const double B = hl * ((t[q] - t[qb]) - (fe - feb));
           sink(q, (t[q] - A) - B);
           sink(std::integral_constant<int, qb>{}, (t[qb] - A) + B);
         }
       }
     });
     return m.bad;
+  }
+}
+
+// returns true when the cell is unstable (the values are still produced)
+template <class L, int MODEL, class TV, class Sink>
+__device__ __forceinline__ bool collide(const TV& t, double omega, double lam, Sink&& sink) {
+  if constexpr (MODEL == SLBM_CUMULANT) {
+    return cumulant_collide<L>(t, omega, sink);
+  } else {
+    return relax<L, MODEL>(t, moments<L>(t), omega, lam, sink);
   }
 }
 

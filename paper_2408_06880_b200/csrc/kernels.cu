@@ -77,7 +77,10 @@ enum Kind { kPull = 0, kEven = 1, kOdd = 2 };
 // (16-bit deltas against a per-32-cell base, escapes for folds/halo: 342
 // instead of 376 B/cell, -4% burst / -2.5% sustained: more load
 // instructions than bytes saved); FMA contraction (no change under the
-// power cap, which costs the sweep ~6% of SM clock) — all slower than the
+// power cap, which costs the sweep ~6% of SM clock); round 2: the gather
+// straight into shared memory (cp.async, one-pass moments from the staged
+// column) at 6 CTAs/SM, 78-80 registers (bed 0.86 vs 0.97, C5 phi 0.3 0.81
+// vs 0.82) or 8 CTAs/SM with spills (0.72 / 0.68) — all slower than the
 // plain gather.  What pays is the L2 prefetch of the index list one quarter
 // wave ahead (sweep.cuh): +7-9%.
 template <class L, int MODEL, int KIND, int MINB, bool PF>

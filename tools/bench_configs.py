@@ -240,6 +240,11 @@ def c5(steps):
         eng.poll()
         nf = eng.n_fluid
         mfl = nf * steps / ms * 1e3 / 1e6
+        # per-kernel: the reference loop with an event after every step
+        stream = torch.cuda.ExternalStream(eng.stream())
+        _, te, to = bench.timed_steps(eng, max(20, min(steps, 200)), torch, stream)
+        even_frac = nf * bench.BYTES_EVEN / (te / 1e3) / 1e9 / HBM
+        odd_frac = nf * bench.BYTES_ODD / (to / 1e3) / 1e9 / HBM
         sparse_bytes = eng.device_bytes
         del eng
         # measured dense (direct-addressing) engine on the same geometry
@@ -258,6 +263,8 @@ def c5(steps):
               "dense_equivalent_mflups_model": round(dense_equiv, 1),
               "sparse_over_dense_measured": round(mfl / mfl_d, 3),
               "pair_frac": round(mfl * 1e6 * 340 / (HBM * 1e9), 4),
+              "even_frac": round(even_frac, 4), "odd_frac": round(odd_frac, 4),
+              "ms_even": round(te, 4), "ms_odd": round(to, 4),
               "device_bytes": sparse_bytes, "dense_device_bytes": dense_bytes,
               "model_memory_bytes": int(model_bytes),
               "device_bytes_per_fluid_cell": round(sparse_bytes / nf, 1)})

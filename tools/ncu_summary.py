@@ -92,8 +92,9 @@ def main():
         fh.write("\n".join(lines) + "\n")
     latest = {f"{k}_dram_bytes_per_launch": sum(v) / len(v) for k, v in traffic.items()}
     latest["source"] = f"profiles/{tag}_kernels.md"
-    with open(os.path.join(ROOT, "profiles", "latest_traffic.json"), "w") as fh:
-        json.dump(latest, fh, indent=1)
+    if os.environ.get("NO_TRAFFIC") != "1":  # other workloads must not feed the bench line
+        with open(os.path.join(ROOT, "profiles", "latest_traffic.json"), "w") as fh:
+            json.dump(latest, fh, indent=1)
     print("\n".join(lines))
     if len(sys.argv) > 3:
         summarize_launches(tag, sys.argv[3])

@@ -32,6 +32,11 @@ def main():
         phi = float(os.environ.get("PHI", 1.0))
         fl = geometry.obstacle_flags((edge,) * 3, phi, 1)
         eng = DenseEngine(fl, st, p, "aa", device=0, check="deferred")
+    elif os.environ.get("OBSTACLE"):  # C5: cell-wise random obstacles at porosity PHI
+        from paper_2408_06880_b200 import geometry
+
+        fl = geometry.obstacle_flags((edge,) * 3, float(os.environ.get("PHI", 0.3)), 1)
+        eng = SparseEngine(fl, st, p, "aa", device=0, check="deferred")
     else:
         fl = bench.make_flags(edge, 0)
         eng = SparseEngine(fl, st, p, "aa", device=0, check="deferred")

@@ -48,7 +48,12 @@ def main():
     odd_variants = [int(v) for v in os.environ.get("ODD_VARIANTS", "0,2").split(",")]
     st = make_stencil("d3q19" if q == 19 else "d3q27")
     p = CollisionParams(bench.OMEGA, model, bench.magic_lambda(bench.OMEGA))
-    fl = bench.make_flags(edge, 0)
+    if os.environ.get("OBSTACLE"):  # C5: cell-wise random obstacles at porosity PHI
+        from paper_2408_06880_b200 import geometry
+
+        fl = geometry.obstacle_flags((edge,) * 3, float(os.environ.get("PHI", 0.3)), 1)
+    else:
+        fl = bench.make_flags(edge, 0)
     eng = SparseEngine(fl, st, p, "aa", device=0, check="deferred")
     n = eng.n_fluid
     lib = _abi.load()
@@ -93,10 +98,12 @@ def main():
     small = bench.make_flags(48, 0)
     ref = None
     for v in [v for v in variants if v != 2]:  # 2 = memory probe, not LBM
+        if model == "cumulant" and v >= 3:
+            continue
         for ov in odd_variants:
-            lib.slbm_set_tuning(0, v)
-            lib.slbm_set_tuning(1, ov)
             e = SparseEngine(small, st, p, "aa", device=0)
+            e.set_tuning(0, v)
+            e.set_tuning(1, ov)
             e.init_equilibrium(1.0, np.array([0.02, 0.01, 0.0]))
             e.run(6, use_graph=False)
             s = e.canonical_state()
