@@ -41,6 +41,9 @@ extern "C" {
 #define SLBM_SRT 0
 #define SLBM_TRT 1
 #define SLBM_CUMULANT 2
+/* internal model code: the cumulant with general higher-order rates, chosen
+ * by slbm_engine_set_cumulant_rates (create engines with SLBM_CUMULANT) */
+#define SLBM_CUMULANT_GEN 3
 
 /* streaming patterns (sparse.py:45) */
 #define SLBM_PULL 0
@@ -107,6 +110,13 @@ int slbm_engine_info(const SlbmEngine* eng, SlbmInfo* info);
 int slbm_engine_stream(const SlbmEngine* eng, void** stream);
 int slbm_engine_set_stream(SlbmEngine* eng, void* stream);
 int slbm_engine_set_params(SlbmEngine* eng, int model, double omega, double lambda_odd);
+/* Cumulant relaxation rates beyond the shear rate omega (Geier et al. 2015;
+ * extension, unpinned): bulk = w2 (trace of the second-order cumulants) and
+ * higher = {w3, w4, w5, w6, w7, w8, w9, w10} (NULL: all 1).  All higher
+ * rates 1 selects the closed-form kernel, anything else (or force_general)
+ * the general one.  The engine must use the cumulant model.                */
+int slbm_engine_set_cumulant_rates(SlbmEngine* eng, double bulk, const double* higher,
+                                   int force_general);
 
 /* ---- exported lists (for parity checks against the reference) -----------
  * idx: (q-1, n_fluid) uint32 (sparse.py:186); fluid_coords: (n_fluid, dim)

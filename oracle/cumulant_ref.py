@@ -5,7 +5,7 @@ CPU restatement of the D3Q27 cumulant collision implemented in
 cumulant model, so this is NOT pinned to the reference; it is
 an independent numpy transcription of the same algorithm (Geier et al.
 2015, non-parametrised: shear rate omega, bulk and all higher orders rate
-1) with the identical floating-point operation order, so the CUDA kernel
+1; the bulk rate is a parameter) with the identical floating-point operation order, so the CUDA kernel
 can be checked bit for bit against it, and it is itself checked against
 physics: mass/momentum conservation, the product-form equilibrium as a
 fixed point, omega = 1 giving that equilibrium, and the shear-wave decay
@@ -60,8 +60,10 @@ def _back3_odd(k1, c):
     return (k1 * c["bm"]) * 0.5, -(k1 * c["b0"]), (k1 * c["bp"]) * 0.5
 
 
-def cumulant_collide(t, omega, st):
-    """(27, n) pre-collision values -> (27, n) post-collision values."""
+def cumulant_collide(t, omega, st, bulk=1.0):
+    """(27, n) pre-collision values -> (27, n) post-collision values; shear
+    rate omega, bulk rate ``bulk`` (trace of the second order), higher
+    orders rate 1 (cumulant.cuh cumulant_collide, same operation order)."""
     assert st.q == 27
     rho, (ux, uy, uz) = moments_seedless(t, st)
     c = st.c
@@ -77,7 +79,8 @@ def cumulant_collide(t, omega, st):
     om1 = 1.0 - omega
     dxy = om1 * (kxx - kyy)
     dxz = om1 * (kxx - kzz)
-    sxx = ((rho + dxy) + dxz) / 3.0
+    tr = rho + (1.0 - bulk) * (((kxx + kyy) + kzz) - rho)
+    sxx = ((tr + dxy) + dxz) / 3.0
     syy = sxx - dxy
     szz = sxx - dxz
     sxy, sxz, syz = om1 * kxy, om1 * kxz, om1 * kyz

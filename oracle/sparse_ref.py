@@ -80,10 +80,17 @@ def collide(t, params, st):
     """core.py:149-170 (SRT / TRT); "cumulant" -> oracle/cumulant_ref.py
     (not in the reference, unpinned)"""
     if params.model == "cumulant":
+        moments(t, st)  # same instability check as every collision
+        higher = getattr(params, "higher_omegas", None)
+        bulk = float(getattr(params, "bulk_omega", 1.0))
+        if higher is not None and any(float(w) != 1.0 for w in higher):
+            # general rates: the independent restatement (tolerance, not bits)
+            from .cumulant_geier import collide_general
+
+            return collide_general(t, params.omega, bulk, higher, st)
         from .cumulant_ref import cumulant_collide
 
-        moments(t, st)  # same instability check as every collision
-        return cumulant_collide(t, params.omega, st)
+        return cumulant_collide(t, params.omega, st, bulk)
     rho, u = moments(t, st)
     feq = equilibrium(rho, u, st)
     if params.model == "srt":

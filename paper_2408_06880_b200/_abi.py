@@ -57,6 +57,7 @@ SIGNATURES = {
     "slbm_engine_stream": [vp, C.POINTER(vp)],
     "slbm_engine_set_stream": [vp, vp],
     "slbm_engine_set_params": [vp, C.c_int, C.c_double, C.c_double],
+    "slbm_engine_set_cumulant_rates": [vp, C.c_double, C.POINTER(C.c_double), C.c_int],
     "slbm_export_lists": [vp, c_u32p, c_i64p, c_i64p, c_i64p, c_dp, c_i64p, c_i64p, c_i64p],
     "slbm_export_split": [vp, c_i64p, c_i64p],
     "slbm_init_canonical": [vp, c_dp],

@@ -65,9 +65,17 @@ def as_parity(parity):
 
 @dataclass
 class CollisionParams:
+    """Reference fields (core.py:50-74) plus, for the cumulant model only
+    (extension, unpinned; Geier et al. 2015 §4): ``bulk_omega`` = w2, the
+    rate of the trace of the second-order cumulants (bulk viscosity
+    zeta = 2/9 (1/w2 - 1/2)), and ``higher_omegas`` = (w3, ..., w10) for the
+    third- to sixth-order cumulants (None: all 1, the closed-form kernel)."""
+
     omega: float
     model: str = "srt"
     lambda_odd: float | None = None
+    bulk_omega: float = 1.0
+    higher_omegas: tuple | None = None
 
     def __post_init__(self) -> None:
         if not (0.0 < self.omega < 2.0):
@@ -81,6 +89,13 @@ class CollisionParams:
                 raise errors.make(
                     "ConfigurationError", f"lambda_odd must lie in (0, 2), got {self.lambda_odd}"
                 )
+        if self.model != "cumulant" and (self.bulk_omega != 1.0 or self.higher_omegas is not None):
+            raise errors.make("ConfigurationError", "bulk / higher-order rates are cumulant-only")
+        rates = [self.bulk_omega] + list(self.higher_omegas or [])
+        if self.higher_omegas is not None and len(self.higher_omegas) != 8:
+            raise errors.make("ConfigurationError", "higher_omegas needs 8 rates (w3..w10)")
+        if not all(0.0 < float(w) < 2.0 for w in rates):
+            raise errors.make("ConfigurationError", f"cumulant rates must lie in (0, 2), got {rates}")
 
 
 def omega_from_viscosity(nu: float) -> float:
@@ -107,5 +122,13 @@ def params_code(params) -> tuple[int, float, float]:
     model = getattr(params, "model", "srt")
     if model not in MODEL_CODE:
         raise errors.make("ConfigurationError", f"unknown collision model {model!r}")
+    if model == "cumulant":  # the second rate word carries the bulk rate
+        return MODEL_CODE[model], float(params.omega), float(getattr(params, "bulk_omega", 1.0))
     lam = getattr(params, "lambda_odd", None)
     return MODEL_CODE[model], float(params.omega), float(lam if lam is not None else params.omega)
+
+
+def cumulant_rates(params):
+    """(bulk, higher (8,) or None) of a cumulant CollisionParams (duck-typed)."""
+    higher = getattr(params, "higher_omegas", None)
+    return float(getattr(params, "bulk_omega", 1.0)), (None if higher is None else tuple(higher))

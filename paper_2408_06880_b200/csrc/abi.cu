@@ -92,13 +92,14 @@ void free_engine(SlbmEngine* e) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (e->h_bad) cudaFreeHost(e->h_bad);
+  if (e->d_hr) cudaFree(e->d_hr);
   if (e->own_stream) cudaStreamDestroy(e->own_stream);
   delete e;
 }
 
 int check_model(int q, int model) {
   if (model == SLBM_SRT || model == SLBM_TRT) return SLBM_OK;
-  if (model == SLBM_CUMULANT) {
+  if (model == SLBM_CUMULANT) {  // general rates: slbm_engine_set_cumulant_rates
     if (q != 27) return fail(SLBM_ECONFIG, "cumulant collision needs the d3q27 stencil");
     return SLBM_OK;
   }
@@ -375,6 +376,35 @@ int slbm_engine_set_params(SlbmEngine* e, int model, double omega, double lambda
   e->model = model;
   e->omega = omega;
   e->lambda_odd = lambda_odd;
+  for (double& w : e->hr) w = 1.0;  // back to the closed-form cumulant
+  for (auto& gx : e->graph)
+    if (gx) {
+      cudaGraphExecDestroy(gx);
+      gx = nullptr;
+    }
+  return SLBM_OK;
+}
+
+int slbm_engine_set_cumulant_rates(SlbmEngine* e, double bulk, const double* higher,
+                                   int force_general) {
+  CHECK_ENGINE(e);
+  if (e->model != SLBM_CUMULANT && e->model != SLBM_CUMULANT_GEN)
+    return fail(SLBM_ECONFIG, "cumulant rates need an engine with the cumulant model");
+  double hr[8] = {1, 1, 1, 1, 1, 1, 1, 1};
+  if (higher)
+    for (int k = 0; k < 8; ++k) hr[k] = higher[k];
+  auto ok = [](double w) { return std::isfinite(w) && w > 0.0 && w < 2.0; };
+  if (!ok(bulk)) return fail(SLBM_ECONFIG, "bulk rate must lie in (0, 2)");
+  for (int k = 0; k < 8; ++k)
+    if (!ok(hr[k])) return fail(SLBM_ECONFIG, "higher-order cumulant rates must lie in (0, 2)");
+  bool general = force_general != 0;
+  for (int k = 0; k < 8; ++k) general = general || hr[k] != 1.0;
+  DeviceGuard guard(e->device);
+  if (general && !e->d_hr) SLBM_CUDA_TRY(cudaMalloc(&e->d_hr, sizeof(hr)));
+  if (e->d_hr) SLBM_CUDA_TRY(cudaMemcpy(e->d_hr, hr, sizeof(hr), cudaMemcpyHostToDevice));
+  std::memcpy(e->hr, hr, sizeof(hr));
+  e->lambda_odd = bulk;
+  e->model = general ? SLBM_CUMULANT_GEN : SLBM_CUMULANT;
   for (auto& gx : e->graph)
     if (gx) {
       cudaGraphExecDestroy(gx);

@@ -136,7 +136,7 @@ __device__ __forceinline__ void feq_pair(const Moments<L>& m, double& fe, double
 template <class L, int MODEL, class TV, class Sink>
 __device__ __forceinline__ bool relax(const TV& t, const Moments<L>& m, double omega, double lam,
                                       Sink&& sink) {
-  static_assert(MODEL != SLBM_CUMULANT, "cumulant relaxes in moment space (cumulant.cuh)");
+  static_assert(MODEL == SLBM_SRT || MODEL == SLBM_TRT, "cumulants relax in cumulant.cuh");
   {
     const double ho = 0.5 * omega, hl = 0.5 * lam;  // TRT: exact halvings
     // rest direction: cu = 0, so poly = (1 + 0) - 1.5usq exactly, and the
@@ -177,11 +177,15 @@ __device__ __forceinline__ bool relax(const TV& t, const Moments<L>& m, double o
   }
 }
 
-// returns true when the cell is unstable (the values are still produced)
+// returns true when the cell is unstable (the values are still produced).
+// Cumulant models: `lam` is the bulk rate, `hr` the higher-order rates.
 template <class L, int MODEL, class TV, class Sink>
-__device__ __forceinline__ bool collide(const TV& t, double omega, double lam, Sink&& sink) {
+__device__ __forceinline__ bool collide(const TV& t, double omega, double lam, Sink&& sink,
+                                        const double* hr = nullptr) {
   if constexpr (MODEL == SLBM_CUMULANT) {
-    return cumulant_collide<L>(t, omega, sink);
+    return cumulant_collide<L>(t, omega, lam, sink);
+  } else if constexpr (MODEL == SLBM_CUMULANT_GEN) {
+    return cumulant_collide_general<L>(t, omega, lam, hr, sink);
   } else {
     return relax<L, MODEL>(t, moments<L>(t), omega, lam, sink);
   }

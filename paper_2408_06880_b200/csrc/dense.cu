@@ -50,6 +50,7 @@ struct DenseArgs {
   int32_t frame_w[3];
   int phase;                // SLBM_PHASE_*
   double omega, lam;
+  const double* hr;         // cumulant: higher-order rates
   unsigned long long* bad;
   const unsigned long long* step;
 };
@@ -154,7 +155,7 @@ __global__ void __launch_bounds__(128, 4) k_dense(const DenseArgs a, uint32_t ah
     if (SPEC && m == kSolid) return;  // loads above were harmless reads
     bad = collide<L, MODEL>(t, a.omega, a.lam, [&](auto q, double v) {
       pdf[uint32_t(decltype(q)::value) * np + p] = v;
-    });
+    }, a.hr);
   } else {
     const bool face = x == 0 || x == X - 1 || y == 0 || y == Y - 1 ||
                       (L::DIM == 3 && (z == 0 || z == Z - 1));
@@ -203,12 +204,12 @@ __global__ void __launch_bounds__(128, 4) k_dense(const DenseArgs a, uint32_t ah
           if ((m & kHasUbb) && ((m >> qb) & 1u)) v = v + ubb_corr_of(a, i, qb);
         }
         pdf[addr[qb]] = v;
-      });
+      }, a.hr);
     } else {
       double* dst = a.dst;
       bad = collide<L, MODEL>(t, a.omega, a.lam, [&](auto q, double v) {
         dst[uint32_t(decltype(q)::value) * np + p] = v;
-      });
+      }, a.hr);
     }
   }
   if (bad) atomicMin(a.bad, *a.step);
@@ -226,6 +227,7 @@ struct DenseOddArgs {
   uint32_t X, Y, PX, PY, offz;
   uint32_t base[28];  // q * npad
   double omega, lam;
+  const double* hr;
   unsigned long long* bad;
   const unsigned long long* step;
 };
@@ -248,7 +250,7 @@ __global__ void __launch_bounds__(128, L::Q == 27 ? 5 : 6) k_dense_odd(const Den
   const bool fluid = a.mask[row * a.X + x] != kSolid;
   if (collide<L, MODEL>(t, a.omega, a.lam, [&](auto q, double v) {
         if (fluid) a.pdf[a.base[decltype(q)::value] + p] = v;
-      }) && fluid)
+      }, a.hr) && fluid)
     atomicMin(a.bad, *a.step);
 }
 
@@ -376,6 +378,7 @@ DenseArgs dense_args(SlbmEngine* e) {
   a.phase = SLBM_PHASE_ALL;
   a.omega = e->omega;
   a.lam = e->lambda_odd;
+  a.hr = e->d_hr;
   a.bad = e->d_bad;
   a.step = e->d_step;
   return a;
@@ -495,6 +498,7 @@ int dense_step(SlbmEngine* e, int phase) {
   for (int q = 0; q < 28 && q < e->q; ++q) oa.base[q] = uint32_t(q) * uint32_t(a.npad);
   oa.omega = a.omega;
   oa.lam = a.lam;
+  oa.hr = a.hr;
   oa.bad = a.bad;
   oa.step = a.step;
   with_lattice(e->q, [&](auto lat) {
@@ -521,8 +525,12 @@ int dense_step(SlbmEngine* e, int phase) {
       go(std::integral_constant<int, SLBM_SRT>{});
     else if (e->model == SLBM_TRT)
       go(std::integral_constant<int, SLBM_TRT>{});
-    else if constexpr (L::Q == 27)
-      go(std::integral_constant<int, SLBM_CUMULANT>{});
+    else if constexpr (L::Q == 27) {
+      if (e->model == SLBM_CUMULANT)
+        go(std::integral_constant<int, SLBM_CUMULANT>{});
+      else
+        go(std::integral_constant<int, SLBM_CUMULANT_GEN>{});
+    }
   });
   SLBM_CUDA_TRY(cudaGetLastError());
   return SLBM_OK;

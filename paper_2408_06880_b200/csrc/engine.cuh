@@ -35,7 +35,9 @@ struct SlbmEngine {
   int device = 0;
   int dim = 3, q = 19;
   int model = SLBM_SRT;
-  double omega = 1.0, lambda_odd = 1.0;
+  double omega = 1.0, lambda_odd = 1.0;  // cumulant: lambda_odd holds the bulk rate
+  double hr[8] = {1, 1, 1, 1, 1, 1, 1, 1};  // cumulant w3..w10 (host copy)
+  double* d_hr = nullptr;                   // ... on the device (general cumulant only)
   int pattern = SLBM_PULL;
   int parity = SLBM_EVEN;
   SlbmTuning tune = slbm::g_tuning_defaults;

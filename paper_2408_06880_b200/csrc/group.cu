@@ -14,6 +14,8 @@
 #include <vector>
 
 #include "collide.cuh"
+#include <cstring>
+
 #include "engine.cuh"
 #include "sweep.cuh"
 
@@ -42,6 +44,7 @@ struct SlbmGroup {
   int device = 0;
   int q = 19, model = SLBM_SRT, pattern = SLBM_AA;
   double omega = 1.0, lam = 1.0;
+  const double* hr = nullptr;  // cumulant: higher-order rates of the first engine
   std::vector<SlbmEngine*> engines;
   // tables[phase][flip] -> device array of GroupArgs (one per engine)
   GroupArgs* table[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
@@ -89,7 +92,8 @@ __device__ __forceinline__ int find_engine(const uint32_t* __restrict__ start, i
 template <class L, int MODEL, int KIND>
 __global__ void __launch_bounds__(kGB, KIND == 2 ? 6 : 4) k_group(const GroupArgs* __restrict__ table,
                                                   const uint32_t* __restrict__ start, int n_eng,
-                                                  double omega, double lam, uint32_t ahead) {
+                                                  double omega, double lam, const double* hr,
+                                                  uint32_t ahead) {
   // every thread finds its engine and reads the (tiny, L1-resident) table
   // row itself: no single-thread staging + __syncthreads at CTA start, which
   // cost ~15% of the even sweep (measured, tools/slab_probe.py)
@@ -118,14 +122,14 @@ __global__ void __launch_bounds__(kGB, KIND == 2 ? 6 : 4) k_group(const GroupArg
   if (c < a.lo || (a.skip && ((__ldg(a.skip + (c >> 5)) >> (c & 31)) & 1u))) return;
   bool bad;
   if constexpr (KIND == 2) {
-    bad = cell_local<L, MODEL>(a.pdf, a.base, c, omega, lam);
+    bad = cell_local<L, MODEL>(a.pdf, a.base, c, omega, lam, hr);
   } else {
     uint32_t s[L::Q];
     double t[L::Q];
     load_slots<L>(s, idx, pitch, c);
     gather<L>(t, a.pdf, s);
     if (cids) prefetch_idx_ahead<L::Q - 1, kGB>(idx, pitch, cids, n_cells, pos0, ahead);
-    bad = collide_scatter<L, MODEL, KIND == 1>(t, s, a.pdf, a.dst, a.base, c, omega, lam);
+    bad = collide_scatter<L, MODEL, KIND == 1>(t, s, a.pdf, a.dst, a.base, c, omega, lam, hr);
   }
   if (bad) atomicMin(a.bad, *a.step);
 }
@@ -212,7 +216,8 @@ int slbm_group_create(SlbmEngine** engines, int n, SlbmGroup** out) {
     if (e->layout != 0) return fail(SLBM_ECONFIG, "block groups hold sparse engines only");
     if (e->q != e0->q || e->model != e0->model || e->pattern != e0->pattern ||
         e->omega != e0->omega || e->lambda_odd != e0->lambda_odd || e->device != e0->device ||
-        e->parity != e0->parity || e->has_split != e0->has_split)
+        e->parity != e0->parity || e->has_split != e0->has_split ||
+        std::memcmp(e->hr, e0->hr, sizeof(e->hr)) != 0)
       return fail(SLBM_ECONFIG, "group engines must share stencil, collision, pattern, device "
                                 "and parity");
   }
@@ -224,6 +229,7 @@ int slbm_group_create(SlbmEngine** engines, int n, SlbmGroup** out) {
   g->pattern = e0->pattern;
   g->omega = e0->omega;
   g->lam = e0->lambda_odd;
+  g->hr = e0->d_hr;
   g->engines.assign(engines, engines + n);
   // pull: each engine's e->pdf is "current"; record the flip as 0
   for (int phase = 0; phase < 3; ++phase) {
@@ -355,20 +361,24 @@ int slbm_group_step(SlbmGroup* g, int phase, void* stream) {
       constexpr int M = decltype(mc)::value;
       if (kind == 0)
         { k_group<L, M, 0><<<g->n_cta[phase], kGB, 0, s>>>(tab, g->cta_start[phase], n, g->omega, g->lam,
-                                                           ahead); slbm::count_launch(); }
+                                                           g->hr, ahead); slbm::count_launch(); }
       else if (kind == 1)
         { k_group<L, M, 1><<<g->n_cta[phase], kGB, 0, s>>>(tab, g->cta_start[phase], n, g->omega, g->lam,
-                                                           ahead); slbm::count_launch(); }
+                                                           g->hr, ahead); slbm::count_launch(); }
       else
         { k_group<L, M, 2><<<g->n_cta[phase], kGB, 0, s>>>(tab, g->cta_start[phase], n, g->omega, g->lam,
-                                                           ahead); slbm::count_launch(); }
+                                                           g->hr, ahead); slbm::count_launch(); }
     };
     if (g->model == SLBM_SRT)
       go(std::integral_constant<int, SLBM_SRT>{});
     else if (g->model == SLBM_TRT)
       go(std::integral_constant<int, SLBM_TRT>{});
-    else if constexpr (L::Q == 27)
-      go(std::integral_constant<int, SLBM_CUMULANT>{});
+    else if constexpr (L::Q == 27) {
+      if (g->model == SLBM_CUMULANT)
+        go(std::integral_constant<int, SLBM_CUMULANT>{});
+      else
+        go(std::integral_constant<int, SLBM_CUMULANT_GEN>{});
+    }
   });
   SLBM_CUDA_TRY(cudaGetLastError());
   return SLBM_OK;

@@ -43,6 +43,7 @@ struct SweepArgs {
   uint32_t idx_pitch;  // elements per index-list row (256-B aligned rows)
   uint32_t base[28];   // device group starts (SlbmEngine::pbase)
   double omega, lam;
+  const double* hr;  // cumulant: higher-order rates w3..w10 (device)
   unsigned long long* bad;
   const unsigned long long* step;
 };
@@ -108,7 +109,7 @@ __global__ void __launch_bounds__(kIB, MINB) k_index_sweep(const SweepArgs a, ui
     if (a.cids != nullptr)
       prefetch_idx_ahead<L::Q - 1, kIB>(a.idx, a.idx_pitch, a.cids, a.n_cells, first, ahead);
   }
-  if (collide_scatter<L, MODEL, KIND == kEven>(t, s, a.pdf, a.dst, a.base, c, a.omega, a.lam))
+  if (collide_scatter<L, MODEL, KIND == kEven>(t, s, a.pdf, a.dst, a.base, c, a.omega, a.lam, a.hr))
     flag_bad(a);
 }
 
@@ -135,7 +136,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_aa_odd(const SweepArgs a) {
   if (i >= a.n_cells) return;
   const uint32_t c = a.cids ? a.cids[i] : a.offset + i;
   if (c < a.lo || (a.skip && ((__ldg(a.skip + (c >> 5)) >> (c & 31)) & 1u))) return;
-  if (cell_local<L, MODEL>(a.pdf, a.base, c, a.omega, a.lam)) flag_bad(a);
+  if (cell_local<L, MODEL>(a.pdf, a.base, c, a.omega, a.lam, a.hr)) flag_bad(a);
 }
 
 int num_sms() {
@@ -190,8 +191,12 @@ void launch_model(int model, int kind, const SweepArgs& a, unsigned grid, const 
     launch_kind<L, SLBM_SRT>(kind, a, grid, t, s);
   else if (model == SLBM_TRT)
     launch_kind<L, SLBM_TRT>(kind, a, grid, t, s);
-  else if constexpr (L::Q == 27)
-    launch_kind<L, SLBM_CUMULANT>(kind, a, grid, t, s);
+  else if constexpr (L::Q == 27) {
+    if (model == SLBM_CUMULANT)
+      launch_kind<L, SLBM_CUMULANT>(kind, a, grid, t, s);
+    else
+      launch_kind<L, SLBM_CUMULANT_GEN>(kind, a, grid, t, s);
+  }
 }
 
 __global__ void k_refresh(double* pdf, const uint32_t* slot, const uint32_t* partner,
@@ -266,12 +271,12 @@ __global__ void __launch_bounds__(kIB, MINB) k_resident(const SweepArgs a, const
         if (nxt < a.n_fluid) prefetch_idx_warp<L::Q - 1>(a.idx, a.idx_pitch, nxt, lane);
         load_slots<L>(s, a.idx, a.idx_pitch, c);
         gather<L>(t, cur, s);
-        bad |= r.pull ? collide_scatter<L, MODEL, false>(t, s, cur, oth, a.base, c, a.omega, a.lam)
-                      : collide_scatter<L, MODEL, true>(t, s, cur, oth, a.base, c, a.omega, a.lam);
+        bad |= r.pull ? collide_scatter<L, MODEL, false>(t, s, cur, oth, a.base, c, a.omega, a.lam, a.hr)
+                      : collide_scatter<L, MODEL, true>(t, s, cur, oth, a.base, c, a.omega, a.lam, a.hr);
       }
     } else {
       for (uint32_t c = tid; c < a.n_fluid; c += nth)
-        bad |= cell_local<L, MODEL>(cur, a.base, c, a.omega, a.lam);
+        bad |= cell_local<L, MODEL>(cur, a.base, c, a.omega, a.lam, a.hr);
     }
     if (bad) atomicMin(a.bad, step0 + k);
     grid.sync();
@@ -437,6 +442,7 @@ SweepArgs sweep_args(SlbmEngine* e) {
   for (int q = 0; q <= e->q && q < 28; ++q) a.base[q] = uint32_t(e->pbase[q]);
   a.omega = e->omega;
   a.lam = e->lambda_odd;
+  a.hr = e->d_hr;
   a.bad = e->d_bad;
   a.step = e->d_step;
   return a;
@@ -604,8 +610,12 @@ int launch_resident(SlbmEngine* e, int64_t n) {
       ce = resident_launch<L, SLBM_SRT>(a, r, e->stream);
     else if (e->model == SLBM_TRT)
       ce = resident_launch<L, SLBM_TRT>(a, r, e->stream);
-    else if constexpr (L::Q == 27)
-      ce = resident_launch<L, SLBM_CUMULANT>(a, r, e->stream);
+    else if constexpr (L::Q == 27) {
+      if (e->model == SLBM_CUMULANT)
+        ce = resident_launch<L, SLBM_CUMULANT>(a, r, e->stream);
+      else
+        ce = resident_launch<L, SLBM_CUMULANT_GEN>(a, r, e->stream);
+    }
   });
   if (ce != cudaSuccess) return fail(SLBM_ECUDA, std::string("resident sweep: ") + cudaGetErrorString(ce));
   return SLBM_OK;

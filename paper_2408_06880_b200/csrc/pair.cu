@@ -538,7 +538,7 @@ void pair_launch(const PairArgs& a, cudaStream_t s) {
 
 
 bool pair_eligible(const SlbmEngine* e) {
-  return e->tune.pair && e->layout == 0 && e->pattern == SLBM_AA && e->n_ghost == 0 &&
+  return e->tune.pair && e->model != SLBM_CUMULANT_GEN && e->layout == 0 && e->pattern == SLBM_AA && e->n_ghost == 0 &&
          e->n_fluid > 0 && e->n_fluid < (int64_t(1) << 31) / 2;
 }
 

@@ -107,15 +107,16 @@ __device__ __forceinline__ void gather(double (&t)[L::Q], const double* pdf,
 template <class L, int MODEL, bool EVEN>
 __device__ __forceinline__ bool collide_scatter(const double (&t)[L::Q], const uint32_t (&s)[L::Q],
                                                 double* pdf, double* dst, const uint32_t* base,
-                                                uint32_t c, double omega, double lam) {
+                                                uint32_t c, double omega, double lam,
+                                                const double* hr = nullptr) {
   if constexpr (EVEN) {
     return collide<L, MODEL>(t, omega, lam, [&](auto q, double v) {
       constexpr int qb = L::INV[decltype(q)::value];
       pdf[s[qb]] = v;
-    });
+    }, hr);
   } else {
     return collide<L, MODEL>(t, omega, lam,
-                             [&](auto q, double v) { dst[base[decltype(q)::value] + c] = v; });
+                             [&](auto q, double v) { dst[base[decltype(q)::value] + c] = v; }, hr);
   }
 }
 
@@ -133,14 +134,14 @@ __device__ __forceinline__ double ld_pdf(const double* p) {
 // groups, write the own groups — every access a coalesced row
 template <class L, int MODEL, bool CG = false>
 __device__ __forceinline__ bool cell_local(double* pdf, const uint32_t* base, uint32_t c,
-                                           double omega, double lam) {
+                                           double omega, double lam, const double* hr = nullptr) {
   double t[L::Q];
   sfor<0, L::Q>([&](auto q) {
     constexpr int qb = L::INV[q];
     t[q] = ld_pdf<CG>(pdf + base[qb] + c);
   });
   return collide<L, MODEL>(t, omega, lam,
-                           [&](auto q, double v) { pdf[base[decltype(q)::value] + c] = v; });
+                           [&](auto q, double v) { pdf[base[decltype(q)::value] + c] = v; }, hr);
 }
 
 // Fixed-density outlet (extension; the reference has none).

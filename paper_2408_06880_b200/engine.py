@@ -33,7 +33,7 @@ import os
 import numpy as np
 
 from . import _abi, errors
-from .collision import is_even, params_code, parity_class
+from .collision import cumulant_rates, is_even, params_code, parity_class
 from .counters import Counters
 from .lattice import stencil_code
 from .tags import OUTLET, UBB, rev_shape
@@ -139,6 +139,10 @@ class SparseEngine:
             C.byref(handle),
         )
         self._h = handle
+        if getattr(params, "model", "srt") == "cumulant":
+            bulk, higher = cumulant_rates(params)
+            if bulk != 1.0 or higher is not None:
+                self.set_cumulant_rates(bulk, higher)
         info = self.info()
         q = stencil.q
         self.n_fluid = int(info.n_fluid)
@@ -337,6 +341,15 @@ class SparseEngine:
 
     def synchronize(self) -> None:
         _abi.call("slbm_synchronize", self._h)
+
+    def set_cumulant_rates(self, bulk: float = 1.0, higher=None, force_general: bool = False) -> None:
+        """Cumulant model: bulk rate w2 and higher-order rates w3..w10
+        (include/slbm_b200.h slbm_engine_set_cumulant_rates)."""
+        arr = None
+        if higher is not None:
+            arr = np.ascontiguousarray(np.asarray(higher, dtype=np.float64).reshape(8))
+        _abi.call("slbm_engine_set_cumulant_rates", self._h, float(bulk),
+                  _abi.ptr(arr, C.c_double), 1 if force_general else 0)
 
     def set_tuning(self, knob: int, value: int) -> None:
         """Kernel-selection knob of THIS engine (include/slbm_b200.h, knobs
