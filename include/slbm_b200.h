@@ -279,7 +279,13 @@ int slbm_voxelize_spheres(const int32_t* dims, const double* centers, int64_t n,
 typedef struct SlbmGroup SlbmGroup;
 int slbm_group_create(SlbmEngine** engines, int n, SlbmGroup** out);
 int slbm_group_destroy(SlbmGroup* group);
+/* Per step: refresh (or boundary), the sweep(s), finish.  refresh = ONE
+ * launch: every engine's step counter + 1, UBB refresh and outlet of every
+ * block; boundary = the same launch also running `halo`'s device-local edges
+ * of `phase` (exchange.py:222-253 for blocks on this GPU).  finish only
+ * flips host state (the counters advanced in the boundary launch).        */
 int slbm_group_refresh(SlbmGroup* group, int parity, void* stream);
+int slbm_group_boundary(SlbmGroup* group, SlbmHalo* halo, int phase, int parity, void* stream);
 int slbm_group_step(SlbmGroup* group, int phase, void* stream);
 int slbm_group_finish(SlbmGroup* group, void* stream);
 

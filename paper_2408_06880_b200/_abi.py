@@ -113,6 +113,7 @@ SIGNATURES = {
     "slbm_group_create": [C.POINTER(vp), C.c_int, C.POINTER(vp)],
     "slbm_group_destroy": [vp],
     "slbm_group_refresh": [vp, C.c_int, vp],
+    "slbm_group_boundary": [vp, vp, C.c_int, C.c_int, vp],
     "slbm_group_step": [vp, C.c_int, vp],
     "slbm_group_finish": [vp, vp],
     "slbm_capture_begin": [vp],

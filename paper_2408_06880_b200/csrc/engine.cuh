@@ -123,6 +123,21 @@ struct SlbmEngine {
 
 namespace slbm {
 
+// Device-local halo edges of one phase (halo.cu), for kernels that run them
+// fused with other per-step work (group.cu k_group_boundary):
+// pdf[de[i]][ds[i]] = pdf[se[i]][ss[i]], engines indexed by the halo.
+constexpr int kMaxHaloEngines = 512;
+struct PdfTable {
+  double* p[kMaxHaloEngines];
+};
+struct LocalEdges {
+  const uint16_t *se = nullptr, *de = nullptr;
+  const uint32_t *ss = nullptr, *ds = nullptr;
+  int64_t n = 0;
+};
+// committed local program of `phase`; the table holds the engines' current pdf
+int halo_local_edges(SlbmHalo* h, int phase, PdfTable* table, LocalEdges* edges);
+
 // kernels / launchers implemented in kernels.cu
 int launch_step(SlbmEngine* e, int phase);
 int launch_refresh(SlbmEngine* e, int parity);

@@ -131,37 +131,52 @@ __global__ void __launch_bounds__(kGB, KIND == 2 ? 6 : 4) k_group(const GroupArg
     if (cids) prefetch_idx_ahead<L::Q - 1, kGB>(idx, pitch, cids, n_cells, pos0, ahead);
     bad = collide_scatter<L, MODEL, KIND == 1>(t, s, a.pdf, a.dst, a.base, c, omega, lam, hr);
   }
-  if (bad) atomicMin(a.bad, *a.step);
+  // the group's boundary kernel advanced the step counter before this sweep
+  if (bad) atomicMin(a.bad, *a.step - 1);
 }
 
-__global__ void k_group_refresh(const GroupArgs* table, const uint16_t* eng, const uint32_t* slot,
-                                const uint32_t* partner, const double* corr, int64_t n,
-                                int parity) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double* pdf = table[eng[i]].pdf;
-  if (parity == SLBM_EVEN)
-    pdf[slot[i]] = pdf[partner[i]] + corr[i];
-  else
-    pdf[partner[i]] = pdf[slot[i]] + corr[i];
-}
-
+// Everything a block group does between two sweeps, in ONE launch (the
+// strong-scaling small-share path: per-step fixed costs):
+//   * every engine's step counter += 1 (finish_step of the previous step's
+//     device half: the sweeps report an instability at *step - 1);
+//   * the device-local halo edges of this phase (exchange.py:222-253 for
+//     blocks on this GPU);
+//   * the UBB refresh (sparse.py:295-304) and the fixed-density outlet of
+//     every block.
+// The three programs touch disjoint slots -- a slot has exactly one upwind
+// source (a fluid cell of the own block, a cell of another block, or a wall)
+// -- and none reads a slot another writes, so they run concurrently; the
+// per-engine path (halo kernel, then refresh) gives the same bits.
 template <class L>
-__global__ void k_group_outlet(const GroupArgs* table, const OutletTab* ot, const uint16_t* eng,
-                               const uint32_t* idx, int64_t n, int parity) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int e = eng[i];
-  const uint32_t k = idx[i];
-  const OutletTab& o = ot[e];
-  const GroupArgs& a = table[e];
-  outlet_entry<L>(a.pdf, a.base, o.slot[k], o.partner[k], o.cell[k], o.dir[k], o.rho[k],
-                  o.u + 3 * size_t(k), parity);
-}
-
-__global__ void k_group_advance(unsigned long long** steps, int n) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) *steps[i] += 1;
+__global__ void k_group_boundary(PdfTable lt, LocalEdges le, const GroupArgs* table,
+                                 const uint16_t* ueng, const uint32_t* uslot,
+                                 const uint32_t* upartner, const double* ucorr, int64_t n_ubb,
+                                 const OutletTab* ot, const uint16_t* oeng, const uint32_t* oidx,
+                                 int64_t n_out, unsigned long long** steps, int n_eng, int parity) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n_eng) *steps[i] += 1;
+  if (i < le.n) {
+    lt.p[le.de[i]][le.ds[i]] = lt.p[le.se[i]][le.ss[i]];
+    return;
+  }
+  i -= le.n;
+  if (i < n_ubb) {
+    double* pdf = table[ueng[i]].pdf;
+    if (parity == SLBM_EVEN)
+      pdf[uslot[i]] = pdf[upartner[i]] + ucorr[i];
+    else
+      pdf[upartner[i]] = pdf[uslot[i]] + ucorr[i];
+    return;
+  }
+  i -= n_ubb;
+  if (i < n_out) {
+    const int e = oeng[i];
+    const uint32_t k = oidx[i];
+    const OutletTab& o = ot[e];
+    const GroupArgs& a = table[e];
+    outlet_entry<L>(a.pdf, a.base, o.slot[k], o.partner[k], o.cell[k], o.dir[k], o.rho[k],
+                    o.u + 3 * size_t(k), parity);
+  }
 }
 
 template <class F>
@@ -317,26 +332,34 @@ int slbm_group_destroy(SlbmGroup* g) {
   return SLBM_OK;
 }
 
-// refresh_boundary of every engine (sparse.py:295-304), on `stream`
+int group_boundary(SlbmGroup* g, SlbmHalo* halo, int phase, int parity, cudaStream_t s) {
+  PdfTable lt{};
+  LocalEdges le{};
+  if (halo) SLBM_TRY(halo_local_edges(halo, phase, &lt, &le));
+  const int flip = g->pattern == SLBM_PULL ? g->flip : 0;
+  const int n = int(g->engines.size());
+  const int64_t work = std::max<int64_t>(n, le.n + g->n_ubb + g->n_out);
+  on_lattice(g->q, [&](auto lat) {
+    using L = decltype(lat);
+    { k_group_boundary<L><<<unsigned((work + 127) / 128), 128, 0, s>>>(
+        lt, le, g->table[0][flip], g->ubb_eng, g->ubb_slot, g->ubb_partner, g->ubb_corr,
+        g->n_ubb, g->out_tab, g->out_eng, g->out_idx, g->n_out, g->steps, n, parity); slbm::count_launch(); }
+  });
+  SLBM_CUDA_TRY(cudaGetLastError());
+  return SLBM_OK;
+}
+
+// refresh_boundary of every engine (sparse.py:295-304) + the step counters,
+// one launch on `stream` (k_group_boundary without halo edges)
 int slbm_group_refresh(SlbmGroup* g, int parity, void* stream) {
   if (!g) return fail(SLBM_ECONFIG, "null group");
-  cudaStream_t s = (cudaStream_t)stream;
-  if (g->n_ubb) {
-    const int flip = g->pattern == SLBM_PULL ? g->flip : 0;
-    { k_group_refresh<<<unsigned((g->n_ubb + 255) / 256), 256, 0, s>>>(
-        g->table[0][flip], g->ubb_eng, g->ubb_slot, g->ubb_partner, g->ubb_corr, g->n_ubb, parity); slbm::count_launch(); }
-    SLBM_CUDA_TRY(cudaGetLastError());
-  }
-  if (g->n_out) {  // every outlet entry of every block: one launch
-    const int flip = g->pattern == SLBM_PULL ? g->flip : 0;
-    on_lattice(g->q, [&](auto lat) {
-      using L = decltype(lat);
-      { k_group_outlet<L><<<unsigned((g->n_out + 127) / 128), 128, 0, s>>>(
-          g->table[0][flip], g->out_tab, g->out_eng, g->out_idx, g->n_out, parity); slbm::count_launch(); }
-    });
-    SLBM_CUDA_TRY(cudaGetLastError());
-  }
-  return SLBM_OK;
+  return group_boundary(g, nullptr, 0, parity, (cudaStream_t)stream);
+}
+
+// ... and the device-local halo edges of `phase` of `halo` in the same launch
+int slbm_group_boundary(SlbmGroup* g, SlbmHalo* halo, int phase, int parity, void* stream) {
+  if (!g) return fail(SLBM_ECONFIG, "null group");
+  return group_boundary(g, halo, phase, parity, (cudaStream_t)stream);
 }
 
 // one sweep of `phase` over every engine of the group, one launch
@@ -384,8 +407,8 @@ int slbm_group_step(SlbmGroup* g, int phase, void* stream) {
   return SLBM_OK;
 }
 
-// finish_step of every engine (sparse.py:243-249): host state flips, one
-// device kernel advances all step counters
+// finish_step of every engine (sparse.py:243-249): host state flips; the
+// device step counters advance in the next step's boundary kernel
 int slbm_group_finish(SlbmGroup* g, void* stream) {
   if (!g) return fail(SLBM_ECONFIG, "null group");
   for (SlbmEngine* e : g->engines) {
@@ -396,8 +419,7 @@ int slbm_group_finish(SlbmGroup* g, void* stream) {
     e->steps_done += 1;
   }
   if (g->pattern == SLBM_PULL) g->flip ^= 1;
-  const int n = int(g->engines.size());
-  { k_group_advance<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(g->steps, n); slbm::count_launch(); }
+  (void)stream;
   SLBM_CUDA_TRY(cudaGetLastError());
   return SLBM_OK;
 }

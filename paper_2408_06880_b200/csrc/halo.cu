@@ -36,11 +36,7 @@
 namespace slbm {
 namespace {
 
-constexpr int kMaxEngines = 512;
-
-struct PdfTable {
-  double* p[kMaxEngines];
-};
+constexpr int kMaxEngines = kMaxHaloEngines;
 
 __global__ void k_local(PdfTable t, const uint16_t* se, const uint32_t* ss, const uint16_t* de,
                         const uint32_t* ds, int64_t n) {
@@ -466,6 +462,26 @@ int slbm_halo_commit(SlbmHalo* h, void* nccl_comm) {
   h->committed = true;
   return SLBM_OK;
 }
+
+}  // extern "C"
+
+namespace slbm {
+int halo_local_edges(SlbmHalo* h, int phase, PdfTable* table, LocalEdges* edges) {
+  if (!h || (phase != 0 && phase != 1)) return fail(SLBM_ECONFIG, "bad halo or phase");
+  *table = h->table();
+  *edges = LocalEdges{};
+  if (!h->committed) return SLBM_OK;  // no edges registered yet
+  const PhaseProg& p = h->ph[phase];
+  edges->se = p.d_lse;
+  edges->ss = p.d_lss;
+  edges->de = p.d_lde;
+  edges->ds = p.d_lds;
+  edges->n = p.n_local;
+  return SLBM_OK;
+}
+}  // namespace slbm
+
+extern "C" {
 
 int slbm_halo_local(SlbmHalo* h, int phase) {
   SLBM_TRY(check_phase(h, phase));

@@ -500,15 +500,24 @@ class Domain:
         den = sum(s[1] for s in self.overlap_samples)
         return num / den if den > 0 else 0.0
 
+    def _fused_boundary(self) -> bool:
+        """Local halo edges + refresh + step counters as one group launch."""
+        return self._group is not None and type(self._halo) is DeviceHalo
+
     def step_sequential(self) -> None:
         """exchange.py:330-346 on the device: exchange, then whole-block sweeps."""
         phase = phase_for(self.pattern, self.parity)
         e0 = self._mark("slbm.exchange")
-        self._halo.start(phase, self._stream)
-        self._halo.wait(self._stream)
-        self._sample(e0, None, None, self._mark("slbm.sweep"))
-        self._count_exchange(phase)
-        self._refresh_all()
+        if not self._has_remote and self._fused_boundary():
+            self._sample(e0, None, None, self._mark("slbm.sweep"))
+            self._count_exchange(phase)
+            self._group.boundary(self._halo, phase, self.parity, self._stream)
+        else:
+            self._halo.start(phase, self._stream)
+            self._halo.wait(self._stream)
+            self._sample(e0, None, None, self._mark("slbm.sweep"))
+            self._count_exchange(phase)
+            self._refresh_all()
         self._sweep("all")
         self._finish_all()
         self._mark()  # closes the last NVTX range
@@ -525,16 +534,22 @@ class Domain:
         overlapped driver reports."""
         phase = phase_for(self.pattern, self.parity)
         e0 = self._mark("slbm.exchange_start")
+        fused = self._fused_boundary() and (self._face_frames or not self._has_remote)
         if self._face_frames:
             # remote edges on the comm stream; local edges first on this one
             self._halo.start(phase, self._stream, with_local=False)
-            self._halo.local_on(phase, self._stream)
-        else:
+            if not fused:
+                self._halo.local_on(phase, self._stream)
+        elif not fused:
             self._halo.start(phase, self._stream)
         self._count_exchange(phase)
-        self._refresh_all()
+        if fused:  # local edges + refresh + step counters: one launch
+            self._group.boundary(self._halo, phase, self.parity, self._stream)
+        else:
+            self._refresh_all()
         if not self._has_remote:
-            self._halo.wait(self._stream)
+            if not fused:
+                self._halo.wait(self._stream)
             self._sample(e0, None, None, self._mark("slbm.sweep"))
             self._sweep("all")
             for e in self.local_engines():
@@ -739,6 +754,15 @@ class BlockGroup:
 
         _abi.call("slbm_group_refresh", self._h, int(getattr(parity, "value", parity)),
                   C.c_void_p(stream or 0))
+
+    def boundary(self, halo, phase, parity, stream):
+        """refresh + the halo's device-local edges of ``phase``, one launch."""
+        import ctypes as C
+
+        from . import _abi
+
+        _abi.call("slbm_group_boundary", self._h, halo.handle, int(phase.value),
+                  int(getattr(parity, "value", parity)), C.c_void_p(stream or 0))
 
     def step(self, phase: str, stream):
         import ctypes as C

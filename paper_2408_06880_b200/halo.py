@@ -206,6 +206,10 @@ class DeviceHalo:
         if peer is not None:
             _abi.call("slbm_halo_use_peer", self._h, int(peer[0]))
 
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
             _abi.load().slbm_halo_destroy(self._h)
