@@ -7,6 +7,7 @@
 #include <atomic>
 #include <string>
 #include <type_traits>
+#include <utility>
 
 #include "../../include/slbm_b200.h"
 #include "lattice_tables.h"
@@ -20,6 +21,37 @@ namespace slbm {
 // kernels that reached the GPU (cub / NCCL kernels are not counted).
 extern std::atomic<long long> g_launches;
 inline void count_launch(long long n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// ---- programmatic dependent launch (PDL) ---------------------------------
+// Per-step kernel chains (boundary -> sweep -> boundary ...) are launched with
+// programmatic stream serialization: a kernel's CTAs may be scheduled while
+// its predecessor drains.  Every kernel launched this way calls
+// pdl_launch_dependents() early and pdl_wait() in EVERY thread before it
+// touches data the predecessor writes (and before any early return), so
+// "completed" stays transitive along the chain.  Both are no-ops when the
+// kernel was launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <class... KArgs, class... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+  if (e == cudaSuccess) count_launch();
+  return e;
+}
 
 // ---- error plumbing -------------------------------------------------------
 void set_error(const std::string& msg);

@@ -50,6 +50,9 @@ struct SlbmGroup {
   GroupArgs* table[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
   uint32_t* cta_start[3] = {nullptr, nullptr, nullptr};
   uint32_t n_cta[3] = {0, 0, 0};
+  // the cell-local (odd) sweep: CTAs of kOddTiles tiles (own prefix)
+  uint32_t* cta_start_odd[3] = {nullptr, nullptr, nullptr};
+  uint32_t n_cta_odd[3] = {0, 0, 0};
   // batched UBB program
   uint16_t* ubb_eng = nullptr;
   uint32_t *ubb_slot = nullptr, *ubb_partner = nullptr;
@@ -76,6 +79,9 @@ struct OutletTab {
 namespace {
 
 constexpr int kGB = 128;
+// The odd sweep's CTAs stage their engine's table row in shared memory (one
+// barrier per CTA); two 128-cell tiles per CTA halve that per-cell cost.
+constexpr int kOddTiles = 2;
 
 __device__ __forceinline__ int find_engine(const uint32_t* __restrict__ start, int n, uint32_t cta) {
   int lo = 0, hi = n;  // last e with start[e] <= cta
@@ -107,7 +113,8 @@ __global__ void __launch_bounds__(kGB, KIND == 2 ? 6 : 4) k_group(const GroupArg
     __syncthreads();
   }
   const GroupArgs& a = KIND == 2 ? staged : table[eng];
-  const uint32_t pos0 = (blockIdx.x - first) * kGB;  // this CTA's first sweep position
+  constexpr int kTiles = KIND == 2 ? kOddTiles : 1;
+  const uint32_t pos0 = (blockIdx.x - first) * kGB * kTiles;  // this CTA's first sweep position
   const uint32_t* idx = a.idx;
   const uint32_t* cids = a.cids;
   const uint32_t pitch = a.idx_pitch, n_cells = a.n_cells, offset = a.offset;
@@ -116,20 +123,25 @@ __global__ void __launch_bounds__(kGB, KIND == 2 ? 6 : 4) k_group(const GroupArg
   if (KIND != 2 && cids == nullptr)
     prefetch_idx_ahead<L::Q - 1, kGB>(idx, pitch, nullptr, offset + n_cells, offset + pos0,
                                       ahead);
-  const uint32_t i = pos0 + threadIdx.x;
-  if (i >= n_cells) return;
-  const uint32_t c = cids ? cids[i] : offset + i;
-  if (c < a.lo || (a.skip && ((__ldg(a.skip + (c >> 5)) >> (c & 31)) & 1u))) return;
-  bool bad;
-  if constexpr (KIND == 2) {
-    bad = cell_local<L, MODEL>(a.pdf, a.base, c, omega, lam, hr);
-  } else {
-    uint32_t s[L::Q];
-    double t[L::Q];
-    load_slots<L>(s, idx, pitch, c);
-    gather<L>(t, a.pdf, s);
-    if (cids) prefetch_idx_ahead<L::Q - 1, kGB>(idx, pitch, cids, n_cells, pos0, ahead);
-    bad = collide_scatter<L, MODEL, KIND == 1>(t, s, a.pdf, a.dst, a.base, c, omega, lam, hr);
+  pdl_launch_dependents();
+  pdl_wait();  // the boundary kernel's halo / wall values (read-only lists above)
+  bool bad = false;
+#pragma unroll
+  for (int tile = 0; tile < kTiles; ++tile) {
+    const uint32_t i = pos0 + tile * kGB + threadIdx.x;
+    if (i >= n_cells) break;
+    const uint32_t c = cids ? cids[i] : offset + i;
+    if (c < a.lo || (a.skip && ((__ldg(a.skip + (c >> 5)) >> (c & 31)) & 1u))) continue;
+    if constexpr (KIND == 2) {
+      bad |= cell_local<L, MODEL>(a.pdf, a.base, c, omega, lam, hr);
+    } else {
+      uint32_t s[L::Q];
+      double t[L::Q];
+      load_slots<L>(s, idx, pitch, c);
+      gather<L>(t, a.pdf, s);
+      if (cids) prefetch_idx_ahead<L::Q - 1, kGB>(idx, pitch, cids, n_cells, pos0, ahead);
+      bad |= collide_scatter<L, MODEL, KIND == 1>(t, s, a.pdf, a.dst, a.base, c, omega, lam, hr);
+    }
   }
   // the group's boundary kernel advanced the step counter before this sweep
   if (bad) atomicMin(a.bad, *a.step - 1);
@@ -154,6 +166,8 @@ __global__ void k_group_boundary(PdfTable lt, LocalEdges le, const GroupArgs* ta
                                  const OutletTab* ot, const uint16_t* oeng, const uint32_t* oidx,
                                  int64_t n_out, unsigned long long** steps, int n_eng, int parity) {
   int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  pdl_launch_dependents();
+  pdl_wait();  // the previous sweep
   if (i < n_eng) *steps[i] += 1;
   if (i < le.n) {
     lt.p[le.de[i]][le.ds[i]] = lt.p[le.se[i]][le.ss[i]];
@@ -258,6 +272,15 @@ int slbm_group_create(SlbmEngine** engines, int n, SlbmGroup** out) {
     SLBM_CUDA_TRY(cudaMalloc(&g->cta_start[phase], (n + 1) * sizeof(uint32_t)));
     SLBM_CUDA_TRY(cudaMemcpy(g->cta_start[phase], start.data(), (n + 1) * sizeof(uint32_t),
                              cudaMemcpyHostToDevice));
+    std::vector<uint32_t> odd(n + 1, 0);
+    for (int i = 0; i < n; ++i) {
+      const GroupArgs a = args_of(engines[i], phase, 0);
+      odd[i + 1] = odd[i] + (a.n_cells + kGB * kOddTiles - 1) / (kGB * kOddTiles);
+    }
+    g->n_cta_odd[phase] = odd[n];
+    SLBM_CUDA_TRY(cudaMalloc(&g->cta_start_odd[phase], (n + 1) * sizeof(uint32_t)));
+    SLBM_CUDA_TRY(cudaMemcpy(g->cta_start_odd[phase], odd.data(), (n + 1) * sizeof(uint32_t),
+                             cudaMemcpyHostToDevice));
     for (int flip = 0; flip < 2; ++flip) {
       std::vector<GroupArgs> tab(n);
       for (int i = 0; i < n; ++i) tab[i] = args_of(engines[i], phase, flip);
@@ -276,9 +299,20 @@ int slbm_group_create(SlbmEngine** engines, int n, SlbmGroup** out) {
     for (int i = 0; i < n; ++i) {
       SlbmEngine* e = engines[i];
       tab[i] = OutletTab{e->out_slot, e->out_partner, e->out_cell, e->out_dir, e->out_rho, e->out_u};
-      for (int64_t k = 0; k < e->n_out; ++k) {
+      // entries in cell order: the (up to 5 / 9) entries of one cell sit in
+      // one warp and read its populations once (the engine's own order is by
+      // direction; each entry is independent, so the order is free)
+      std::vector<uint32_t> cell(size_t(e->n_out));
+      if (e->n_out)
+        SLBM_CUDA_TRY(cudaMemcpy(cell.data(), e->out_cell, e->n_out * sizeof(uint32_t),
+                                 cudaMemcpyDeviceToHost));
+      std::vector<uint32_t> order(size_t(e->n_out));
+      for (int64_t k = 0; k < e->n_out; ++k) order[k] = uint32_t(k);
+      std::stable_sort(order.begin(), order.end(),
+                       [&](uint32_t a, uint32_t b) { return cell[a] < cell[b]; });
+      for (uint32_t k : order) {
         oe.push_back(uint16_t(i));
-        oi.push_back(uint32_t(k));
+        oi.push_back(k);
       }
     }
     g->n_out = int64_t(oe.size());
@@ -323,6 +357,7 @@ int slbm_group_destroy(SlbmGroup* g) {
     for (int f = 0; f < 2; ++f)
       if (g->table[p][f]) cudaFree(g->table[p][f]);
     if (g->cta_start[p]) cudaFree(g->cta_start[p]);
+    if (g->cta_start_odd[p]) cudaFree(g->cta_start_odd[p]);
   }
   void* ptrs[] = {g->ubb_eng, g->ubb_slot, g->ubb_partner, g->ubb_corr, g->steps,
                   g->out_tab, g->out_eng, g->out_idx};
@@ -339,13 +374,15 @@ int group_boundary(SlbmGroup* g, SlbmHalo* halo, int phase, int parity, cudaStre
   const int flip = g->pattern == SLBM_PULL ? g->flip : 0;
   const int n = int(g->engines.size());
   const int64_t work = std::max<int64_t>(n, le.n + g->n_ubb + g->n_out);
+  cudaError_t err = cudaSuccess;
   on_lattice(g->q, [&](auto lat) {
     using L = decltype(lat);
-    { k_group_boundary<L><<<unsigned((work + 127) / 128), 128, 0, s>>>(
-        lt, le, g->table[0][flip], g->ubb_eng, g->ubb_slot, g->ubb_partner, g->ubb_corr,
-        g->n_ubb, g->out_tab, g->out_eng, g->out_idx, g->n_out, g->steps, n, parity); slbm::count_launch(); }
+    err = launch_pdl(k_group_boundary<L>, dim3(unsigned((work + 127) / 128)), dim3(128), 0, s,
+                     lt, le, g->table[0][flip], g->ubb_eng, g->ubb_slot, g->ubb_partner,
+                     g->ubb_corr, g->n_ubb, g->out_tab, g->out_eng, g->out_idx, g->n_out,
+                     g->steps, n, parity);
   });
-  SLBM_CUDA_TRY(cudaGetLastError());
+  SLBM_CUDA_TRY(err);
   return SLBM_OK;
 }
 
@@ -374,6 +411,7 @@ int slbm_group_step(SlbmGroup* g, int phase, void* stream) {
   const int flip = g->pattern == SLBM_PULL ? g->flip : 0;
   const GroupArgs* tab = g->table[phase][flip];
   const int n = int(g->engines.size());
+  cudaError_t err = cudaSuccess;
   on_lattice(g->q, [&](auto lat) {
     using L = decltype(lat);
     int dev = 0, sms = 148;
@@ -383,14 +421,14 @@ int slbm_group_step(SlbmGroup* g, int phase, void* stream) {
     auto go = [&](auto mc) {
       constexpr int M = decltype(mc)::value;
       if (kind == 0)
-        { k_group<L, M, 0><<<g->n_cta[phase], kGB, 0, s>>>(tab, g->cta_start[phase], n, g->omega, g->lam,
-                                                           g->hr, ahead); slbm::count_launch(); }
+        err = launch_pdl(k_group<L, M, 0>, dim3(g->n_cta[phase]), dim3(kGB), 0, s, tab,
+                         g->cta_start[phase], n, g->omega, g->lam, g->hr, ahead);
       else if (kind == 1)
-        { k_group<L, M, 1><<<g->n_cta[phase], kGB, 0, s>>>(tab, g->cta_start[phase], n, g->omega, g->lam,
-                                                           g->hr, ahead); slbm::count_launch(); }
+        err = launch_pdl(k_group<L, M, 1>, dim3(g->n_cta[phase]), dim3(kGB), 0, s, tab,
+                         g->cta_start[phase], n, g->omega, g->lam, g->hr, ahead);
       else
-        { k_group<L, M, 2><<<g->n_cta[phase], kGB, 0, s>>>(tab, g->cta_start[phase], n, g->omega, g->lam,
-                                                           g->hr, ahead); slbm::count_launch(); }
+        err = launch_pdl(k_group<L, M, 2>, dim3(g->n_cta_odd[phase]), dim3(kGB), 0, s, tab,
+                         g->cta_start_odd[phase], n, g->omega, g->lam, g->hr, ahead);
     };
     if (g->model == SLBM_SRT)
       go(std::integral_constant<int, SLBM_SRT>{});
@@ -403,7 +441,7 @@ int slbm_group_step(SlbmGroup* g, int phase, void* stream) {
         go(std::integral_constant<int, SLBM_CUMULANT_GEN>{});
     }
   });
-  SLBM_CUDA_TRY(cudaGetLastError());
+  SLBM_CUDA_TRY(err);
   return SLBM_OK;
 }
 

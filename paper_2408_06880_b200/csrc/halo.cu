@@ -402,6 +402,28 @@ int slbm_halo_commit(SlbmHalo* h, void* nccl_comm) {
   h->nccl = (ncclComm_t)nccl_comm;
   int64_t max_send = 0, max_recv = 0;
   for (auto& p : h->ph) {
+    {
+      // local entries in (destination engine, destination slot) order: each
+      // entry writes a distinct slot, so the order is free, and sorted the
+      // warp's writes are consecutive slots of one direction group and its
+      // reads (the same face cells upwind) follow them -- coalesced on both
+      // sides instead of cell-major x direction (C4: ~1.4 M entries a step)
+      const size_t n = p.l_se.size();
+      std::vector<size_t> ord(n);
+      for (size_t k = 0; k < n; ++k) ord[k] = k;
+      std::sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
+        return p.l_de[a] != p.l_de[b] ? p.l_de[a] < p.l_de[b] : p.l_ds[a] < p.l_ds[b];
+      });
+      auto perm = [&](auto& v) {
+        auto w = v;
+        for (size_t k = 0; k < n; ++k) w[k] = v[ord[k]];
+        v.swap(w);
+      };
+      perm(p.l_se);
+      perm(p.l_ss);
+      perm(p.l_de);
+      perm(p.l_ds);
+    }
     SLBM_TRY(upload(p.l_se, &p.d_lse));
     SLBM_TRY(upload(p.l_ss, &p.d_lss));
     SLBM_TRY(upload(p.l_de, &p.d_lde));
