@@ -11,7 +11,7 @@ timeout 1200 python -m pytest tests -m gpu -x -q ${PYTEST_ARGS} > gpurun_out/pyt
 fi
 timeout 600 python bench.py ${BENCH_ARGS:---steps 200 --warmup 10} > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/summary.txt
 if [ -z "$NO_NCU" ]; then
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 4 --warmup 3 --no-cpu > gpurun_out/ncu_launches.log 2>&1; echo "ncu launches rc=$?" >> gpurun_out/summary.txt
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 4 --warmup 3 --no-cpu --sustained-s 0 > gpurun_out/ncu_launches.log 2>&1; echo "ncu launches rc=$?" >> gpurun_out/summary.txt
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_index_sweep|k_aa_odd" -s 2 -c 2 -o gpurun_out/prof_aa -f python tools/profile_step.py > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?" >> gpurun_out/summary.txt
 fi
 tail -3 gpurun_out/pytest_gpu.log >> gpurun_out/summary.txt 2>/dev/null
