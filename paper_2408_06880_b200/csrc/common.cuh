@@ -53,6 +53,17 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   return e;
 }
 
+// ---- address space of pointers read from device tables -------------------
+// A pointer loaded from memory (a block table, a shared-memory staging copy)
+// is generic to the compiler: its loads and stores become LD/ST with a
+// run-time space check instead of LDG/STG, ~9 % on the group sweeps
+// (tools/group_probe.py).  Every table pointer is a cudaMalloc address.
+template <class T>
+__device__ __forceinline__ T* gmem(T* p) {
+  __builtin_assume(__isGlobal(p));
+  return p;
+}
+
 // ---- error plumbing -------------------------------------------------------
 void set_error(const std::string& msg);
 const char* last_error();

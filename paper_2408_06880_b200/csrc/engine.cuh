@@ -134,6 +134,7 @@ struct LocalEdges {
   const uint16_t *se = nullptr, *de = nullptr;
   const uint32_t *ss = nullptr, *ds = nullptr;
   int64_t n = 0;
+  int n_eng = 0;  // engines of the halo (entries of the PdfTable)
 };
 // committed local program of `phase`; the table holds the engines' current pdf
 int halo_local_edges(SlbmHalo* h, int phase, PdfTable* table, LocalEdges* edges);

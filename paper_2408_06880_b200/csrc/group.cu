@@ -36,6 +36,25 @@ struct GroupArgs {
   unsigned long long* bad;
   const unsigned long long* step;
 };
+// What an index-list CTA needs before its first load, per engine, held in
+// the launch's kernel parameters (constant bank) together with the CTA
+// prefix: finding the engine and its lists then costs constant-cache hits
+// instead of a chain of dependent global loads (binary search over the
+// prefix, then the table row) -- that chain held ~11 % of the group even
+// sweep's stall samples and made it ~9 % slower than the single-engine
+// sweep on the same block (tools/group_probe.py).
+struct HotArgs {
+  const uint32_t* idx;
+  double* pdf;
+  const uint32_t* cids;
+  const uint32_t* skip;
+  uint32_t offset, n_cells, idx_pitch, lo;
+};
+template <int CAP>
+struct GroupHot {
+  uint32_t start[CAP + 1];
+  HotArgs hot[CAP];
+};
 }  // namespace slbm
 
 using namespace slbm;
@@ -48,6 +67,10 @@ struct SlbmGroup {
   std::vector<SlbmEngine*> engines;
   // tables[phase][flip] -> device array of GroupArgs (one per engine)
   GroupArgs* table[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
+  // the same per (phase, flip) as kernel-parameter blocks (index-list sweeps)
+  GroupHot<16>* hot16[3][2] = {};
+  GroupHot<128>* hot128[3][2] = {};
+  GroupHot<512>* hot512[3][2] = {};
   uint32_t* cta_start[3] = {nullptr, nullptr, nullptr};
   uint32_t n_cta[3] = {0, 0, 0};
   // the cell-local (odd) sweep: CTAs of kOddTiles tiles (own prefix)
@@ -82,6 +105,9 @@ constexpr int kGB = 128;
 // The odd sweep's CTAs stage their engine's table row in shared memory (one
 // barrier per CTA); two 128-cell tiles per CTA halve that per-cell cost.
 constexpr int kOddTiles = 2;
+// index-list sweeps of the global-table kernel: one tile per CTA (two
+// measured slower: the second tile spills and runs after the first)
+constexpr int kEvenTiles = 1;
 
 __device__ __forceinline__ int find_engine(const uint32_t* __restrict__ start, int n, uint32_t cta) {
   int lo = 0, hi = n;  // last e with start[e] <= cta
@@ -95,6 +121,80 @@ __device__ __forceinline__ int find_engine(const uint32_t* __restrict__ start, i
   return lo;
 }
 
+// identity-order rows of CTA blockIdx + ahead of the group sweep
+template <class L, int TILES>
+__device__ __forceinline__ void prefetch_group_ahead(const GroupArgs* __restrict__ table,
+                                                     const uint32_t* __restrict__ start,
+                                                     int n_eng, int eng, uint32_t ahead) {
+  constexpr int kPfThreads = (kPairedIdx<L::Q - 1> ? (L::Q - 1) / 2 : L::Q - 1) *
+                             (kGB / (kPairedIdx<L::Q - 1> ? 16 : 32));
+  const uint32_t tgt = blockIdx.x + ahead;
+  if (threadIdx.x >= kPfThreads || tgt >= gridDim.x) return;
+  const int e2 = (eng + 1 >= n_eng || tgt < start[eng + 1]) ? eng : find_engine(start, n_eng, tgt);
+  const GroupArgs& b = table[e2];
+  if (b.cids != nullptr) return;
+#pragma unroll
+  for (int t = 0; t < TILES; ++t)
+    prefetch_idx_ahead<L::Q - 1, kGB>(gmem(b.idx), b.idx_pitch, nullptr, b.offset + b.n_cells,
+                                      b.offset + ((tgt - start[e2]) * TILES + t) * kGB, 0);
+}
+
+// index-list group sweep (AA even / pull) with the block table in the
+// kernel parameters (GroupHot); bodies as k_index_sweep
+template <class L, int MODEL, int KIND, int CAP>
+__global__ void __launch_bounds__(kGB, 4)
+    k_group_hot(const __grid_constant__ GroupHot<CAP> gh, const GroupArgs* __restrict__ table,
+                int n_eng, double omega, double lam, const double* hr, uint32_t ahead) {
+  static_assert(KIND != 2, "the cell-local sweep keeps the global table");
+  int eng = 0;  // last e with start[e] <= blockIdx.x (constant-bank binary search)
+  {
+    int hi = n_eng;
+    while (hi - eng > 1) {
+      const int mid = (eng + hi) >> 1;
+      if (gh.start[mid] <= blockIdx.x)
+        eng = mid;
+      else
+        hi = mid;
+    }
+  }
+  const HotArgs& a = gh.hot[eng];
+  const uint32_t i = (blockIdx.x - gh.start[eng]) * kGB + threadIdx.x;
+  const uint32_t* idx = gmem(a.idx);
+  double* pdf = gmem(a.pdf);
+  // identity sweeps: rows of CTA blockIdx + ahead (it may be the next engine's)
+  {
+    constexpr int kPfThreads = (kPairedIdx<L::Q - 1> ? (L::Q - 1) / 2 : L::Q - 1) *
+                               (kGB / (kPairedIdx<L::Q - 1> ? 16 : 32));
+    const uint32_t tgt = blockIdx.x + ahead;
+    if (threadIdx.x < kPfThreads && tgt < gridDim.x) {
+      int e2 = eng;
+      while (e2 + 1 < n_eng && gh.start[e2 + 1] <= tgt) ++e2;
+      const HotArgs& b = gh.hot[e2];
+      if (b.cids == nullptr)
+        prefetch_idx_ahead<L::Q - 1, kGB>(gmem(b.idx), b.idx_pitch, nullptr, b.offset + b.n_cells,
+                                          b.offset + (tgt - gh.start[e2]) * kGB, 0);
+    }
+  }
+  pdl_launch_dependents();
+  pdl_wait();  // the boundary kernel's halo / wall values
+  if (i >= a.n_cells) return;
+  const uint32_t c = a.cids ? gmem(a.cids)[i] : a.offset + i;
+  if (c < a.lo) return;
+  const uint32_t skip_word = a.skip ? __ldg(gmem(a.skip) + (c >> 5)) : 0u;
+  uint32_t s[L::Q];
+  double t[L::Q];
+  load_slots<L>(s, idx, a.idx_pitch, c);
+  if ((skip_word >> (c & 31)) & 1u) return;
+  gather<L>(t, pdf, s);
+  if (a.cids)
+    prefetch_idx_ahead<L::Q - 1, kGB>(idx, a.idx_pitch, gmem(a.cids), a.n_cells,
+                                      (blockIdx.x - gh.start[eng]) * kGB, ahead);
+  const GroupArgs& g = table[eng];
+  double* dst = KIND == 0 ? gmem(g.dst) : nullptr;
+  if (collide_scatter<L, MODEL, KIND == 1>(t, s, pdf, dst, g.base, c, omega, lam, hr))
+    atomicMin(g.bad, *g.step - 1);  // the boundary kernel advanced the counter
+}
+
 template <class L, int MODEL, int KIND>
 __global__ void __launch_bounds__(kGB, KIND == 2 ? 6 : 4) k_group(const GroupArgs* __restrict__ table,
                                                   const uint32_t* __restrict__ start, int n_eng,
@@ -103,6 +203,9 @@ __global__ void __launch_bounds__(kGB, KIND == 2 ? 6 : 4) k_group(const GroupArg
   // every thread finds its engine and reads the (tiny, L1-resident) table
   // row itself: no single-thread staging + __syncthreads at CTA start, which
   // cost ~15% of the even sweep (measured, tools/slab_probe.py)
+  // engine of this CTA: binary search over the (L1-resident) CTA prefix --
+  // a per-CTA engine map measured slower (its line is an L2 round trip per
+  // CTA, consecutive CTAs land on different SMs)
   const int eng = find_engine(start, n_eng, blockIdx.x);
   const uint32_t first = start[eng];
   // the odd sweep addresses 2Q group rows through base[]: staged in shared
@@ -113,16 +216,14 @@ __global__ void __launch_bounds__(kGB, KIND == 2 ? 6 : 4) k_group(const GroupArg
     __syncthreads();
   }
   const GroupArgs& a = KIND == 2 ? staged : table[eng];
-  constexpr int kTiles = KIND == 2 ? kOddTiles : 1;
+  constexpr int kTiles = KIND == 2 ? kOddTiles : kEvenTiles;
   const uint32_t pos0 = (blockIdx.x - first) * kGB * kTiles;  // this CTA's first sweep position
-  const uint32_t* idx = a.idx;
-  const uint32_t* cids = a.cids;
+  const uint32_t* idx = gmem(a.idx);
+  const uint32_t* cids = a.cids ? gmem(a.cids) : nullptr;
+  const uint32_t* skip = a.skip ? gmem(a.skip) : nullptr;
+  double* pdf = KIND != 2 ? gmem(a.pdf) : nullptr;
+  double* dst = KIND == 0 ? gmem(a.dst) : nullptr;  // pull only
   const uint32_t pitch = a.idx_pitch, n_cells = a.n_cells, offset = a.offset;
-  // index-list rows of this engine's CTA `ahead` positions later (sweep.cuh),
-  // issued first as in the single-engine sweep
-  if (KIND != 2 && cids == nullptr)
-    prefetch_idx_ahead<L::Q - 1, kGB>(idx, pitch, nullptr, offset + n_cells, offset + pos0,
-                                      ahead);
   pdl_launch_dependents();
   pdl_wait();  // the boundary kernel's halo / wall values (read-only lists above)
   bool bad = false;
@@ -131,16 +232,23 @@ __global__ void __launch_bounds__(kGB, KIND == 2 ? 6 : 4) k_group(const GroupArg
     const uint32_t i = pos0 + tile * kGB + threadIdx.x;
     if (i >= n_cells) break;
     const uint32_t c = cids ? cids[i] : offset + i;
-    if (c < a.lo || (a.skip && ((__ldg(a.skip + (c >> 5)) >> (c & 31)) & 1u))) continue;
+    if (c < a.lo || (skip && ((__ldg(skip + (c >> 5)) >> (c & 31)) & 1u))) continue;
     if constexpr (KIND == 2) {
       bad |= cell_local<L, MODEL>(a.pdf, a.base, c, omega, lam, hr);
     } else {
       uint32_t s[L::Q];
       double t[L::Q];
       load_slots<L>(s, idx, pitch, c);
-      gather<L>(t, a.pdf, s);
-      if (cids) prefetch_idx_ahead<L::Q - 1, kGB>(idx, pitch, cids, n_cells, pos0, ahead);
-      bad |= collide_scatter<L, MODEL, KIND == 1>(t, s, a.pdf, a.dst, a.base, c, omega, lam, hr);
+      gather<L>(t, pdf, s);
+      // index-list rows of the CTA `ahead` CTAs later (sweep.cuh), issued
+      // after this CTA's own loads: finding them takes dependent table
+      // reads (the CTA may belong to the next engine -- a per-engine
+      // distance left the first quarter wave of every block without it)
+      if (tile == 0) prefetch_group_ahead<L, kTiles>(table, start, n_eng, eng, ahead);
+      if (cids)
+        prefetch_idx_ahead<L::Q - 1, kGB>(idx, pitch, cids, n_cells, pos0 + tile * kGB,
+                                          ahead * kTiles);
+      bad |= collide_scatter<L, MODEL, KIND == 1>(t, s, pdf, dst, a.base, c, omega, lam, hr);
     }
   }
   // the group's boundary kernel advanced the step counter before this sweep
@@ -159,38 +267,102 @@ __global__ void __launch_bounds__(kGB, KIND == 2 ? 6 : 4) k_group(const GroupArg
 // source (a fluid cell of the own block, a cell of another block, or a wall)
 // -- and none reads a slot another writes, so they run concurrently; the
 // per-engine path (halo kernel, then refresh) gives the same bits.
+// Work split by CTA ranges (no section test per thread): halo CTAs and UBB
+// CTAs copy kBItems entries per thread with all index and value loads of a
+// thread issued before its stores (the program is latency bound: ~1.4 M
+// 8-byte copies per phase for the C4 artery's 50 blocks), outlet CTAs one
+// entry per thread.  The halo engines' pdf pointers are staged in shared
+// memory (a divergent index into the kernel-parameter table serialises).
+constexpr int kBT = 128;
+constexpr int kBItems = 4;
+
 template <class L>
-__global__ void k_group_boundary(PdfTable lt, LocalEdges le, const GroupArgs* table,
-                                 const uint16_t* ueng, const uint32_t* uslot,
-                                 const uint32_t* upartner, const double* ucorr, int64_t n_ubb,
-                                 const OutletTab* ot, const uint16_t* oeng, const uint32_t* oidx,
-                                 int64_t n_out, unsigned long long** steps, int n_eng, int parity) {
-  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(kBT) k_group_boundary(
+    const __grid_constant__ PdfTable lt, LocalEdges le, const GroupArgs* __restrict__ table,
+    const uint16_t* __restrict__ ueng, const uint32_t* __restrict__ uslot,
+    const uint32_t* __restrict__ upartner, const double* __restrict__ ucorr, int64_t n_ubb,
+    const OutletTab* __restrict__ ot, const uint16_t* __restrict__ oeng,
+    const uint32_t* __restrict__ oidx, int64_t n_out, unsigned long long** steps, int n_eng,
+    int parity, uint32_t cta_halo, uint32_t cta_ubb) {
   pdl_launch_dependents();
-  pdl_wait();  // the previous sweep
-  if (i < n_eng) *steps[i] += 1;
-  if (i < le.n) {
-    lt.p[le.de[i]][le.ds[i]] = lt.p[le.se[i]][le.ss[i]];
+  const uint32_t b = blockIdx.x;
+  if (b == 0) {
+    pdl_wait();  // the previous sweep reads the step counters
+    for (int e = threadIdx.x; e < n_eng; e += kBT) *steps[e] += 1;
+  }
+  if (b < cta_halo) {
+    __shared__ double* sp[kMaxHaloEngines];
+    for (int e = threadIdx.x; e < le.n_eng; e += kBT) sp[e] = gmem(lt.p[e]);
+    __syncthreads();
+    const int64_t i0 = int64_t(b) * kBT * kBItems + threadIdx.x;
+    uint16_t se[kBItems], de[kBItems];
+    uint32_t ss[kBItems], ds[kBItems];
+    double v[kBItems];
+#pragma unroll
+    for (int k = 0; k < kBItems; ++k) {
+      const int64_t i = i0 + k * kBT;
+      if (i < le.n) {
+        se[k] = le.se[i];
+        ss[k] = le.ss[i];
+        de[k] = le.de[i];
+        ds[k] = le.ds[i];
+      }
+    }
+    pdl_wait();  // the previous sweep wrote the source slots
+#pragma unroll
+    for (int k = 0; k < kBItems; ++k)
+      if (i0 + k * kBT < le.n) v[k] = gmem(sp[se[k]])[ss[k]];
+#pragma unroll
+    for (int k = 0; k < kBItems; ++k)
+      if (i0 + k * kBT < le.n) gmem(sp[de[k]])[ds[k]] = v[k];
     return;
   }
-  i -= le.n;
-  if (i < n_ubb) {
-    double* pdf = table[ueng[i]].pdf;
-    if (parity == SLBM_EVEN)
-      pdf[uslot[i]] = pdf[upartner[i]] + ucorr[i];
-    else
-      pdf[upartner[i]] = pdf[uslot[i]] + ucorr[i];
+  if (b < cta_halo + cta_ubb) {  // sparse.py:301-304
+    const int64_t i0 = int64_t(b - cta_halo) * kBT * kBItems + threadIdx.x;
+    double* pdf[kBItems];
+    uint32_t from[kBItems], to[kBItems];
+    double corr[kBItems], v[kBItems];
+#pragma unroll
+    for (int k = 0; k < kBItems; ++k) {
+      const int64_t i = i0 + k * kBT;
+      if (i < n_ubb) {
+        pdf[k] = gmem(table[ueng[i]].pdf);
+        from[k] = parity == SLBM_EVEN ? upartner[i] : uslot[i];
+        to[k] = parity == SLBM_EVEN ? uslot[i] : upartner[i];
+        corr[k] = ucorr[i];
+      }
+    }
+    pdl_wait();
+#pragma unroll
+    for (int k = 0; k < kBItems; ++k)
+      if (i0 + k * kBT < n_ubb) v[k] = gmem(pdf[k])[from[k]];
+#pragma unroll
+    for (int k = 0; k < kBItems; ++k)
+      if (i0 + k * kBT < n_ubb) gmem(pdf[k])[to[k]] = v[k] + corr[k];
     return;
   }
-  i -= n_ubb;
+  const int64_t i = int64_t(b - cta_halo - cta_ubb) * kBT + threadIdx.x;
+  int e = 0;
+  uint32_t k = 0;
   if (i < n_out) {
-    const int e = oeng[i];
-    const uint32_t k = oidx[i];
+    e = oeng[i];
+    k = oidx[i];
+  }
+  pdl_wait();  // in every thread, so the chain's completion stays transitive
+  if (i < n_out) {
     const OutletTab& o = ot[e];
     const GroupArgs& a = table[e];
-    outlet_entry<L>(a.pdf, a.base, o.slot[k], o.partner[k], o.cell[k], o.dir[k], o.rho[k],
-                    o.u + 3 * size_t(k), parity);
+    outlet_entry<L>(gmem(a.pdf), a.base, gmem(o.slot)[k], gmem(o.partner)[k], gmem(o.cell)[k],
+                    gmem(o.dir)[k], gmem(o.rho)[k], gmem(o.u) + 3 * size_t(k), parity);
   }
+}
+
+// CTA prefix of a phase on the device: start[e] = first CTA of engine e
+int upload_prefix(const std::vector<uint32_t>& start, uint32_t** out) {
+  SLBM_CUDA_TRY(cudaMalloc(out, start.size() * sizeof(uint32_t)));
+  SLBM_CUDA_TRY(cudaMemcpy(*out, start.data(), start.size() * sizeof(uint32_t),
+                           cudaMemcpyHostToDevice));
+  return SLBM_OK;
 }
 
 template <class F>
@@ -232,6 +404,18 @@ GroupArgs args_of(SlbmEngine* e, int phase, int flip) {
   return a;
 }
 
+template <int CAP>
+void fill_hot(GroupHot<CAP>*& out, SlbmEngine* const* engines, int n, int phase, int flip,
+              const std::vector<uint32_t>& start) {
+  out = new GroupHot<CAP>();
+  for (int i = 0; i <= n; ++i) out->start[i] = start[i];
+  for (int i = 0; i < n; ++i) {
+    const GroupArgs a = args_of(engines[i], phase, flip);
+    out->hot[i] = HotArgs{a.idx, a.pdf, a.cids, a.skip, a.offset, a.n_cells, a.idx_pitch, a.lo};
+  }
+}
+
+
 }  // namespace
 
 extern "C" {
@@ -266,21 +450,27 @@ int slbm_group_create(SlbmEngine** engines, int n, SlbmGroup** out) {
     std::vector<uint32_t> start(n + 1, 0);
     for (int i = 0; i < n; ++i) {
       const GroupArgs a = args_of(engines[i], phase, 0);
-      start[i + 1] = start[i] + (a.n_cells + kGB - 1) / kGB;
+      start[i + 1] = start[i] + (a.n_cells + kGB * kEvenTiles - 1) / (kGB * kEvenTiles);
     }
     g->n_cta[phase] = start[n];
-    SLBM_CUDA_TRY(cudaMalloc(&g->cta_start[phase], (n + 1) * sizeof(uint32_t)));
-    SLBM_CUDA_TRY(cudaMemcpy(g->cta_start[phase], start.data(), (n + 1) * sizeof(uint32_t),
-                             cudaMemcpyHostToDevice));
+    SLBM_TRY(upload_prefix(start, &g->cta_start[phase]));
     std::vector<uint32_t> odd(n + 1, 0);
     for (int i = 0; i < n; ++i) {
       const GroupArgs a = args_of(engines[i], phase, 0);
       odd[i + 1] = odd[i] + (a.n_cells + kGB * kOddTiles - 1) / (kGB * kOddTiles);
     }
     g->n_cta_odd[phase] = odd[n];
-    SLBM_CUDA_TRY(cudaMalloc(&g->cta_start_odd[phase], (n + 1) * sizeof(uint32_t)));
-    SLBM_CUDA_TRY(cudaMemcpy(g->cta_start_odd[phase], odd.data(), (n + 1) * sizeof(uint32_t),
-                             cudaMemcpyHostToDevice));
+    SLBM_TRY(upload_prefix(odd, &g->cta_start_odd[phase]));
+    {
+      for (int flip = 0; flip < 2; ++flip) {
+        if (n <= 16)
+          fill_hot(g->hot16[phase][flip], engines, n, phase, flip, start);
+        else if (n <= 128)
+          fill_hot(g->hot128[phase][flip], engines, n, phase, flip, start);
+        else if (n <= 512)
+          fill_hot(g->hot512[phase][flip], engines, n, phase, flip, start);
+      }
+    }
     for (int flip = 0; flip < 2; ++flip) {
       std::vector<GroupArgs> tab(n);
       for (int i = 0; i < n; ++i) tab[i] = args_of(engines[i], phase, flip);
@@ -359,6 +549,12 @@ int slbm_group_destroy(SlbmGroup* g) {
     if (g->cta_start[p]) cudaFree(g->cta_start[p]);
     if (g->cta_start_odd[p]) cudaFree(g->cta_start_odd[p]);
   }
+  for (int p = 0; p < 3; ++p)
+    for (int f = 0; f < 2; ++f) {
+      delete g->hot16[p][f];
+      delete g->hot128[p][f];
+      delete g->hot512[p][f];
+    }
   void* ptrs[] = {g->ubb_eng, g->ubb_slot, g->ubb_partner, g->ubb_corr, g->steps,
                   g->out_tab, g->out_eng, g->out_idx};
   for (void* p : ptrs)
@@ -373,14 +569,17 @@ int group_boundary(SlbmGroup* g, SlbmHalo* halo, int phase, int parity, cudaStre
   if (halo) SLBM_TRY(halo_local_edges(halo, phase, &lt, &le));
   const int flip = g->pattern == SLBM_PULL ? g->flip : 0;
   const int n = int(g->engines.size());
-  const int64_t work = std::max<int64_t>(n, le.n + g->n_ubb + g->n_out);
+  constexpr int64_t kPer = kBT * kBItems;
+  const uint32_t cta_halo = uint32_t((le.n + kPer - 1) / kPer);
+  const uint32_t cta_ubb = uint32_t((g->n_ubb + kPer - 1) / kPer);
+  const uint32_t cta_out = uint32_t((g->n_out + kBT - 1) / kBT);
+  const uint32_t grid = std::max(1u, cta_halo + cta_ubb + cta_out);
   cudaError_t err = cudaSuccess;
   on_lattice(g->q, [&](auto lat) {
     using L = decltype(lat);
-    err = launch_pdl(k_group_boundary<L>, dim3(unsigned((work + 127) / 128)), dim3(128), 0, s,
-                     lt, le, g->table[0][flip], g->ubb_eng, g->ubb_slot, g->ubb_partner,
-                     g->ubb_corr, g->n_ubb, g->out_tab, g->out_eng, g->out_idx, g->n_out,
-                     g->steps, n, parity);
+    err = launch_pdl(k_group_boundary<L>, dim3(grid), dim3(kBT), 0, s, lt, le, g->table[0][flip],
+                     g->ubb_eng, g->ubb_slot, g->ubb_partner, g->ubb_corr, g->n_ubb, g->out_tab,
+                     g->out_eng, g->out_idx, g->n_out, g->steps, n, parity, cta_halo, cta_ubb);
   });
   SLBM_CUDA_TRY(err);
   return SLBM_OK;
@@ -420,6 +619,20 @@ int slbm_group_step(SlbmGroup* g, int phase, void* stream) {
     const uint32_t ahead = uint32_t(sms);  // one quarter wave at 4 CTAs/SM
     auto go = [&](auto mc) {
       constexpr int M = decltype(mc)::value;
+      auto hot = [&](auto* gh) -> bool {  // kernel-parameter block table
+        if (!gh || kind == 2) return false;
+        constexpr int CAP = int(sizeof(gh->hot) / sizeof(HotArgs));
+        if (kind == 0)
+          err = launch_pdl(k_group_hot<L, M, 0, CAP>, dim3(g->n_cta[phase]), dim3(kGB), 0, s, *gh,
+                           tab, n, g->omega, g->lam, g->hr, ahead);
+        else
+          err = launch_pdl(k_group_hot<L, M, 1, CAP>, dim3(g->n_cta[phase]), dim3(kGB), 0, s, *gh,
+                           tab, n, g->omega, g->lam, g->hr, ahead);
+        return true;
+      };
+      if (hot(g->hot16[phase][flip]) || hot(g->hot128[phase][flip]) ||
+          hot(g->hot512[phase][flip]))
+        return;
       if (kind == 0)
         err = launch_pdl(k_group<L, M, 0>, dim3(g->n_cta[phase]), dim3(kGB), 0, s, tab,
                          g->cta_start[phase], n, g->omega, g->lam, g->hr, ahead);

@@ -499,6 +499,7 @@ int halo_local_edges(SlbmHalo* h, int phase, PdfTable* table, LocalEdges* edges)
   edges->de = p.d_lde;
   edges->ds = p.d_lds;
   edges->n = p.n_local;
+  edges->n_eng = int(h->engines.size());
   return SLBM_OK;
 }
 }  // namespace slbm

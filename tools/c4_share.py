@@ -63,6 +63,9 @@ def measure(dom, label, profile=True):
             dom.run(n, driver="overlapped", use_graph=True)
             torch.cuda.synchronize()
         agg = {}
+        seq = [(ev.name.replace("(anonymous namespace)::", "").split("(")[0][:40], round(ev.device_time_total, 1))
+               for ev in prof.events() if ev.device_type.name == "CUDA"]
+        out["first_launches_us"] = seq[:8]
         for ev in prof.events():
             if ev.device_type.name == "CUDA":
                 k = ev.name.replace("(anonymous namespace)::", "").split("(")[0][:60]
@@ -83,6 +86,13 @@ def main():
     st = make_stencil("d3q19")
     p = CollisionParams(1.7, "trt", trt_magic_lambda(1.7))
     fw = os.environ.get("FRAME", "halo")
+    if os.environ.get("BLOCK_SWEEP"):  # the same tree in blocks of 512 / 256 / 128
+        for b in (512, 256, 128):
+            dom = Domain(fl, b, st, p, pattern="aa", frame_width=fw, device=0, check="deferred")
+            measure(dom, f"full, blocks of {b}^3")
+            del dom
+            torch.cuda.empty_cache()
+        return
     dom = Domain(fl, 128, st, p, pattern="aa", frame_width=fw, device=0, check="deferred")
     measure(dom, "full")
     asg = dom.balance(workers)

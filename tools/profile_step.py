@@ -32,6 +32,11 @@ def main():
         phi = float(os.environ.get("PHI", 1.0))
         fl = geometry.obstacle_flags((edge,) * 3, phi, 1)
         eng = DenseEngine(fl, st, p, "aa", device=0, check="deferred")
+    elif os.environ.get("ARTERY"):  # C4 vessel tree as one block
+        from paper_2408_06880_b200 import geometry
+
+        fl = geometry.artery_flags((edge,) * 3, seed=0, r_root=40.0, r_min=14.0)
+        eng = SparseEngine(fl, st, p, "aa", device=0, check="deferred")
     elif os.environ.get("OBSTACLE"):  # C5: cell-wise random obstacles at porosity PHI
         from paper_2408_06880_b200 import geometry
 

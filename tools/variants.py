@@ -52,6 +52,10 @@ def main():
         from paper_2408_06880_b200 import geometry
 
         fl = geometry.obstacle_flags((edge,) * 3, float(os.environ.get("PHI", 0.3)), 1)
+    elif os.environ.get("ARTERY"):  # C4: the configs[3] vessel tree as one block
+        from paper_2408_06880_b200 import geometry
+
+        fl = geometry.artery_flags((edge,) * 3, seed=0, r_root=40.0, r_min=14.0)
     else:
         fl = bench.make_flags(edge, 0)
     eng = SparseEngine(fl, st, p, "aa", device=0, check="deferred")
