@@ -288,6 +288,25 @@ int slbm_group_refresh(SlbmGroup* group, int parity, void* stream);
 int slbm_group_boundary(SlbmGroup* group, SlbmHalo* halo, int phase, int parity, void* stream);
 int slbm_group_step(SlbmGroup* group, int phase, void* stream);
 int slbm_group_finish(SlbmGroup* group, void* stream);
+/* AA groups: serve the device-local edges of `halo` by direct addressing
+ * instead of copies (extension; exchange.py:222-253 copies them).  All
+ * engines' pdf buffers move into one pool and the index-list sweeps read a
+ * rewritten list whose ghost entries of local edges address the source
+ * slot; the REVERSED local program must be the exact inverse of the
+ * CANONICAL one (checked).  Bit-identical results; ghost slots of local
+ * edges are no longer maintained and the halo's local program is switched
+ * off.  SLBM_ECONFIG when not applicable (nothing changed then).        */
+int slbm_group_link_halo(SlbmGroup* group, SlbmHalo* halo);
+/* Linked groups only (no-op otherwise): the local edges' (source slot,
+ * ghost slot) pairs, mode 0 ghost <- source, 1 swap, 2 source <- ghost.
+ * The reference's state after an AA even step has the source slots of
+ * local edges still stale (the REVERSED exchange delivers them before the
+ * odd step) and the even step's values in the ghosts.  A linked group
+ * writes the sources directly; when the state after an even step is
+ * handed back to the caller, mode 0 before that step and mode 1 after it
+ * reproduce the reference's state exactly (sources and ghosts), and mode 2
+ * before the next odd step is its REVERSED local exchange.             */
+int slbm_group_stale_copy(SlbmGroup* group, int mode, void* stream);
 
 /* CUDA graph capture of arbitrary engine / halo work issued on `stream`
  * (e.g. one AA step pair of a whole multi-block domain incl. NCCL): begin,

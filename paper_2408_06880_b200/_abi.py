@@ -116,6 +116,8 @@ SIGNATURES = {
     "slbm_group_boundary": [vp, vp, C.c_int, C.c_int, vp],
     "slbm_group_step": [vp, C.c_int, vp],
     "slbm_group_finish": [vp, vp],
+    "slbm_group_link_halo": [vp, vp],
+    "slbm_group_stale_copy": [vp, C.c_int, vp],
     "slbm_capture_begin": [vp],
     "slbm_capture_end": [vp, C.POINTER(vp)],
     "slbm_graph_launch": [vp, vp],

@@ -82,6 +82,13 @@ void free_engine(SlbmEngine* e) {
   for (auto& gx : e->graph)
     if (gx) cudaGraphExecDestroy(gx);
   free_pair(e);
+  if (e->pool) {  // the pdf is part of a group's pool: release this engine's share
+    if (--e->pool->refs == 0) {
+      cudaFree(e->pool->base);
+      delete e->pool;
+    }
+    e->pdf = nullptr;
+  }
   void* ptrs[] = {e->pdf,         e->tmp,          e->idx,       e->x_flat,
                   e->cid_map,     e->ubb_slot,     e->ubb_partner, e->ubb_corr,
                   e->ghost_key,   e->frame_cids,   e->frame_bits, e->d_bad,

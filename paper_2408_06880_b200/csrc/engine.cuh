@@ -7,6 +7,12 @@
 
 namespace slbm {
 struct PairPlan;
+// one device allocation holding the pdf buffers of several engines (block
+// groups with direct local halo edges, group.cu); freed with its last engine
+struct PdfPool {
+  double* base = nullptr;
+  int refs = 0;
+};
 }
 
 // Kernel-selection knobs (slbm_engine_set_tuning; include/slbm_b200.h).  Each
@@ -62,6 +68,7 @@ struct SlbmEngine {
 
   // device memory
   double* pdf = nullptr;   // active buffer
+  slbm::PdfPool* pool = nullptr;  // pdf lives in this pool (not freed on its own)
   double* tmp = nullptr;   // pull: second buffer
   int layout = 0;  // 0 sparse (index list), 1 dense (direct addressing)
   uint32_t* dense_mask = nullptr;       // per box cell fold mask (dense)
@@ -138,6 +145,12 @@ struct LocalEdges {
 };
 // committed local program of `phase`; the table holds the engines' current pdf
 int halo_local_edges(SlbmHalo* h, int phase, PdfTable* table, LocalEdges* edges);
+// host copy of the committed local program of `phase` (engine ids index
+// `engines`), and switching it off (direct local edges, group.cu)
+int halo_local_program(SlbmHalo* h, int phase, std::vector<SlbmEngine*>* engines,
+                       std::vector<uint16_t>* se, std::vector<uint32_t>* ss,
+                       std::vector<uint16_t>* de, std::vector<uint32_t>* ds);
+void halo_disable_local(SlbmHalo* h);
 
 // kernels / launchers implemented in kernels.cu
 int launch_step(SlbmEngine* e, int phase);

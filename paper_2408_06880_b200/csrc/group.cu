@@ -11,6 +11,7 @@
 // the step counters are batched the same way.  With the halo program this
 // makes one domain step O(1) launches, which a CUDA graph then replays.
 #include <algorithm>
+#include <unordered_map>
 #include <vector>
 
 #include "collide.cuh"
@@ -35,6 +36,13 @@ struct GroupArgs {
   uint32_t base[28];  // device group starts (pbase)
   unsigned long long* bad;
   const unsigned long long* step;
+  // addressing of the index-list sweeps: the engine's own list and buffer,
+  // or, with direct local halo edges (slbm_group_link_halo), the group's
+  // rewritten list over the shared pdf pool (slots relative to spdf, a
+  // cell's own rest slot at slot_off + c)
+  const uint32_t* sidx;
+  double* spdf;
+  uint32_t slot_off;
 };
 // What an index-list CTA needs before its first load, per engine, held in
 // the launch's kernel parameters (constant bank) together with the CTA
@@ -49,6 +57,7 @@ struct HotArgs {
   const uint32_t* cids;
   const uint32_t* skip;
   uint32_t offset, n_cells, idx_pitch, lo;
+  uint32_t slot_off, pad;
 };
 template <int CAP>
 struct GroupHot {
@@ -71,6 +80,18 @@ struct SlbmGroup {
   GroupHot<16>* hot16[3][2] = {};
   GroupHot<128>* hot128[3][2] = {};
   GroupHot<512>* hot512[3][2] = {};
+  // direct local halo edges (slbm_group_link_halo): every engine's pdf lives
+  // in one pool, the index-list sweeps read a rewritten list whose ghost
+  // entries of local edges address the source engine's slot in the pool
+  bool direct = false;
+  double* pool = nullptr;
+  std::vector<uint32_t> pool_off;  // per engine, in pdf elements
+  std::vector<uint32_t*> gidx;     // per engine, (q-1) x idx_pitch
+  // the local edges as (source slot, ghost slot) pool offsets, for
+  // slbm_group_stale_copy
+  uint32_t* save_src = nullptr;
+  uint32_t* save_dst = nullptr;
+  int64_t n_save = 0;
   uint32_t* cta_start[3] = {nullptr, nullptr, nullptr};
   uint32_t n_cta[3] = {0, 0, 0};
   // the cell-local (odd) sweep: CTAs of kOddTiles tiles (own prefix)
@@ -135,7 +156,7 @@ __device__ __forceinline__ void prefetch_group_ahead(const GroupArgs* __restrict
   if (b.cids != nullptr) return;
 #pragma unroll
   for (int t = 0; t < TILES; ++t)
-    prefetch_idx_ahead<L::Q - 1, kGB>(gmem(b.idx), b.idx_pitch, nullptr, b.offset + b.n_cells,
+    prefetch_idx_ahead<L::Q - 1, kGB>(gmem(b.sidx), b.idx_pitch, nullptr, b.offset + b.n_cells,
                                       b.offset + ((tgt - start[e2]) * TILES + t) * kGB, 0);
 }
 
@@ -184,6 +205,7 @@ __global__ void __launch_bounds__(kGB, 4)
   uint32_t s[L::Q];
   double t[L::Q];
   load_slots<L>(s, idx, a.idx_pitch, c);
+  s[0] = a.slot_off + c;
   if ((skip_word >> (c & 31)) & 1u) return;
   gather<L>(t, pdf, s);
   if (a.cids)
@@ -218,10 +240,10 @@ __global__ void __launch_bounds__(kGB, KIND == 2 ? 6 : 4) k_group(const GroupArg
   const GroupArgs& a = KIND == 2 ? staged : table[eng];
   constexpr int kTiles = KIND == 2 ? kOddTiles : kEvenTiles;
   const uint32_t pos0 = (blockIdx.x - first) * kGB * kTiles;  // this CTA's first sweep position
-  const uint32_t* idx = gmem(a.idx);
+  const uint32_t* idx = gmem(a.sidx);
   const uint32_t* cids = a.cids ? gmem(a.cids) : nullptr;
   const uint32_t* skip = a.skip ? gmem(a.skip) : nullptr;
-  double* pdf = KIND != 2 ? gmem(a.pdf) : nullptr;
+  double* pdf = KIND != 2 ? gmem(a.spdf) : nullptr;
   double* dst = KIND == 0 ? gmem(a.dst) : nullptr;  // pull only
   const uint32_t pitch = a.idx_pitch, n_cells = a.n_cells, offset = a.offset;
   pdl_launch_dependents();
@@ -239,6 +261,7 @@ __global__ void __launch_bounds__(kGB, KIND == 2 ? 6 : 4) k_group(const GroupArg
       uint32_t s[L::Q];
       double t[L::Q];
       load_slots<L>(s, idx, pitch, c);
+      s[0] = a.slot_off + c;
       gather<L>(t, pdf, s);
       // index-list rows of the CTA `ahead` CTAs later (sweep.cuh), issued
       // after this CTA's own loads: finding them takes dependent table
@@ -357,6 +380,42 @@ __global__ void __launch_bounds__(kBT) k_group_boundary(
   }
 }
 
+// ---- direct local halo edges (slbm_group_link_halo) ----
+__global__ void k_add_offset(uint32_t* out, const uint32_t* in, int64_t n, uint32_t off) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = in[i] + off;
+}
+// pos[slot] = uint32 position in the index list of the entry reading `slot`
+// (a slot is read by at most one (cell, direction): the builder's check)
+__global__ void k_slot_pos(uint32_t* pos, const uint32_t* idx, uint32_t pitch, uint32_t n_fluid,
+                           int rows, int paired) {
+  const int64_t n = int64_t(rows) * n_fluid;
+  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+       k += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t r = uint32_t(k / n_fluid), c = uint32_t(k % n_fluid);
+    const size_t f = idx_offset(paired != 0, pitch, r, c);
+    pos[idx[f]] = uint32_t(f);
+  }
+}
+// mode 0: ghost <- source, 1: swap, 2: source <- ghost
+__global__ void k_pool_copy(double* pool, const uint32_t* src, const uint32_t* dst, int64_t n,
+                            int mode) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t a = mode == 2 ? dst[i] : src[i], b = mode == 2 ? src[i] : dst[i];
+  const double v = pool[a];
+  if (mode == 1) pool[a] = pool[b];
+  pool[b] = v;
+}
+__global__ void k_rewrite(uint32_t* gidx, const uint32_t* pos, const uint32_t* ghost,
+                          const uint32_t* val, int64_t n) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t p = pos[ghost[i]];
+  if (p != 0xFFFFFFFFu) gidx[p] = val[i];
+}
+
 // CTA prefix of a phase on the device: start[e] = first CTA of engine e
 int upload_prefix(const std::vector<uint32_t>& start, uint32_t** out) {
   SLBM_CUDA_TRY(cudaMalloc(out, start.size() * sizeof(uint32_t)));
@@ -401,18 +460,78 @@ GroupArgs args_of(SlbmEngine* e, int phase, int flip) {
   for (int q = 0; q <= e->q && q < 28; ++q) a.base[q] = uint32_t(e->pbase[q]);
   a.bad = e->d_bad;
   a.step = e->d_step;
+  a.sidx = a.idx;
+  a.spdf = a.pdf;
+  a.slot_off = 0;
+  return a;
+}
+
+// engine i of the group: with direct local halo edges the index-list sweeps
+// address the pool through the group's rewritten list (AA: one buffer)
+GroupArgs gargs_of(const SlbmGroup* g, int i, int phase, int flip) {
+  GroupArgs a = args_of(g->engines[i], phase, flip);
+  if (g->direct) {
+    a.sidx = g->gidx[i];
+    a.spdf = g->pool;
+    a.slot_off = g->pool_off[i];
+  }
   return a;
 }
 
 template <int CAP>
-void fill_hot(GroupHot<CAP>*& out, SlbmEngine* const* engines, int n, int phase, int flip,
+void fill_hot(GroupHot<CAP>*& out, const SlbmGroup* g, int phase, int flip,
               const std::vector<uint32_t>& start) {
+  const int n = int(g->engines.size());
+  delete out;
   out = new GroupHot<CAP>();
   for (int i = 0; i <= n; ++i) out->start[i] = start[i];
   for (int i = 0; i < n; ++i) {
-    const GroupArgs a = args_of(engines[i], phase, flip);
-    out->hot[i] = HotArgs{a.idx, a.pdf, a.cids, a.skip, a.offset, a.n_cells, a.idx_pitch, a.lo};
+    const GroupArgs a = gargs_of(g, i, phase, flip);
+    out->hot[i] = HotArgs{a.sidx,     a.spdf,      a.cids, a.skip, a.offset,
+                          a.n_cells, a.idx_pitch, a.lo,   a.slot_off, 0};
   }
+}
+
+// CTA prefixes, device tables and kernel-parameter blocks of every phase
+int build_tables(SlbmGroup* g) {
+  const int n = int(g->engines.size());
+  SlbmEngine* e0 = g->engines[0];
+  for (int phase = 0; phase < 3; ++phase) {
+    if (phase && !e0->has_split) continue;
+    std::vector<uint32_t> start(n + 1, 0);
+    for (int i = 0; i < n; ++i) {
+      const GroupArgs a = args_of(g->engines[i], phase, 0);
+      start[i + 1] = start[i] + (a.n_cells + kGB * kEvenTiles - 1) / (kGB * kEvenTiles);
+    }
+    g->n_cta[phase] = start[n];
+    if (g->cta_start[phase]) cudaFree(g->cta_start[phase]);
+    SLBM_TRY(upload_prefix(start, &g->cta_start[phase]));
+    std::vector<uint32_t> odd(n + 1, 0);
+    for (int i = 0; i < n; ++i) {
+      const GroupArgs a = args_of(g->engines[i], phase, 0);
+      odd[i + 1] = odd[i] + (a.n_cells + kGB * kOddTiles - 1) / (kGB * kOddTiles);
+    }
+    g->n_cta_odd[phase] = odd[n];
+    if (g->cta_start_odd[phase]) cudaFree(g->cta_start_odd[phase]);
+    SLBM_TRY(upload_prefix(odd, &g->cta_start_odd[phase]));
+    for (int flip = 0; flip < 2; ++flip) {
+      if (n <= 16)
+        fill_hot(g->hot16[phase][flip], g, phase, flip, start);
+      else if (n <= 128)
+        fill_hot(g->hot128[phase][flip], g, phase, flip, start);
+      else if (n <= 512)
+        fill_hot(g->hot512[phase][flip], g, phase, flip, start);
+    }
+    for (int flip = 0; flip < 2; ++flip) {
+      std::vector<GroupArgs> tab(n);
+      for (int i = 0; i < n; ++i) tab[i] = gargs_of(g, i, phase, flip);
+      if (g->table[phase][flip]) cudaFree(g->table[phase][flip]);
+      SLBM_CUDA_TRY(cudaMalloc(&g->table[phase][flip], n * sizeof(GroupArgs)));
+      SLBM_CUDA_TRY(cudaMemcpy(g->table[phase][flip], tab.data(), n * sizeof(GroupArgs),
+                               cudaMemcpyHostToDevice));
+    }
+  }
+  return SLBM_OK;
 }
 
 
@@ -445,40 +564,7 @@ int slbm_group_create(SlbmEngine** engines, int n, SlbmGroup** out) {
   g->hr = e0->d_hr;
   g->engines.assign(engines, engines + n);
   // pull: each engine's e->pdf is "current"; record the flip as 0
-  for (int phase = 0; phase < 3; ++phase) {
-    if (phase && !e0->has_split) continue;
-    std::vector<uint32_t> start(n + 1, 0);
-    for (int i = 0; i < n; ++i) {
-      const GroupArgs a = args_of(engines[i], phase, 0);
-      start[i + 1] = start[i] + (a.n_cells + kGB * kEvenTiles - 1) / (kGB * kEvenTiles);
-    }
-    g->n_cta[phase] = start[n];
-    SLBM_TRY(upload_prefix(start, &g->cta_start[phase]));
-    std::vector<uint32_t> odd(n + 1, 0);
-    for (int i = 0; i < n; ++i) {
-      const GroupArgs a = args_of(engines[i], phase, 0);
-      odd[i + 1] = odd[i] + (a.n_cells + kGB * kOddTiles - 1) / (kGB * kOddTiles);
-    }
-    g->n_cta_odd[phase] = odd[n];
-    SLBM_TRY(upload_prefix(odd, &g->cta_start_odd[phase]));
-    {
-      for (int flip = 0; flip < 2; ++flip) {
-        if (n <= 16)
-          fill_hot(g->hot16[phase][flip], engines, n, phase, flip, start);
-        else if (n <= 128)
-          fill_hot(g->hot128[phase][flip], engines, n, phase, flip, start);
-        else if (n <= 512)
-          fill_hot(g->hot512[phase][flip], engines, n, phase, flip, start);
-      }
-    }
-    for (int flip = 0; flip < 2; ++flip) {
-      std::vector<GroupArgs> tab(n);
-      for (int i = 0; i < n; ++i) tab[i] = args_of(engines[i], phase, flip);
-      SLBM_CUDA_TRY(cudaMalloc(&g->table[phase][flip], n * sizeof(GroupArgs)));
-      SLBM_CUDA_TRY(cudaMemcpy(g->table[phase][flip], tab.data(), n * sizeof(GroupArgs),
-                               cudaMemcpyHostToDevice));
-    }
-  }
+  SLBM_TRY(build_tables(g));
   // concatenated UBB program with engine ids
   for (int i = 0; i < n; ++i) g->n_ubb += engines[i]->n_ubb;
   for (int i = 0; i < n; ++i) g->has_outlets |= engines[i]->n_out > 0;
@@ -540,6 +626,158 @@ int slbm_group_create(SlbmEngine** engines, int n, SlbmGroup** out) {
   return SLBM_OK;
 }
 
+// Direct local halo edges for an AA block group (extension of the group
+// path; the reference copies every local edge twice a step pair,
+// exchange.py:222-253).  Every engine's pdf moves into one pool, and the
+// index-list sweeps read a rewritten copy of each engine's list in which a
+// ghost slot fed by a local CANONICAL edge (B, s) -> (A, g) addresses B's
+// slot s in the pool.  The combined AA step then reads the value the copy
+// would have delivered and writes its result where the REVERSED copy would
+// have taken it (the REVERSED program is checked to be the exact inverse),
+// so both local copies disappear and the results are bit-identical.  Ghost
+// slots of local edges are left unmaintained (internal buffers); remote
+// edges keep their ghost slots and messages.  The halo's local program is
+// switched off.
+int slbm_group_link_halo(SlbmGroup* g, SlbmHalo* h) {
+  if (!g || !h) return fail(SLBM_ECONFIG, "null group or halo");
+  if (g->direct) return SLBM_OK;
+  if (g->pattern != SLBM_AA) return fail(SLBM_ECONFIG, "direct local halo edges need the AA pattern");
+  cudaSetDevice(g->device);
+  const int n = int(g->engines.size());
+  std::vector<SlbmEngine*> heng;
+  std::vector<uint16_t> cse, cde, rse, rde;
+  std::vector<uint32_t> css, cds, rss, rds;
+  SLBM_TRY(halo_local_program(h, 0, &heng, &cse, &css, &cde, &cds));
+  SLBM_TRY(halo_local_program(h, 1, &heng, &rse, &rss, &rde, &rds));
+  if (cse.empty()) return fail(SLBM_ECONFIG, "the halo has no local edges");
+  std::vector<int> gid(heng.size(), -1);
+  for (size_t k = 0; k < heng.size(); ++k)
+    for (int i = 0; i < n; ++i)
+      if (heng[k] == g->engines[i]) gid[k] = i;
+  auto key = [](uint64_t e, uint64_t slot) { return (e << 32) | slot; };
+  std::unordered_map<uint64_t, uint64_t> fwd;  // (A, ghost g) -> (B, source s)
+  fwd.reserve(cse.size() * 2);
+  for (size_t k = 0; k < cse.size(); ++k) {
+    if (gid[cse[k]] < 0 || gid[cde[k]] < 0)
+      return fail(SLBM_ECONFIG, "local halo edge with an engine outside the group");
+    if (!fwd.emplace(key(gid[cde[k]], cds[k]), key(gid[cse[k]], css[k])).second)
+      return fail(SLBM_EPROTOCOL, "ghost slot fed twice");
+  }
+  if (rse.size() != cse.size()) return fail(SLBM_ECONFIG, "REVERSED local program is not the inverse");
+  for (size_t k = 0; k < rse.size(); ++k) {
+    if (gid[rse[k]] < 0 || gid[rde[k]] < 0)
+      return fail(SLBM_ECONFIG, "local halo edge with an engine outside the group");
+    auto it = fwd.find(key(gid[rse[k]], rss[k]));
+    if (it == fwd.end() || it->second != key(gid[rde[k]], rds[k]))
+      return fail(SLBM_ECONFIG, "REVERSED local program is not the inverse");
+  }
+  // pool layout: engines back to back, 32-element (256 B) aligned
+  std::vector<uint32_t> off(n);
+  int64_t total = 0;
+  for (int i = 0; i < n; ++i) {
+    if (g->engines[i]->pool) return fail(SLBM_ECONFIG, "engine already pooled");
+    off[i] = uint32_t(total);
+    total += (g->engines[i]->phys_slots + 31) / 32 * 32;
+    if (total >= (int64_t(1) << 32)) return fail(SLBM_ECONFIG, "group pool exceeds 2^32 slots");
+  }
+  SLBM_CUDA_TRY(cudaDeviceSynchronize());
+  double* pool = nullptr;
+  SLBM_CUDA_TRY(cudaMalloc(&pool, size_t(total) * sizeof(double)));
+  std::vector<uint32_t*> gidx(n, nullptr);
+  for (int i = 0; i < n; ++i) {
+    SlbmEngine* e = g->engines[i];
+    const int64_t entries = int64_t(e->q - 1) * e->idx_pitch;
+    if (cudaMalloc(&gidx[i], size_t(entries) * sizeof(uint32_t)) != cudaSuccess) {
+      for (auto* p : gidx)
+        if (p) cudaFree(p);
+      cudaFree(pool);
+      return fail(SLBM_ECUDA, "out of device memory for the group index lists");
+    }
+    if (entries) {
+      k_add_offset<<<1024, 256>>>(gidx[i], e->idx, entries, off[i]);
+      slbm::count_launch();
+    }
+  }
+  // the CANONICAL program in pool offsets (saving the stale source values)
+  {
+    std::vector<uint32_t> ss_(cse.size()), dd_(cse.size());
+    for (size_t k = 0; k < cse.size(); ++k) {
+      ss_[k] = off[gid[cse[k]]] + css[k];
+      dd_[k] = off[gid[cde[k]]] + cds[k];
+    }
+    SLBM_CUDA_TRY(cudaMalloc(&g->save_src, ss_.size() * 4));
+    SLBM_CUDA_TRY(cudaMalloc(&g->save_dst, dd_.size() * 4));
+    SLBM_CUDA_TRY(cudaMemcpy(g->save_src, ss_.data(), ss_.size() * 4, cudaMemcpyHostToDevice));
+    SLBM_CUDA_TRY(cudaMemcpy(g->save_dst, dd_.data(), dd_.size() * 4, cudaMemcpyHostToDevice));
+    g->n_save = int64_t(ss_.size());
+  }
+  // rewrite the ghost entries of local edges, per destination engine
+  std::vector<std::vector<uint32_t>> ghost(n), val(n);
+  for (size_t k = 0; k < cse.size(); ++k) {
+    const int a = gid[cde[k]], b = gid[cse[k]];
+    ghost[a].push_back(cds[k]);
+    val[a].push_back(off[b] + css[k]);
+  }
+  for (int i = 0; i < n; ++i) {
+    if (ghost[i].empty()) continue;
+    SlbmEngine* e = g->engines[i];
+    uint32_t *pos = nullptr, *dg = nullptr, *dv = nullptr;
+    const size_t m = ghost[i].size();
+    SLBM_CUDA_TRY(cudaMalloc(&pos, size_t(e->phys_slots) * sizeof(uint32_t)));
+    SLBM_CUDA_TRY(cudaMemset(pos, 0xFF, size_t(e->phys_slots) * sizeof(uint32_t)));
+    k_slot_pos<<<1024, 256>>>(pos, e->idx, uint32_t(e->idx_pitch), uint32_t(e->n_fluid), e->q - 1,
+                              (e->q == 19) ? 1 : 0);
+    slbm::count_launch();
+    SLBM_CUDA_TRY(cudaMalloc(&dg, m * sizeof(uint32_t)));
+    SLBM_CUDA_TRY(cudaMalloc(&dv, m * sizeof(uint32_t)));
+    SLBM_CUDA_TRY(cudaMemcpy(dg, ghost[i].data(), m * 4, cudaMemcpyHostToDevice));
+    SLBM_CUDA_TRY(cudaMemcpy(dv, val[i].data(), m * 4, cudaMemcpyHostToDevice));
+    k_rewrite<<<unsigned((m + 255) / 256), 256>>>(gidx[i], pos, dg, dv, int64_t(m));
+    slbm::count_launch();
+    SLBM_CUDA_TRY(cudaDeviceSynchronize());
+    cudaFree(pos);
+    cudaFree(dg);
+    cudaFree(dv);
+  }
+  // move every engine's pdf into the pool
+  PdfPool* ref = new PdfPool{pool, 0};
+  for (int i = 0; i < n; ++i) {
+    SlbmEngine* e = g->engines[i];
+    SLBM_CUDA_TRY(cudaMemcpy(pool + off[i], e->pdf, size_t(e->phys_slots) * sizeof(double),
+                             cudaMemcpyDeviceToDevice));
+    cudaFree(e->pdf);
+    e->pdf = pool + off[i];
+    e->pool = ref;
+    ++ref->refs;
+    for (auto& gx : e->graph) {  // captured with the old buffer
+      if (gx) cudaGraphExecDestroy(gx);
+      gx = nullptr;
+    }
+  }
+  SLBM_CUDA_TRY(cudaGetLastError());
+  g->direct = true;
+  g->pool = pool;
+  g->pool_off = off;
+  g->gidx = gidx;
+  halo_disable_local(h);
+  SLBM_TRY(build_tables(g));
+  SLBM_CUDA_TRY(cudaDeviceSynchronize());
+  return SLBM_OK;
+}
+
+// the local edges' (source slot, ghost slot) pairs of a linked group, on
+// `stream`: mode 0 ghost <- source, 1 swap, 2 source <- ghost
+int slbm_group_stale_copy(SlbmGroup* g, int mode, void* stream) {
+  if (!g) return fail(SLBM_ECONFIG, "null group");
+  if (mode < 0 || mode > 2) return fail(SLBM_ECONFIG, "stale copy mode 0, 1 or 2");
+  if (!g->direct || !g->n_save) return SLBM_OK;
+  cudaSetDevice(g->device);
+  { k_pool_copy<<<unsigned((g->n_save + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        g->pool, g->save_src, g->save_dst, g->n_save, mode); slbm::count_launch(); }
+  SLBM_CUDA_TRY(cudaGetLastError());
+  return SLBM_OK;
+}
+
 int slbm_group_destroy(SlbmGroup* g) {
   if (!g) return SLBM_OK;
   cudaSetDevice(g->device);
@@ -555,6 +793,10 @@ int slbm_group_destroy(SlbmGroup* g) {
       delete g->hot128[p][f];
       delete g->hot512[p][f];
     }
+  for (auto* p : g->gidx)
+    if (p) cudaFree(p);
+  if (g->save_src) cudaFree(g->save_src);
+  if (g->save_dst) cudaFree(g->save_dst);
   void* ptrs[] = {g->ubb_eng, g->ubb_slot, g->ubb_partner, g->ubb_corr, g->steps,
                   g->out_tab, g->out_eng, g->out_idx};
   for (void* p : ptrs)

@@ -488,6 +488,24 @@ int slbm_halo_commit(SlbmHalo* h, void* nccl_comm) {
 }  // extern "C"
 
 namespace slbm {
+int halo_local_program(SlbmHalo* h, int phase, std::vector<SlbmEngine*>* engines,
+                       std::vector<uint16_t>* se, std::vector<uint32_t>* ss,
+                       std::vector<uint16_t>* de, std::vector<uint32_t>* ds) {
+  if (!h || (phase != 0 && phase != 1)) return fail(SLBM_ECONFIG, "bad halo or phase");
+  if (!h->committed) return fail(SLBM_ECONFIG, "halo not committed");
+  const PhaseProg& p = h->ph[phase];
+  *engines = h->engines;
+  *se = p.l_se;
+  *ss = p.l_ss;
+  *de = p.l_de;
+  *ds = p.l_ds;
+  return SLBM_OK;
+}
+
+void halo_disable_local(SlbmHalo* h) {
+  for (auto& p : h->ph) p.n_local = 0;
+}
+
 int halo_local_edges(SlbmHalo* h, int phase, PdfTable* table, LocalEdges* edges) {
   if (!h || (phase != 0 && phase != 1)) return fail(SLBM_ECONFIG, "bad halo or phase");
   *table = h->table();

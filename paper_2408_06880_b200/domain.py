@@ -25,6 +25,8 @@ receiver stores the storable entries.
 
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -285,6 +287,11 @@ class Domain:
         self._comm = _comm
         self._halo = self._build_halo()
         self._face_frames = self._narrow_frames() if engine_factory is None else False
+        self.direct_halo = False
+        # direct local edges (linked group): steps left in the current call,
+        # this one included (1 outside run()); see _stale_before
+        self._left = 1
+        self._stale_pending = False
         self._group = self._build_group() if engine_factory is None else None
         self.overlap_samples: list[tuple[float, float]] = []
         self.trace = False
@@ -336,7 +343,14 @@ class Domain:
         engines = self.local_engines()
         if len(engines) < 2 or any(getattr(e, "layout", "") != "sparse" for e in engines):
             return None
-        return BlockGroup(engines)
+        group = BlockGroup(engines)
+        # AA: device-local halo edges by direct addressing instead of copies
+        # (slbm_group_link_halo; bit-identical).  SLBM_DIRECT_HALO=0 keeps
+        # the copy program (A/B measurements).
+        if (self.pattern == "aa" and type(self._halo) is DeviceHalo
+                and os.environ.get("SLBM_DIRECT_HALO", "1") != "0"):
+            self.direct_halo = group.link_halo(self._halo)
+        return group
 
     # -- construction ------------------------------------------------------------
 
@@ -504,8 +518,39 @@ class Domain:
         """Local halo edges + refresh + step counters as one group launch."""
         return self._group is not None and type(self._halo) is DeviceHalo
 
+    def _stale_before(self) -> None:
+        """Linked group (direct local edges).  The copy program leaves, after
+        an AA even step, the source slots of local edges stale (its REVERSED
+        exchange delivers the even step's values before the odd step) and
+        those values in the ghosts; the linked group writes the sources
+        directly and never touches the ghosts.  So that every call hands back
+        the copy program's state slot for slot, the even step that ends a
+        call copies the stale sources into the ghosts first and swaps the
+        two afterwards (the next odd step then starts with the REVERSED
+        local exchange, ghost -> source), and the even step just before a
+        call's last (odd) step copies its values into the ghosts.  Steps in
+        the middle of a run do none of this."""
+        if not self.direct_halo:
+            return
+        if is_even(self.parity):
+            if self._left == 1:
+                self._group.stale_copy(0, self._stream)
+        elif self._stale_pending:
+            self._group.stale_copy(2, self._stream)
+            self._stale_pending = False
+
+    def _stale_after(self) -> None:
+        if not (self.direct_halo and is_even(self.parity)):
+            return
+        if self._left == 1:
+            self._group.stale_copy(1, self._stream)
+            self._stale_pending = True
+        elif self._left == 2:
+            self._group.stale_copy(0, self._stream)
+
     def step_sequential(self) -> None:
         """exchange.py:330-346 on the device: exchange, then whole-block sweeps."""
+        self._stale_before()
         phase = phase_for(self.pattern, self.parity)
         e0 = self._mark("slbm.exchange")
         if not self._has_remote and self._fused_boundary():
@@ -519,6 +564,7 @@ class Domain:
             self._count_exchange(phase)
             self._refresh_all()
         self._sweep("all")
+        self._stale_after()
         self._finish_all()
         self._mark()  # closes the last NVTX range
 
@@ -532,6 +578,7 @@ class Domain:
         avoids the split sweeps' cost (C4 artery: 0.51 -> 0.40 ms/step).
         Counters still record the interior/frame split the reference's
         overlapped driver reports."""
+        self._stale_before()
         phase = phase_for(self.pattern, self.parity)
         e0 = self._mark("slbm.exchange_start")
         fused = self._fused_boundary() and (self._face_frames or not self._has_remote)
@@ -562,6 +609,7 @@ class Domain:
             self._halo.wait(self._stream)
             self._sample(e0, e1, e2, self._mark("slbm.frame"))
             self._sweep("frame")
+        self._stale_after()
         self._finish_all()
         self._mark()  # closes the last NVTX range
 
@@ -572,15 +620,29 @@ class Domain:
         and replays it, so many-block domains are not host-launch bound."""
         fn = self._driver(driver)
         steps = int(steps)
-        if use_graph and self.check == "deferred" and self._graph_capable():
-            while steps >= 2:
-                self._replay_pair(driver, fn)
-                steps -= 2
-        for _ in range(steps):
-            fn()
-            if self.check == "step":
-                self._poll_or_raise()
-            self.steps_done += 1
+        try:
+            if use_graph and self.check == "deferred" and self._graph_capable():
+                # graphs hold (even, odd) pairs of mid-run steps: an odd start
+                # runs one step first, the last two steps run alone
+                if not is_even(self.parity) and steps >= 5:
+                    self._left = steps
+                    fn()
+                    if self.check == "step":
+                        self._poll_or_raise()
+                    self.steps_done += 1
+                    steps -= 1
+                self._left = steps
+                while steps >= 4 and is_even(self.parity):
+                    self._replay_pair(driver, fn)
+                    steps -= 2
+            for k in range(steps):
+                self._left = steps - k
+                fn()
+                if self.check == "step":
+                    self._poll_or_raise()
+                self.steps_done += 1
+        finally:
+            self._left = 1
 
     def _graph_capable(self) -> bool:
         return bool(self._stream) and isinstance(self._halo, DeviceHalo)
@@ -733,6 +795,22 @@ class BlockGroup:
         h = C.c_void_p()
         _abi.call("slbm_group_create", arr, len(self.engines), C.byref(h))
         self._h = h
+
+    def link_halo(self, halo) -> bool:
+        """Serve ``halo``'s device-local edges by direct addressing
+        (slbm_group_link_halo); False when not applicable (nothing changed)."""
+        from . import _abi
+
+        return _abi.load().slbm_group_link_halo(self._h, halo.handle) == 0
+
+    def stale_copy(self, mode: int, stream):
+        """slbm_group_stale_copy: local edges' source/ghost slots, mode 0
+        ghost <- source, 1 swap, 2 source <- ghost."""
+        import ctypes as C
+
+        from . import _abi
+
+        _abi.call("slbm_group_stale_copy", self._h, int(mode), C.c_void_p(stream or 0))
 
     def close(self):
         from . import _abi
