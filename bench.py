@@ -848,16 +848,17 @@ def impl_artery(args, rank, world, local_rank):
     from paper_2408_06880_b200 import _abi
 
     launches0 = _abi.launch_count()
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps // 2 + 1)]
+    # one run() call (whole-domain graph per step pair): a linked group does
+    # its call-boundary work once, as a user's long run does
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     evs[0].record(stream)
-    for k in range(steps // 2):  # whole-domain graph per step pair, an event after each
-        dom.run(2, driver="overlapped", use_graph=True)
-        evs[k + 1].record(stream)
+    dom.run(steps, driver="overlapped", use_graph=True)
+    evs[1].record(stream)
     evs[-1].synchronize()
     launches = int(reduce(_abi.launch_count() - launches0, "sum"))
     clocks.mark("t1")
     ms = reduce(evs[0].elapsed_time(evs[-1]))
-    t_pair = reduce(statistics.mean(evs[k].elapsed_time(evs[k + 1]) for k in range(steps // 2)))
+    t_pair = ms / (steps // 2)
     dom.poll()
     clocks.stop()
     total = int(reduce(dom.local_fluid(), "sum"))
@@ -897,8 +898,8 @@ def impl_artery(args, rank, world, local_rank):
                    "blocks_per_rank": len(dom.local_engines()), "build_s": round(build_s, 2),
                    "l2": "inputs larger than L2 (~1.5 GB)"},
         "roofline": {"bound": "hbm", "kernel": "whole step: block-group sweeps + halo + boundary",
-                     "timing": "CUDA events after every step pair inside the timed region, max "
-                               "over ranks", "ms_per_pair": round(t_pair, 4),
+                     "timing": "CUDA events around the timed run() call (one graph replay per "
+                               "step pair), mean per pair, max over ranks", "ms_per_pair": round(t_pair, 4),
                      "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                      "frac": round(achieved / hbm, 4), "traffic": None,
                      "bytes_per_cell": (BYTES_EVEN + BYTES_ODD) / 2, "peak_source": hbm_src},

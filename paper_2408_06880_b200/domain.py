@@ -622,17 +622,18 @@ class Domain:
         steps = int(steps)
         try:
             if use_graph and self.check == "deferred" and self._graph_capable():
-                # graphs hold (even, odd) pairs of mid-run steps: an odd start
-                # runs one step first, the last two steps run alone
-                if not is_even(self.parity) and steps >= 5:
+                # graphs hold (even, odd) pairs: an odd start runs one step
+                # first; a linked group's last pair of a call is its own
+                # graph (the call-boundary copy after the even step)
+                if not is_even(self.parity) and steps >= 3:
                     self._left = steps
                     fn()
                     if self.check == "step":
                         self._poll_or_raise()
                     self.steps_done += 1
                     steps -= 1
-                self._left = steps
-                while steps >= 4 and is_even(self.parity):
+                while steps >= 2 and is_even(self.parity):
+                    self._left = steps
                     self._replay_pair(driver, fn)
                     steps -= 2
             for k in range(steps):
@@ -654,7 +655,8 @@ class Domain:
         # the captured pair bakes in buffer pointers: AA keys on parity, pull
         # on which of each engine's two buffers is current (finish_step swaps)
         key = (driver, getattr(self.parity, "value", self.parity),
-               tuple(e.buffer_state() for e in self.local_engines()))
+               tuple(e.buffer_state() for e in self.local_engines()),
+               self.direct_halo and self._left == 2)
         graphs = self.__dict__.setdefault("_graphs", {})
         if key not in graphs:
             engines = self.local_engines()

@@ -442,7 +442,15 @@ def test_launch_count_is_graph_aware(gpu_lib):
     c0 = _abi.launch_count()
     dom.run(2, driver="overlapped")
     eager = _abi.launch_count() - c0
-    dom.run(2, driver="overlapped", use_graph=True)  # capture + first replay
+    dom.run(6, driver="overlapped", use_graph=True)  # capture + first replay
+    # run(n) replays (even, odd) pairs; a linked group's last pair of a call
+    # is its own graph (with the call-boundary copy), so two more steps per
+    # call are exactly one more replay of the mid-run pair
     c0 = _abi.launch_count()
     dom.run(4, driver="overlapped", use_graph=True)
-    assert _abi.launch_count() - c0 == 2 * eager > 0
+    n4 = _abi.launch_count() - c0
+    c0 = _abi.launch_count()
+    dom.run(6, driver="overlapped", use_graph=True)
+    pair = _abi.launch_count() - c0 - n4
+    # one block group: one boundary launch + one sweep per step
+    assert pair == 4 and eager >= 4

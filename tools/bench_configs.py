@@ -125,7 +125,7 @@ def c3(steps):
         eng.run(4)
         ms = timed_run(eng, steps)
         eng.poll()
-        te, to = bench.time_kernels(eng, torch)
+        _, te, to = bench.timed_steps(eng, 20, torch, torch.cuda.ExternalStream(eng.stream()))
         be, bo = 2 * 27 * 8 + 26 * 4, 2 * 27 * 8
         nf = eng.n_fluid
         emit({"config": "c3", "model": model, "n_fluid": nf, "porosity": round(nf / edge**3, 4),
