@@ -147,11 +147,15 @@ int slbm_canonical_state(SlbmEngine* eng, double* values);
 /* host rho (rev_shape) and u (rev_shape + (dim,)), zeros at non-fluid cells;
  * SLBM_EUNSTABLE when a density is <= 0 or non-finite (core.py:108-111)    */
 int slbm_macroscopic(SlbmEngine* eng, double* rho, double* u);
-/* sum over fluid cells and directions of the canonical state (mass), fp64 */
 /* the same fields per fluid cell in cid order (rho: n_fluid, u: n_fluid x
  * dim): what Domain.gather_macroscopics scatters into the global box for
  * sparse blocks instead of moving each block's full box                   */
 int slbm_macroscopic_compact(SlbmEngine* eng, double* rho, double* u);
+/* Monitors: total mass and momentum of the canonical state over all fluid
+ * cells, fp64 -- one pass over the groups, warp-shuffle reductions with a
+ * fixed reduction tree (bit-reproducible run to run).  out4 = {mass,
+ * momentum x, y, z}; total_mass = out4[0].                                 */
+int slbm_total_moments(SlbmEngine* eng, double* out4);
 int slbm_total_mass(SlbmEngine* eng, double* mass);
 
 /* ---- stepping (sparse.py:226-304) ---------------------------------------- */

@@ -67,6 +67,7 @@ SIGNATURES = {
     "slbm_macroscopic": [vp, c_dp, c_dp],
     "slbm_macroscopic_compact": [vp, C.POINTER(C.c_double), C.POINTER(C.c_double)],
     "slbm_total_mass": [vp, c_dp],
+    "slbm_total_moments": [vp, c_dp],
     "slbm_refresh_boundary": [vp, C.c_int],
     "slbm_step": [vp, C.c_int],
     "slbm_finish_step": [vp],

@@ -668,31 +668,47 @@ int slbm_macroscopic_compact(SlbmEngine* e, double* rho, double* u) {
   return copy_d2h(u, d_u, n * e->dim * sizeof(double), e->device, e->stream);
 }
 
-int slbm_total_mass(SlbmEngine* e, double* mass) {
+int slbm_total_moments(SlbmEngine* e, double* out4) {
   CHECK_ENGINE(e);
+  if (!out4) return fail(SLBM_ECONFIG, "null output");
   DeviceGuard guard(e->device);
   const bool odd = e->pattern == SLBM_AA && e->parity == SLBM_ODD;
   if (odd) SLBM_TRY(launch_refresh(e, SLBM_ODD));
-  const size_t nq = e->layout ? size_t(e->q) * e->n_fluid : 0;
-  SLBM_TRY(e->ensure_scratch((size_t(e->q) + nq) * sizeof(double)));
-  if (e->layout) {
+  if (e->layout) {  // dense: canonical (q, n) array, per-direction sums
+    const size_t nq = size_t(e->q) * e->n_fluid;
+    SLBM_TRY(e->ensure_scratch((size_t(e->q) + nq) * sizeof(double)));
     double* d_f = e->d_scratch + e->q;
     SLBM_TRY(dense_canonical(e, d_f));
     for (int r = 0; r < e->q; ++r)
       SLBM_TRY(launch_sum(d_f + size_t(r) * e->n_fluid, e->n_fluid, e->d_scratch + r, e->stream));
-  } else {
+    std::vector<double> parts(e->q);
+    SLBM_CUDA_TRY(cudaMemcpyAsync(parts.data(), e->d_scratch, e->q * sizeof(double),
+                                  cudaMemcpyDeviceToHost, e->stream));
+    SLBM_CUDA_TRY(cudaStreamSynchronize(e->stream));
+    for (int k = 0; k < 4; ++k) out4[k] = 0.0;
     for (int r = 0; r < e->q; ++r) {
-      const int g = odd ? e->dirs.inv[r] : r;
-      SLBM_TRY(launch_sum(e->pdf + e->pbase[g], e->n_fluid, e->d_scratch + r, e->stream));
+      out4[0] += parts[r];
+      for (int a = 0; a < 3; ++a)
+        if (e->dirs.c[r][a] > 0)
+          out4[1 + a] += parts[r];
+        else if (e->dirs.c[r][a] < 0)
+          out4[1 + a] -= parts[r];
     }
+    return SLBM_OK;
   }
-  std::vector<double> parts(e->q);
-  SLBM_CUDA_TRY(cudaMemcpyAsync(parts.data(), e->d_scratch, e->q * sizeof(double),
-                                cudaMemcpyDeviceToHost, e->stream));
+  SLBM_TRY(e->ensure_scratch(4 * sizeof(double)));
+  SLBM_TRY(launch_moments(e, e->d_scratch));
+  SLBM_CUDA_TRY(cudaMemcpyAsync(out4, e->d_scratch, 4 * sizeof(double), cudaMemcpyDeviceToHost,
+                                e->stream));
   SLBM_CUDA_TRY(cudaStreamSynchronize(e->stream));
-  double m = 0.0;
-  for (double p : parts) m += p;
-  *mass = m;
+  return SLBM_OK;
+}
+
+int slbm_total_mass(SlbmEngine* e, double* mass) {
+  if (!mass) return fail(SLBM_ECONFIG, "null output");
+  double m[4];
+  SLBM_TRY(slbm_total_moments(e, m));
+  *mass = m[0];
   return SLBM_OK;
 }
 

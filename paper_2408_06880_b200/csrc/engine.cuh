@@ -183,6 +183,7 @@ int launch_fill(double* p, int64_t n, double v, cudaStream_t s);
 int launch_equilibrium(SlbmEngine* e, const double* rho, int rho_scalar, const double* u,
                        int u_scalar, double* dev_out);
 int launch_sum(const double* p, int64_t n, double* dev_out, cudaStream_t s);
+int launch_moments(SlbmEngine* e, double* dev_out);  // mass, momentum x/y/z (sparse)
 int launch_equilibrium_qn(SlbmEngine* e, const double* rho, int rho_scalar, const double* u,
                           int u_scalar, double* out);
 int launch_slot_lookup(SlbmEngine* e, const int64_t* d_qs, const int64_t* d_pflat, int64_t n,

@@ -16,7 +16,6 @@
 //              gather as the even step, dst[base[r] + c] = out_r; 376 B/cell
 // base[] / idx hold device addresses (256-B aligned groups, engine.cuh).
 #include <cooperative_groups.h>
-#include <cub/cub.cuh>
 
 #include <algorithm>
 #include <climits>
@@ -720,13 +719,105 @@ int launch_fill(double* p, int64_t n, double v, cudaStream_t s) {
   return SLBM_OK;
 }
 
+// Deterministic reductions with warp shuffles: a fixed grid of kRedBlocks
+// CTAs strides over the input (the assignment of elements to threads, and
+// so the summation order, depends only on n), each CTA reduces its 256
+// partial sums through __shfl_down_sync and one shared-memory step into one
+// partial per CTA, and a single CTA reduces the kRedBlocks partials in the
+// same fixed tree order.  Same input -> same bits on every run (an atomic
+// accumulation would not be), no library kernel on the path.
+constexpr int kRedBlocks = 592;  // 148 SMs x 4
+constexpr int kRedThreads = 256;
+
+template <int K>
+__device__ __forceinline__ void block_reduce_store(double (&v)[K], double* out) {
+  __shared__ double w[kRedThreads / 32][K];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int k = 0; k < K; ++k)
+    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_down_sync(0xffffffffu, v[k], o);
+  if (lane == 0)
+    for (int k = 0; k < K; ++k) w[warp][k] = v[k];
+  __syncthreads();
+  if (warp == 0) {
+    for (int k = 0; k < K; ++k) {
+      double x = lane < kRedThreads / 32 ? w[lane][k] : 0.0;
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+      if (lane == 0) out[k] = x;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_sum_partial(const double* p, int64_t n,
+                                                             double* part) {
+  double v[1] = {0.0};
+  for (int64_t i = int64_t(blockIdx.x) * kRedThreads + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * kRedThreads)
+    v[0] += p[i];
+  block_reduce_store<1>(v, part + blockIdx.x);
+}
+
+// mass and momentum of every fluid cell from its canonical populations at
+// the current parity (even: group q; odd: group inv q), one pass
+template <class L>
+__global__ void __launch_bounds__(kRedThreads) k_moments_partial(const double* pdf, SweepArgs a,
+                                                                 int odd, double* part) {
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  for (uint32_t c = blockIdx.x * kRedThreads + threadIdx.x; c < a.n_fluid;
+       c += gridDim.x * kRedThreads) {
+    double rho = 0.0, j[3] = {0.0, 0.0, 0.0};
+    sfor<0, L::Q>([&](auto q) {
+      constexpr int qb = L::INV[q];
+      const double f = pdf[a.base[odd ? qb : int(q)] + c];
+      rho += f;
+      if constexpr (L::CX[q] > 0) j[0] += f;
+      if constexpr (L::CX[q] < 0) j[0] -= f;
+      if constexpr (L::CY[q] > 0) j[1] += f;
+      if constexpr (L::CY[q] < 0) j[1] -= f;
+      if constexpr (L::CZ[q] > 0) j[2] += f;
+      if constexpr (L::CZ[q] < 0) j[2] -= f;
+    });
+    v[0] += rho;
+    v[1] += j[0];
+    v[2] += j[1];
+    v[3] += j[2];
+  }
+  block_reduce_store<4>(v, part + 4 * blockIdx.x);
+}
+
+// K sums of `n` strided partials (partial b of sum k at part[b * K + k])
+template <int K>
+__global__ void __launch_bounds__(kRedThreads) k_reduce_final(const double* part, int n,
+                                                              double* out) {
+  double v[K];
+  for (int k = 0; k < K; ++k) v[k] = 0.0;
+  for (int b = threadIdx.x; b < n; b += kRedThreads)
+    for (int k = 0; k < K; ++k) v[k] += part[b * K + k];
+  block_reduce_store<K>(v, out);
+}
+
 int launch_sum(const double* p, int64_t n, double* dev_out, cudaStream_t s) {
-  size_t tmp_bytes = 0;
-  SLBM_CUDA_TRY(cub::DeviceReduce::Sum(nullptr, tmp_bytes, p, dev_out, n, s));
-  void* tmp = nullptr;
-  SLBM_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, s));
-  SLBM_CUDA_TRY(cub::DeviceReduce::Sum(tmp, tmp_bytes, p, dev_out, n, s));
-  SLBM_CUDA_TRY(cudaFreeAsync(tmp, s));
+  double* part = nullptr;
+  SLBM_CUDA_TRY(cudaMallocAsync(&part, kRedBlocks * sizeof(double), s));
+  { k_sum_partial<<<kRedBlocks, kRedThreads, 0, s>>>(p, n, part); slbm::count_launch(); }
+  { k_reduce_final<1><<<1, kRedThreads, 0, s>>>(part, kRedBlocks, dev_out); slbm::count_launch(); }
+  SLBM_CUDA_TRY(cudaGetLastError());
+  SLBM_CUDA_TRY(cudaFreeAsync(part, s));
+  return SLBM_OK;
+}
+
+// total mass and momentum (4 doubles at dev_out) of a sparse engine
+int launch_moments(SlbmEngine* e, double* dev_out) {
+  SweepArgs a = sweep_args(e);
+  const int odd = (e->pattern == SLBM_AA && e->parity == SLBM_ODD) ? 1 : 0;
+  double* part = nullptr;
+  SLBM_CUDA_TRY(cudaMallocAsync(&part, 4 * kRedBlocks * sizeof(double), e->stream));
+  by_lattice(e->q, [&](auto lat) {
+    using L = decltype(lat);
+    { k_moments_partial<L><<<kRedBlocks, kRedThreads, 0, e->stream>>>(e->pdf, a, odd, part); slbm::count_launch(); }
+  });
+  { k_reduce_final<4><<<1, kRedThreads, 0, e->stream>>>(part, kRedBlocks, dev_out); slbm::count_launch(); }
+  SLBM_CUDA_TRY(cudaGetLastError());
+  SLBM_CUDA_TRY(cudaFreeAsync(part, e->stream));
   return SLBM_OK;
 }
 

@@ -753,6 +753,15 @@ class Domain:
             flat_out[:, flat] = blk.engine.canonical_state()
         return out
 
+    def total_moments(self) -> np.ndarray:
+        """(mass, momentum x, y, z) over this rank's fluid cells (monitor):
+        per block one device pass with warp-shuffle reductions, summed in
+        block order."""
+        tot = np.zeros(4)
+        for e in self.local_engines():
+            tot += e.total_moments()
+        return tot
+
     def counters(self) -> Counters:
         total = Counters()
         for e in self.local_engines():

@@ -445,6 +445,13 @@ class SparseEngine:
         _abi.call("slbm_total_mass", self._h, C.byref(m))
         return float(m.value)
 
+    def total_moments(self) -> np.ndarray:
+        """(mass, momentum x, y, z) of the canonical state: one device pass,
+        warp-shuffle reductions in a fixed order (bit-reproducible)."""
+        out = np.zeros(4)
+        _abi.call("slbm_total_moments", self._h, _abi.ptr(out, C.c_double))
+        return out
+
     # -- exchange access ------------------------------------------------------------
 
     def _pflat(self, coords: np.ndarray) -> np.ndarray:
