@@ -23,6 +23,7 @@ p = CollisionParams(bench.OMEGA, "trt", bench.magic_lambda(bench.OMEGA))
 from paper_2408_06880_b200 import _abi  # noqa: E402
 
 _abi.load().slbm_set_tuning(0, int(os.environ.get("VARIANT", 0)))
+_abi.load().slbm_set_tuning(2, int(os.environ.get("AHEAD", 1)))  # idx prefetch, quarter waves
 eng = SparseEngine(bench.make_flags(512, 0), st, p, "aa", device=0, check="deferred")
 eng.init_equilibrium(1.0, np.array([0.01, 0.0, 0.0]))
 eng.run(10)
@@ -60,7 +61,7 @@ for w in range(0, steps, 40):
     e = [t for t, q in zip(per[w:w + 40], par[w:w + 40]) if q == 0]
     o = [t for t, q in zip(per[w:w + 40], par[w:w + 40]) if q == 1]
     win.append((round(float(np.mean(e)), 4), round(float(np.mean(o)), 4)))
-print(json.dumps({"variant": int(os.environ.get("VARIANT", 0)),
+print(json.dumps({"variant": int(os.environ.get("VARIANT", 0)), "ahead": int(os.environ.get("AHEAD", 1)),
                   "mean_even_ms": round(float(np.mean([t for t, q in zip(per, par) if q == 0])), 4),
                   "mean_odd_ms": round(float(np.mean([t for t, q in zip(per, par) if q == 1])), 4),
                   "windows_even_odd_ms": win, "clock_samples": clocks[::4]}))
