@@ -156,6 +156,14 @@ int slbm_macroscopic_compact(SlbmEngine* eng, double* rho, double* u);
  * fixed reduction tree (bit-reproducible run to run).  out4 = {mass,
  * momentum x, y, z}; total_mass = out4[0].                                 */
 int slbm_total_moments(SlbmEngine* eng, double* out4);
+/* Domain.gather_macroscopics on the device (domain.py:246-268): write this
+ * block's fluid cells' rho / u into global device boxes (gdims = global
+ * x, y, z extents; the block at origin x, y, z; solids untouched, so the
+ * caller zeroes the boxes), then move a box to host memory with the staged
+ * multi-threaded copy (any host buffer; pinned ones go by one DMA).      */
+int slbm_macroscopic_global(SlbmEngine* eng, double* dev_rho, double* dev_u,
+                            const int64_t* gdims, const int64_t* origin);
+int slbm_copy_to_host(void* host, const void* dev, int64_t bytes, int device);
 int slbm_total_mass(SlbmEngine* eng, double* mass);
 
 /* ---- stepping (sparse.py:226-304) ---------------------------------------- */

@@ -68,6 +68,8 @@ SIGNATURES = {
     "slbm_macroscopic_compact": [vp, C.POINTER(C.c_double), C.POINTER(C.c_double)],
     "slbm_total_mass": [vp, c_dp],
     "slbm_total_moments": [vp, c_dp],
+    "slbm_macroscopic_global": [vp, vp, vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
+    "slbm_copy_to_host": [vp, vp, C.c_int64, C.c_int],
     "slbm_refresh_boundary": [vp, C.c_int],
     "slbm_step": [vp, C.c_int],
     "slbm_finish_step": [vp],

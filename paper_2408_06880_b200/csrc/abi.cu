@@ -668,6 +668,26 @@ int slbm_macroscopic_compact(SlbmEngine* e, double* rho, double* u) {
   return copy_d2h(u, d_u, n * e->dim * sizeof(double), e->device, e->stream);
 }
 
+int slbm_macroscopic_global(SlbmEngine* e, double* dev_rho, double* dev_u,
+                            const int64_t* gdims, const int64_t* origin) {
+  CHECK_ENGINE(e);
+  if (!dev_rho || !dev_u || !gdims || !origin) return fail(SLBM_ECONFIG, "null argument");
+  if (e->layout) return fail(SLBM_ECONFIG, "global-box read-out: sparse engines only");
+  for (int k = 0; k < 3; ++k)
+    if (origin[k] < 0 || (k < e->dim && origin[k] + e->geo.n[k] > gdims[k]))
+      return fail(SLBM_ECONFIG, "block outside the global box");
+  DeviceGuard guard(e->device);
+  const bool odd = e->pattern == SLBM_AA && e->parity == SLBM_ODD;
+  if (odd) SLBM_TRY(launch_refresh(e, SLBM_ODD));
+  return launch_macroscopic(e, nullptr, dev_rho, dev_u, false, gdims, origin);
+}
+
+int slbm_copy_to_host(void* host, const void* dev, int64_t bytes, int device) {
+  if (!host || !dev || bytes < 0) return fail(SLBM_ECONFIG, "bad copy arguments");
+  DeviceGuard guard(device);
+  return copy_d2h(host, dev, size_t(bytes), device, nullptr);
+}
+
 int slbm_total_moments(SlbmEngine* e, double* out4) {
   CHECK_ENGINE(e);
   if (!out4) return fail(SLBM_ECONFIG, "null output");

@@ -173,8 +173,11 @@ inline void free_pair(SlbmEngine*) {}
 #endif
 int launch_canonical(SlbmEngine* e, double* dev_out);  // (q, n) at current parity
 // box layout (zeros at solids must be pre-set) or compact: one value per fluid cell
+// gdims/origin: write into a global box (rows of gdims[0], gdims[1] rows per
+// plane) at the block's origin instead of the block's own box
 int launch_macroscopic(SlbmEngine* e, const double* dev_canon, double* dev_rho, double* dev_u,
-                       bool compact = false);
+                       bool compact = false, const int64_t* gdims = nullptr,
+                       const int64_t* origin = nullptr);
 int launch_gather(const double* src, const uint32_t* slots, int64_t n, double* out,
                   cudaStream_t s);
 int launch_scatter(double* dst, const uint32_t* slots, int64_t n, const double* in,

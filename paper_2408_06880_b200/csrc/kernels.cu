@@ -303,9 +303,17 @@ __global__ void k_outlet(double* pdf, SweepArgs a, const uint32_t* slot, const u
 }
 
 // canonical (q, n) values per cell straight from the groups (sparse.py:308-321)
+// out: gx == 0 -> the block's own box (or compact with x_flat == nullptr);
+// gx > 0 -> a global box of row length gx, gy rows per plane, the block at
+// origin (ox, oy, oz) (Domain.gather_macroscopics on the device)
+struct MacroOut {
+  int64_t gx = 0, gy = 0, ox = 0, oy = 0, oz = 0;
+};
+
 template <class L>
 __global__ void k_macro(const double* pdf, SweepArgs a, int odd, Geometry g,
-                        const uint32_t* x_flat, double* rho_f, double* u_f, int* bad) {
+                        const uint32_t* x_flat, double* rho_f, double* u_f, int* bad,
+                        MacroOut o) {
   const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= a.n_fluid) return;
   double t[L::Q];
@@ -319,7 +327,7 @@ __global__ void k_macro(const double* pdf, SweepArgs a, int odd, Geometry g,
   if (x_flat) {
     int64_t x, y, z;
     g.coords(x_flat[c], x, y, z);
-    f = g.interior_flat(x, y, z);
+    f = o.gx ? ((z + o.oz) * o.gy + (y + o.oy)) * o.gx + (x + o.ox) : g.interior_flat(x, y, z);
   }
   rho_f[f] = m.rho;
   u_f[f * L::DIM + 0] = m.ux;
@@ -623,7 +631,7 @@ int launch_resident(SlbmEngine* e, int64_t n) {
 // canonical: nullptr -> read the sparse groups of e->pdf at the current
 // parity; else a (q, n_fluid) canonical array (dense engine)
 int launch_macroscopic(SlbmEngine* e, const double* canonical, double* dev_rho, double* dev_u,
-                       bool compact) {
+                       bool compact, const int64_t* gdims, const int64_t* origin) {
   SweepArgs a = sweep_args(e);
   const double* src = e->pdf;
   int odd = (e->pattern == SLBM_AA && e->parity == SLBM_ODD) ? 1 : 0;
@@ -637,8 +645,10 @@ int launch_macroscopic(SlbmEngine* e, const double* canonical, double* dev_rho, 
   SLBM_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int), e->stream));
   by_lattice(e->q, [&](auto lat) {
     using L = decltype(lat);
+    MacroOut o{};
+    if (gdims) o = MacroOut{gdims[0], gdims[1], origin[0], origin[1], origin[2]};
     { k_macro<L><<<grid_for(e->n_fluid, 256), 256, 0, e->stream>>>(
-        src, a, odd, e->geo, compact ? nullptr : e->x_flat, dev_rho, dev_u, bad); slbm::count_launch(); }
+        src, a, odd, e->geo, compact ? nullptr : e->x_flat, dev_rho, dev_u, bad, o); slbm::count_launch(); }
   });
   int h_bad = 0;
   SLBM_CUDA_TRY(cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, e->stream));

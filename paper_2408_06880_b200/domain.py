@@ -719,10 +719,19 @@ class Domain:
         return self.global_flags.tags_interior == FLUID
 
     def gather_macroscopics(self):
-        """domain.py:246-268: global (rho, u) with zeros at solids.  Sparse
-        blocks below porosity 0.5 move only their fluid cells' values
-        (slbm_macroscopic_compact) and scatter them here; denser ones move
-        their whole box."""
+        """domain.py:246-268: global (rho, u) with zeros at solids.
+
+        Sparse domains assemble the global box on the device -- every block
+        writes its fluid cells' fields into one zeroed device box
+        (slbm_macroscopic_global) -- and move it with one staged copy per
+        field (slbm_copy_to_host).  A host-side scatter of the per-block
+        values into a fresh multi-GB box is latency bound (C4 artery: ~1.7 s
+        for 6.3 M cells into a 4.3 GB box, the device path ~0.2 s).  Other
+        domains (dense blocks, or a box that does not fit the free device
+        memory) gather per block on the host."""
+        fast = self._gather_macroscopics_device()
+        if fast is not None:
+            return fast
         shape = rev_shape(self.global_dims)
         dim = self.stencil.dim
         rho = np.zeros(shape)
@@ -741,6 +750,43 @@ class Domain:
                         for a in reversed(range(dim)))
             rho[sel] = r
             u[sel] = v
+        return rho, u
+
+    def _gather_macroscopics_device(self):
+        engines = [b.engine for b in self.local_blocks()]
+        if not engines or any(getattr(e, "layout", "") != "sparse" or not hasattr(e, "handle")
+                              for e in engines):
+            return None
+        import ctypes as C
+
+        import torch
+
+        from . import _abi
+
+        shape = rev_shape(self.global_dims)
+        dim = self.stencil.dim
+        n = int(np.prod(shape))
+        need = 8 * n * (1 + dim)
+        dev = torch.device("cuda", int(engines[0].device))
+        free, _ = torch.cuda.mem_get_info(dev)
+        if need > free // 2:
+            return None
+        d_rho = torch.zeros(n, dtype=torch.float64, device=dev)
+        d_u = torch.zeros(n * dim, dtype=torch.float64, device=dev)
+        torch.cuda.synchronize(dev)
+        gd = np.array(list(self.global_dims) + [1] * (3 - len(self.global_dims)), dtype=np.int64)
+        for blk in self.local_blocks():
+            org = np.array(list(blk.origin) + [0] * (3 - len(blk.origin)), dtype=np.int64)
+            if blk.engine.check == "deferred":
+                blk.engine.poll()  # raise a pending instability, as macroscopic_fields does
+            _abi.call("slbm_macroscopic_global", blk.engine.handle, C.c_void_p(d_rho.data_ptr()),
+                      C.c_void_p(d_u.data_ptr()), _abi.ptr(gd, C.c_int64), _abi.ptr(org, C.c_int64))
+        rho = np.empty(shape)
+        u = np.empty(shape + (dim,))
+        _abi.call("slbm_copy_to_host", _abi.ptr(rho, C.c_double), C.c_void_p(d_rho.data_ptr()),
+                  rho.nbytes, int(engines[0].device))
+        _abi.call("slbm_copy_to_host", _abi.ptr(u, C.c_double), C.c_void_p(d_u.data_ptr()),
+                  u.nbytes, int(engines[0].device))
         return rho, u
 
     def gather_canonical(self) -> np.ndarray:
