@@ -64,6 +64,13 @@ struct GroupHot {
   uint32_t start[CAP + 1];
   HotArgs hot[CAP];
 };
+// the boundary launch's per-engine buffer and group starts, as kernel
+// parameters (the UBB / outlet entries then need no table-row load)
+template <int CAP>
+struct BoundaryHot {
+  double* pdf[CAP];
+  uint32_t base[CAP][28];
+};
 }  // namespace slbm
 
 using namespace slbm;
@@ -109,6 +116,14 @@ struct SlbmGroup {
   struct OutletTab* out_tab = nullptr;
   uint16_t* out_eng = nullptr;
   uint32_t* out_idx = nullptr;
+  // the outlet program flattened in entry order (one coalesced load per
+  // field instead of engine table -> arrays -> entry)
+  uint32_t *fo_slot = nullptr, *fo_partner = nullptr, *fo_cell = nullptr;
+  uint8_t* fo_dir = nullptr;
+  double* fo_rho = nullptr;
+  double** fo_u = nullptr;
+  BoundaryHot<16>* bhot16[2] = {};
+  BoundaryHot<128>* bhot128[2] = {};
   int64_t n_out = 0;
 };
 
@@ -416,6 +431,113 @@ __global__ void k_rewrite(uint32_t* gidx, const uint32_t* pos, const uint32_t* g
   if (p != 0xFFFFFFFFu) gidx[p] = val[i];
 }
 
+__global__ void k_flatten_outlet(const OutletTab* ot, const uint16_t* oeng, const uint32_t* oidx,
+                                 int64_t n, uint32_t* slot, uint32_t* partner, uint32_t* cell,
+                                 uint8_t* dir, double* rho, double** u) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const OutletTab& o = ot[oeng[i]];
+  const uint32_t k = oidx[i];
+  slot[i] = o.slot[k];
+  partner[i] = o.partner[k];
+  cell[i] = o.cell[k];
+  dir[i] = o.dir[k];
+  rho[i] = o.rho[k];
+  u[i] = o.u + 3 * size_t(k);
+}
+
+// The boundary launch with the engines' buffers and group starts in the
+// kernel parameters and the outlet program flattened: every entry is one
+// round of coalesced index loads, then its PDF loads (the table version
+// went entry -> engine table row -> arrays -> PDFs).  Same work and order
+// per entry as k_group_boundary (halo CTAs included).
+template <class L, int CAP>
+__global__ void __launch_bounds__(kBT) k_group_boundary_hot(
+    const __grid_constant__ BoundaryHot<CAP> bh, const __grid_constant__ PdfTable lt,
+    LocalEdges le, const uint16_t* __restrict__ ueng, const uint32_t* __restrict__ uslot,
+    const uint32_t* __restrict__ upartner, const double* __restrict__ ucorr, int64_t n_ubb,
+    const uint16_t* __restrict__ oeng, const uint32_t* __restrict__ fo_slot,
+    const uint32_t* __restrict__ fo_partner, const uint32_t* __restrict__ fo_cell,
+    const uint8_t* __restrict__ fo_dir, const double* __restrict__ fo_rho, double* const* fo_u,
+    int64_t n_out, unsigned long long** steps, int n_eng, int parity, uint32_t cta_halo,
+    uint32_t cta_ubb) {
+  pdl_launch_dependents();
+  const uint32_t b = blockIdx.x;
+  if (b == 0) {
+    pdl_wait();  // the previous sweep reads the step counters
+    for (int e = threadIdx.x; e < n_eng; e += kBT) *steps[e] += 1;
+  }
+  if (b < cta_halo) {
+    __shared__ double* sp[kMaxHaloEngines];
+    for (int e = threadIdx.x; e < le.n_eng; e += kBT) sp[e] = gmem(lt.p[e]);
+    __syncthreads();
+    const int64_t i0 = int64_t(b) * kBT * kBItems + threadIdx.x;
+    uint16_t se[kBItems], de[kBItems];
+    uint32_t ss[kBItems], ds[kBItems];
+    double v[kBItems];
+#pragma unroll
+    for (int k = 0; k < kBItems; ++k) {
+      const int64_t i = i0 + k * kBT;
+      if (i < le.n) {
+        se[k] = le.se[i];
+        ss[k] = le.ss[i];
+        de[k] = le.de[i];
+        ds[k] = le.ds[i];
+      }
+    }
+    pdl_wait();
+#pragma unroll
+    for (int k = 0; k < kBItems; ++k)
+      if (i0 + k * kBT < le.n) v[k] = gmem(sp[se[k]])[ss[k]];
+#pragma unroll
+    for (int k = 0; k < kBItems; ++k)
+      if (i0 + k * kBT < le.n) gmem(sp[de[k]])[ds[k]] = v[k];
+    return;
+  }
+  if (b < cta_halo + cta_ubb) {  // sparse.py:301-304
+    const int64_t i0 = int64_t(b - cta_halo) * kBT * kBItems + threadIdx.x;
+    double* pdf[kBItems];
+    uint32_t from[kBItems], to[kBItems];
+    double corr[kBItems], v[kBItems];
+#pragma unroll
+    for (int k = 0; k < kBItems; ++k) {
+      const int64_t i = i0 + k * kBT;
+      if (i < n_ubb) {
+        pdf[k] = gmem(bh.pdf[ueng[i]]);
+        from[k] = parity == SLBM_EVEN ? upartner[i] : uslot[i];
+        to[k] = parity == SLBM_EVEN ? uslot[i] : upartner[i];
+        corr[k] = ucorr[i];
+      }
+    }
+    pdl_wait();
+#pragma unroll
+    for (int k = 0; k < kBItems; ++k)
+      if (i0 + k * kBT < n_ubb) v[k] = pdf[k][from[k]];
+#pragma unroll
+    for (int k = 0; k < kBItems; ++k)
+      if (i0 + k * kBT < n_ubb) pdf[k][to[k]] = v[k] + corr[k];
+    return;
+  }
+  const int64_t i = int64_t(b - cta_halo - cta_ubb) * kBT + threadIdx.x;
+  int e = 0;
+  uint32_t slot = 0, partner = 0, cell = 0;
+  int dir = 0;
+  double rho = 0.0;
+  double* u = nullptr;
+  if (i < n_out) {
+    e = oeng[i];
+    slot = fo_slot[i];
+    partner = fo_partner[i];
+    cell = fo_cell[i];
+    dir = fo_dir[i];
+    rho = fo_rho[i];
+    u = gmem(fo_u[i]);
+  }
+  pdl_wait();  // in every thread, so the chain's completion stays transitive
+  if (i < n_out)
+    outlet_entry<L>(gmem(bh.pdf[e]), bh.base[e], slot, partner, cell, dir, rho, u, parity);
+}
+
 // CTA prefix of a phase on the device: start[e] = first CTA of engine e
 int upload_prefix(const std::vector<uint32_t>& start, uint32_t** out) {
   SLBM_CUDA_TRY(cudaMalloc(out, start.size() * sizeof(uint32_t)));
@@ -492,9 +614,27 @@ void fill_hot(GroupHot<CAP>*& out, const SlbmGroup* g, int phase, int flip,
   }
 }
 
+template <int CAP>
+void fill_bhot(BoundaryHot<CAP>*& out, const SlbmGroup* g, int flip) {
+  const int n = int(g->engines.size());
+  delete out;
+  out = new BoundaryHot<CAP>();
+  for (int i = 0; i < n; ++i) {
+    const GroupArgs a = args_of(g->engines[i], 0, flip);
+    out->pdf[i] = a.pdf;
+    for (int q = 0; q < 28; ++q) out->base[i][q] = a.base[q];
+  }
+}
+
 // CTA prefixes, device tables and kernel-parameter blocks of every phase
 int build_tables(SlbmGroup* g) {
   const int n = int(g->engines.size());
+  for (int flip = 0; flip < 2; ++flip) {
+    if (n <= 16)
+      fill_bhot(g->bhot16[flip], g, flip);
+    else if (n <= 128)
+      fill_bhot(g->bhot128[flip], g, flip);
+  }
   SlbmEngine* e0 = g->engines[0];
   for (int phase = 0; phase < 3; ++phase) {
     if (phase && !e0->has_split) continue;
@@ -598,6 +738,21 @@ int slbm_group_create(SlbmEngine** engines, int n, SlbmGroup** out) {
     SLBM_CUDA_TRY(cudaMemcpy(g->out_eng, oe.data(), oe.size() * 2, cudaMemcpyHostToDevice));
     SLBM_CUDA_TRY(cudaMalloc(&g->out_idx, oi.size() * sizeof(uint32_t)));
     SLBM_CUDA_TRY(cudaMemcpy(g->out_idx, oi.data(), oi.size() * 4, cudaMemcpyHostToDevice));
+    const size_t m = oe.size();
+    SLBM_CUDA_TRY(cudaMalloc(&g->fo_slot, m * 4));
+    SLBM_CUDA_TRY(cudaMalloc(&g->fo_partner, m * 4));
+    SLBM_CUDA_TRY(cudaMalloc(&g->fo_cell, m * 4));
+    SLBM_CUDA_TRY(cudaMalloc(&g->fo_dir, m));
+    SLBM_CUDA_TRY(cudaMalloc(&g->fo_rho, m * 8));
+    SLBM_CUDA_TRY(cudaMalloc(&g->fo_u, m * sizeof(double*)));
+    if (m) {
+      k_flatten_outlet<<<unsigned((m + 255) / 256), 256>>>(g->out_tab, g->out_eng, g->out_idx,
+                                                            int64_t(m), g->fo_slot, g->fo_partner,
+                                                            g->fo_cell, g->fo_dir, g->fo_rho,
+                                                            g->fo_u);
+      slbm::count_launch();
+      SLBM_CUDA_TRY(cudaDeviceSynchronize());
+    }
   }
   if (g->n_ubb) {
     SLBM_CUDA_TRY(cudaMalloc(&g->ubb_eng, g->n_ubb * sizeof(uint16_t)));
@@ -797,6 +952,13 @@ int slbm_group_destroy(SlbmGroup* g) {
     if (p) cudaFree(p);
   if (g->save_src) cudaFree(g->save_src);
   if (g->save_dst) cudaFree(g->save_dst);
+  for (int f = 0; f < 2; ++f) {
+    delete g->bhot16[f];
+    delete g->bhot128[f];
+  }
+  for (void* p : {(void*)g->fo_slot, (void*)g->fo_partner, (void*)g->fo_cell, (void*)g->fo_dir,
+                  (void*)g->fo_rho, (void*)g->fo_u})
+    if (p) cudaFree(p);
   void* ptrs[] = {g->ubb_eng, g->ubb_slot, g->ubb_partner, g->ubb_corr, g->steps,
                   g->out_tab, g->out_eng, g->out_idx};
   for (void* p : ptrs)
@@ -817,6 +979,25 @@ int group_boundary(SlbmGroup* g, SlbmHalo* halo, int phase, int parity, cudaStre
   const uint32_t cta_out = uint32_t((g->n_out + kBT - 1) / kBT);
   const uint32_t grid = std::max(1u, cta_halo + cta_ubb + cta_out);
   cudaError_t err = cudaSuccess;
+  bool done = false;
+  auto hot = [&](auto* bh) {
+    if (done || !bh || (g->n_out && !g->fo_slot)) return;
+    constexpr int CAP = int(sizeof(bh->pdf) / sizeof(double*));
+    on_lattice(g->q, [&](auto lat) {
+      using L = decltype(lat);
+      err = launch_pdl(k_group_boundary_hot<L, CAP>, dim3(grid), dim3(kBT), 0, s, *bh, lt, le,
+                       g->ubb_eng, g->ubb_slot, g->ubb_partner, g->ubb_corr, g->n_ubb, g->out_eng,
+                       g->fo_slot, g->fo_partner, g->fo_cell, g->fo_dir, g->fo_rho, g->fo_u,
+                       g->n_out, g->steps, n, parity, cta_halo, cta_ubb);
+    });
+    done = true;
+  };
+  hot(g->bhot16[flip]);
+  hot(g->bhot128[flip]);
+  if (done) {
+    SLBM_CUDA_TRY(err);
+    return SLBM_OK;
+  }
   on_lattice(g->q, [&](auto lat) {
     using L = decltype(lat);
     err = launch_pdl(k_group_boundary<L>, dim3(grid), dim3(kBT), 0, s, lt, le, g->table[0][flip],
