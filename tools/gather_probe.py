@@ -1,3 +1,6 @@
+"""Domain.gather_macroscopics wall time on the C4 artery (global box
+assembled on the device + staged copies) and the host copy / fill costs
+beside it.  Tuning aid:  python tools/gather_probe.py"""
 import os, sys, time, json
 sys.path.insert(0, "/root/repo")
 import numpy as np, torch
@@ -5,7 +8,7 @@ from paper_2408_06880_b200 import geometry, _abi
 from paper_2408_06880_b200.collision import CollisionParams, trt_magic_lambda
 from paper_2408_06880_b200.domain import Domain
 from paper_2408_06880_b200.lattice import make_stencil
-print(open("/sys/kernel/mm/transparent_hugepage/enabled").read().strip(), np.core.multiarray._get_madvise_hugepage() if hasattr(np.core.multiarray, "_get_madvise_hugepage") else "?")
+print(open("/sys/kernel/mm/transparent_hugepage/enabled").read().strip())
 fl = geometry.artery_flags((512,) * 3, seed=0, r_root=40.0, r_min=14.0)
 dom = Domain(fl, 128, make_stencil("d3q19"), CollisionParams(1.7, "trt", trt_magic_lambda(1.7)), pattern="aa", frame_width="halo", check="deferred")
 dom.init_equilibrium(); dom.run(2, use_graph=True); dom.synchronize()
