@@ -309,6 +309,8 @@ int slbm_group_finish(SlbmGroup* group, void* stream);
  * edges are no longer maintained and the halo's local program is switched
  * off.  SLBM_ECONFIG when not applicable (nothing changed then).        */
 int slbm_group_link_halo(SlbmGroup* group, SlbmHalo* halo);
+/* (Engines of a linked group refuse slbm_step / slbm_finish_step / slbm_run
+ * with SLBM_ECONFIG: they are stepped through the group only.)           */
 /* Linked groups only (no-op otherwise): the local edges' (source slot,
  * ghost slot) pairs, mode 0 ghost <- source, 1 swap, 2 source <- ghost.
  * The reference's state after an AA even step has the source slots of

@@ -739,8 +739,18 @@ int slbm_refresh_boundary(SlbmEngine* e, int parity) {
   return launch_refresh(e, parity);
 }
 
+// an engine of a linked block group reads other blocks' slots through the
+// group's list; stepping it alone would read its unmaintained ghosts
+#define CHECK_NOT_LINKED(e)                                                       \
+  do {                                                                            \
+    if ((e)->pool)                                                                \
+      return fail(SLBM_ECONFIG, "engine belongs to a linked block group: step it " \
+                                "through the group (Domain)");                    \
+  } while (0)
+
 int slbm_step(SlbmEngine* e, int phase) {
   CHECK_ENGINE(e);
+  CHECK_NOT_LINKED(e);
   if (phase != SLBM_PHASE_ALL && phase != SLBM_PHASE_INTERIOR && phase != SLBM_PHASE_FRAME)
     return fail(SLBM_ECONFIG, "unknown sweep phase");
   if (phase != SLBM_PHASE_ALL && !e->has_split)
@@ -751,6 +761,7 @@ int slbm_step(SlbmEngine* e, int phase) {
 
 int slbm_finish_step(SlbmEngine* e) {
   CHECK_ENGINE(e);
+  CHECK_NOT_LINKED(e);
   DeviceGuard guard(e->device);
   if (e->pattern == SLBM_PULL)
     std::swap(e->pdf, e->tmp);
@@ -762,6 +773,7 @@ int slbm_finish_step(SlbmEngine* e) {
 
 int slbm_run(SlbmEngine* e, int64_t n, int use_graph) {
   CHECK_ENGINE(e);
+  CHECK_NOT_LINKED(e);
   DeviceGuard guard(e->device);
   int64_t done = 0;
   if (use_graph && resident_eligible(e, n)) {  // small block: one launch for all n steps

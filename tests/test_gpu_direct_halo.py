@@ -57,3 +57,13 @@ def test_single_step_calls(gpu_lib):
         b.step_sequential()
         for x, y in zip(_all_slots(a), _all_slots(b)):
             np.testing.assert_array_equal(x, y)
+
+
+def test_linked_engines_refuse_engine_level_steps(gpu_lib):
+    from paper_2408_06880_b200 import errors
+
+    d = _domain(True)
+    e = d.local_blocks()[0].engine
+    with pytest.raises(errors.error_class("ConfigurationError")):
+        e.step()
+    d.run(2)  # the domain still steps them
