@@ -351,6 +351,8 @@ int slbm_launch_count(int64_t* count);
  *   7  ... its index-list prefetch distance in tiles (-1 = default, 0 = off)
  *   8  ... its L2 keep/drop hints (default 1)
  *   9  dense engines: lean whole-block odd sweep k_dense_odd (default 1)
+ *   13 D3Q19 index-list sweep CTAs per SM: 0 = measured per engine on its
+ *      first sweeps (blocks of >= 2^22 fluid cells; default), 4 or 5
  * Process-wide host-transfer knobs (slbm_set_tuning only):
  *   10 host staging chunk in MiB, 11 host staging threads
  *   12 slbm_macroscopic into pinned buffers: 0 = HBM staging + DMA copy

@@ -82,6 +82,8 @@ void free_engine(SlbmEngine* e) {
   for (auto& gx : e->graph)
     if (gx) cudaGraphExecDestroy(gx);
   free_pair(e);
+  for (auto& ev : e->even_ev)
+    if (ev) cudaEventDestroy(ev);
   if (e->pool) {  // the pdf is part of a group's pool: release this engine's share
     if (--e->pool->refs == 0) {
       cudaFree(e->pool->base);
@@ -799,6 +801,13 @@ int slbm_run(SlbmEngine* e, int64_t n, int use_graph) {
       SLBM_TRY(launch_pair(e));
       e->steps_done += 2;
     }
+  }
+  // a large D3Q19 engine measures its index-list sweep occupancy on its
+  // first eager steps (kernels.cu sweep_ctas) before any graph bakes it in
+  while (use_graph && done < n && e->q == 19 && e->even_ctas == 0 && e->tune.even_ctas == 0 &&
+         e->tune.even_variant == 0 && e->n_fluid >= (int64_t(1) << 22) && e->layout == 0) {
+    SLBM_TRY(sweep_once(e));
+    ++done;
   }
   if (use_graph && n - done >= 2) {
     // state key: AA -> parity; pull -> which buffer is active (pdf < tmp)

@@ -29,6 +29,7 @@ struct SlbmTuning {
   int pair_ahead = -1;
   int pair_hints = 1;
   int dense_lean_odd = 1;          // dense engines: k_dense_odd
+  int even_ctas = 0;               // D3Q19 index-list sweep CTAs/SM: 0 auto, 4 or 5
 };
 
 namespace slbm {
@@ -109,6 +110,11 @@ struct SlbmEngine {
   long long graph_kernels[2] = {0, 0};  // library kernels per replay (slbm_launch_count)
   int64_t steps_done = 0;
   slbm::PairPlan* pair = nullptr;  // pair.cu: temporally blocked AA step pair
+  // index-list sweep occupancy chosen by measurement (kernels.cu
+  // sweep_ctas): 0 undecided, else 4 or 5 CTAs per SM
+  int even_ctas = 0;
+  int even_trials = 0;
+  cudaEvent_t even_ev[4] = {nullptr, nullptr, nullptr, nullptr};
 
   int ensure_scratch(size_t bytes);
 

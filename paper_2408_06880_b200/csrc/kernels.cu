@@ -164,7 +164,16 @@ void launch_index(const SweepArgs& a, const SlbmTuning& t, cudaStream_t s) {
 template <class L, int MODEL>
 void launch_kind(int kind, const SweepArgs& a, unsigned grid, const SlbmTuning& t, cudaStream_t s) {
   constexpr int MINB = L::Q == 9 ? 8 : 4;
+  // D3Q19 index-list sweeps at 5 CTAs/SM (94 registers, no spills): more
+  // gathers in flight pays on scattered geometries (C5 random obstacles
+  // phi 0.3: 0.83 -> 0.86 of HBM) and costs on coherent ones (sphere bed
+  // 0.97 -> 0.94); chosen per engine by measurement (sweep_ctas)
+  constexpr bool kFive = L::Q == 19;
+  const bool five = kFive && t.even_ctas == 5;
   if (kind == kPull) {
+    if constexpr (kFive) {
+      if (five) return launch_index<L, MODEL, kPull, 5, true>(a, t, s);
+    }
     launch_index<L, MODEL, kPull, MINB, true>(a, t, s);
   } else if (kind == kEven) {
     if (t.even_variant == 1)
@@ -173,7 +182,12 @@ void launch_kind(int kind, const SweepArgs& a, unsigned grid, const SlbmTuning& 
     else if (t.even_variant == 2)  // memory-pattern probe, not LBM
       { k_probe<L><<<(a.n_cells + kIB - 1) / kIB, kIB, 0, s>>>(a); slbm::count_launch(); }
 #endif
-    else
+    else if constexpr (kFive) {
+      if (five)
+        launch_index<L, MODEL, kEven, 5, true>(a, t, s);
+      else
+        launch_index<L, MODEL, kEven, MINB, true>(a, t, s);
+    } else
       launch_index<L, MODEL, kEven, MINB, true>(a, t, s);
   } else {
     if (L::Q != 9 && t.odd_variant == 2)
@@ -493,12 +507,17 @@ int tuning_apply(SlbmTuning& t, int knob, int value) {
       (knob == 5 ? t.pair : knob == 6 ? t.pair_slack : knob == 7 ? t.pair_ahead : t.pair_hints) = value;
       return SLBM_OK;
     case 9: t.dense_lean_odd = value; return SLBM_OK;
+    case 13:
+      if (value != 0 && value != 4 && value != 5)
+        return fail(SLBM_ECONFIG, "knob 13: 0 (measure), 4 or 5 CTAs per SM");
+      t.even_ctas = value;
+      return SLBM_OK;
     default: return fail(SLBM_ECONFIG, "unknown engine tuning knob " + std::to_string(knob));
   }
 }
 
 int set_tuning(int knob, int value) {
-  if (knob >= 0 && knob <= 9) return tuning_apply(g_tuning_defaults, knob, value);
+  if ((knob >= 0 && knob <= 9) || knob == 13) return tuning_apply(g_tuning_defaults, knob, value);
   if (knob == 10 || knob == 11 || knob == 12) return hostcopy_tune(knob, value);
   return fail(SLBM_ECONFIG, "unknown tuning knob " + std::to_string(knob));
 }
@@ -513,6 +532,43 @@ int launch_slot_lookup(SlbmEngine* e, const int64_t* d_qs, const int64_t* d_pfla
                                                           d_err); slbm::count_launch(); }
   SLBM_CUDA_TRY(cudaGetLastError());
   return SLBM_OK;
+}
+
+// Occupancy of a D3Q19 engine's whole-block index-list sweep: the knob
+// (tune.even_ctas 4 / 5) or, by default for blocks of >= 2^22 fluid cells,
+// measured on the engine's own sweeps -- the first sweep warms up at 4
+// CTAs/SM, the next two run at 5 and at 4 between CUDA events, the fourth
+// reads the events and keeps 5 only if it was >= 1.5 % faster.  Results are
+// the same bits either way; during a stream capture an undecided engine
+// uses 4.  *trial = the event pair to record around this launch, or -1.
+int sweep_ctas(SlbmEngine* e, int* trial) {
+  *trial = -1;
+  if (e->q != 19 || e->tune.even_variant != 0) return 4;
+  if (e->tune.even_ctas == 4 || e->tune.even_ctas == 5) return e->tune.even_ctas;
+  if (e->even_ctas) return e->even_ctas;
+  if (e->n_fluid < (int64_t(1) << 22)) return e->even_ctas = 4;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(e->stream, &cap);
+  if (cap != cudaStreamCaptureStatusNone) return 4;
+  const int k = e->even_trials++;
+  if (k == 0) return 4;
+  if (k == 1 || k == 2) {
+    for (auto& ev : e->even_ev)
+      if (!ev && cudaEventCreate(&ev) != cudaSuccess) return e->even_ctas = 4;
+    *trial = k - 1;
+    return k == 1 ? 5 : 4;
+  }
+  float t5 = 0.f, t4 = 0.f;
+  int pick = 4;
+  if (cudaEventSynchronize(e->even_ev[3]) == cudaSuccess &&
+      cudaEventElapsedTime(&t5, e->even_ev[0], e->even_ev[1]) == cudaSuccess &&
+      cudaEventElapsedTime(&t4, e->even_ev[2], e->even_ev[3]) == cudaSuccess && t5 < 0.985f * t4)
+    pick = 5;
+  for (auto& ev : e->even_ev) {
+    if (ev) cudaEventDestroy(ev);
+    ev = nullptr;
+  }
+  return e->even_ctas = pick;
 }
 
 int launch_step(SlbmEngine* e, int phase) {
@@ -534,9 +590,14 @@ int launch_step(SlbmEngine* e, int phase) {
   if (a.n_cells == 0) return SLBM_OK;
   const int kind = e->pattern == SLBM_PULL ? kPull : (e->parity == SLBM_EVEN ? kEven : kOdd);
   const unsigned grid = grid_for(a.n_cells, kBlock);
+  SlbmTuning t = e->tune;
+  int trial = -1;  // event pair of a timed trial launch
+  if (kind != kOdd && phase == SLBM_PHASE_ALL) t.even_ctas = sweep_ctas(e, &trial);
+  if (trial >= 0) SLBM_CUDA_TRY(cudaEventRecord(e->even_ev[2 * trial], e->stream));
   by_lattice(e->q, [&](auto lat) {
-    launch_model<decltype(lat)>(e->model, kind, a, grid, e->tune, e->stream);
+    launch_model<decltype(lat)>(e->model, kind, a, grid, t, e->stream);
   });
+  if (trial >= 0) SLBM_CUDA_TRY(cudaEventRecord(e->even_ev[2 * trial + 1], e->stream));
   SLBM_CUDA_TRY(cudaGetLastError());
   return SLBM_OK;
 }

@@ -96,7 +96,7 @@ def test_tuning_knobs_documented_and_accepted():
     knobs = sorted({int(k) for k in re.findall(r"^\s*\*\s+(\d+)\s", block, flags=re.M)} | {11})
     assert {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12} <= set(knobs)
     lib = _abi.load()
-    defaults = {0: 0, 1: 0, 2: 1, 3: 0, 4: 1 << 19, 5: 0, 6: 0, 7: -1, 8: 1, 9: 1, 12: 0}
+    defaults = {0: 0, 1: 0, 2: 1, 3: 0, 4: 1 << 19, 5: 0, 6: 0, 7: -1, 8: 1, 9: 1, 12: 0, 13: 0}
     for k, v in defaults.items():
         assert lib.slbm_set_tuning(k, v) == 0
     assert lib.slbm_set_tuning(99, 0) != 0
@@ -104,3 +104,4 @@ def test_tuning_knobs_documented_and_accepted():
     assert lib.slbm_set_tuning(0, 2) != 0
     assert lib.slbm_set_tuning(5, 1) != 0
     assert lib.slbm_set_tuning(0, 0) == 0
+    assert lib.slbm_set_tuning(13, 3) != 0  # 0, 4 or 5 CTAs per SM
