@@ -539,7 +539,8 @@ def roofline_single(eng, t_even, t_odd, ach_even, ach_odd, pair, hbm, hbm_src, l
                     sustained):
     r = {
         "bound": "hbm",
-        "kernel": "k_index_sweep<D3Q19,TRT,even> (index-list AA sweep, 128x4 CTAs, L2 idx prefetch)",
+        "kernel": f"k_index_sweep<D3Q19,TRT,even> (index-list AA sweep, 128-thread CTAs x "
+                  f"{getattr(eng, 'sweep_ctas', 4) or 4} per SM (measured per engine), L2 idx prefetch)",
         "timing": "CUDA events after every step inside the timed region (mean over the "
                   "index-list steps); burst: the timed region is short, see sustained",
         "achieved": round(ach_even, 1),

@@ -353,11 +353,13 @@ int slbm_launch_count(int64_t* count);
  *   9  dense engines: lean whole-block odd sweep k_dense_odd (default 1)
  *   13 D3Q19 index-list sweep CTAs per SM: 0 = measured per engine on its
  *      first sweeps (blocks of >= 2^22 fluid cells; default), 4 or 5
+ *      (slbm_engine_sweep_ctas reports the choice, 0 while undecided)
  * Process-wide host-transfer knobs (slbm_set_tuning only):
  *   10 host staging chunk in MiB, 11 host staging threads
  *   12 slbm_macroscopic into pinned buffers: 0 = HBM staging + DMA copy
  *      (default), 1 = field kernel writes mapped host memory             */
 int slbm_set_tuning(int knob, int value);
+int slbm_engine_sweep_ctas(const SlbmEngine* eng, int* ctas);
 int slbm_engine_set_tuning(SlbmEngine* eng, int knob, int value);
 
 const char* slbm_last_error(void);

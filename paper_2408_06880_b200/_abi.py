@@ -70,6 +70,7 @@ SIGNATURES = {
     "slbm_total_moments": [vp, c_dp],
     "slbm_macroscopic_global": [vp, vp, vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
     "slbm_copy_to_host": [vp, vp, C.c_int64, C.c_int],
+    "slbm_engine_sweep_ctas": [vp, C.POINTER(C.c_int)],
     "slbm_refresh_boundary": [vp, C.c_int],
     "slbm_step": [vp, C.c_int],
     "slbm_finish_step": [vp],

@@ -684,6 +684,13 @@ int slbm_macroscopic_global(SlbmEngine* e, double* dev_rho, double* dev_u,
   return launch_macroscopic(e, nullptr, dev_rho, dev_u, false, gdims, origin);
 }
 
+int slbm_engine_sweep_ctas(const SlbmEngine* e, int* ctas) {
+  CHECK_ENGINE(e);
+  if (!ctas) return fail(SLBM_ECONFIG, "null output");
+  *ctas = e->tune.even_ctas ? e->tune.even_ctas : e->even_ctas;  // 0: not decided yet
+  return SLBM_OK;
+}
+
 int slbm_copy_to_host(void* host, const void* dev, int64_t bytes, int device) {
   if (!host || !dev || bytes < 0) return fail(SLBM_ECONFIG, "bad copy arguments");
   DeviceGuard guard(device);

@@ -114,7 +114,7 @@ struct SlbmEngine {
   // sweep_ctas): 0 undecided, else 4 or 5 CTAs per SM
   int even_ctas = 0;
   int even_trials = 0;
-  cudaEvent_t even_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t even_ev[8] = {};
 
   int ensure_scratch(size_t bytes);
 

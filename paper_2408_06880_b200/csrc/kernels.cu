@@ -537,10 +537,11 @@ int launch_slot_lookup(SlbmEngine* e, const int64_t* d_qs, const int64_t* d_pfla
 // Occupancy of a D3Q19 engine's whole-block index-list sweep: the knob
 // (tune.even_ctas 4 / 5) or, by default for blocks of >= 2^22 fluid cells,
 // measured on the engine's own sweeps -- the first sweep warms up at 4
-// CTAs/SM, the next two run at 5 and at 4 between CUDA events, the fourth
-// reads the events and keeps 5 only if it was >= 1.5 % faster.  Results are
-// the same bits either way; during a stream capture an undecided engine
-// uses 4.  *trial = the event pair to record around this launch, or -1.
+// CTAs/SM, the next four alternate 5, 4, 5, 4 between CUDA events, and the
+// sixth compares the faster trial of each and keeps 5 only if it was
+// >= 1.5 % faster.  Results are the same bits either way; during a stream
+// capture an undecided engine uses 4.  *trial = the event pair to record
+// around this launch, or -1.
 int sweep_ctas(SlbmEngine* e, int* trial) {
   *trial = -1;
   if (e->q != 19 || e->tune.even_variant != 0) return 4;
@@ -552,18 +553,17 @@ int sweep_ctas(SlbmEngine* e, int* trial) {
   if (cap != cudaStreamCaptureStatusNone) return 4;
   const int k = e->even_trials++;
   if (k == 0) return 4;
-  if (k == 1 || k == 2) {
+  if (k <= 4) {
     for (auto& ev : e->even_ev)
       if (!ev && cudaEventCreate(&ev) != cudaSuccess) return e->even_ctas = 4;
     *trial = k - 1;
-    return k == 1 ? 5 : 4;
+    return (k & 1) ? 5 : 4;
   }
-  float t5 = 0.f, t4 = 0.f;
-  int pick = 4;
-  if (cudaEventSynchronize(e->even_ev[3]) == cudaSuccess &&
-      cudaEventElapsedTime(&t5, e->even_ev[0], e->even_ev[1]) == cudaSuccess &&
-      cudaEventElapsedTime(&t4, e->even_ev[2], e->even_ev[3]) == cudaSuccess && t5 < 0.985f * t4)
-    pick = 5;
+  float t[4] = {0.f, 0.f, 0.f, 0.f};
+  bool ok = cudaEventSynchronize(e->even_ev[7]) == cudaSuccess;
+  for (int i = 0; i < 4 && ok; ++i)
+    ok = cudaEventElapsedTime(&t[i], e->even_ev[2 * i], e->even_ev[2 * i + 1]) == cudaSuccess;
+  const int pick = ok && std::min(t[0], t[2]) < 0.985f * std::min(t[1], t[3]) ? 5 : 4;
   for (auto& ev : e->even_ev) {
     if (ev) cudaEventDestroy(ev);
     ev = nullptr;

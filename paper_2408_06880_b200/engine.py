@@ -445,6 +445,14 @@ class SparseEngine:
         _abi.call("slbm_total_mass", self._h, C.byref(m))
         return float(m.value)
 
+    @property
+    def sweep_ctas(self) -> int:
+        """CTAs per SM of the index-list sweep (knob 13 or the engine's own
+        measurement; 0 while undecided)."""
+        v = C.c_int()
+        _abi.call("slbm_engine_sweep_ctas", self._h, C.byref(v))
+        return int(v.value)
+
     def total_moments(self) -> np.ndarray:
         """(mass, momentum x, y, z) of the canonical state: one device pass,
         warp-shuffle reductions in a fixed order (bit-reproducible)."""

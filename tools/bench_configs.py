@@ -235,7 +235,7 @@ def c5(steps):
         fl = geometry.obstacle_flags((edge,) * 3, phi, 1)
         eng = SparseEngine(fl, st, p, "aa", device=0, check="deferred")
         eng.init_equilibrium(1.0, np.array([0.005, 0.0, 0.0]))
-        eng.run(2)
+        eng.run(12)  # the occupancy trials (kernels.cu sweep_ctas) end before timing
         ms = timed_run(eng, steps)
         eng.poll()
         nf = eng.n_fluid
@@ -246,6 +246,7 @@ def c5(steps):
         even_frac = nf * bench.BYTES_EVEN / (te / 1e3) / 1e9 / HBM
         odd_frac = nf * bench.BYTES_ODD / (to / 1e3) / 1e9 / HBM
         sparse_bytes = eng.device_bytes
+        ctas = eng.sweep_ctas
         del eng
         # measured dense (direct-addressing) engine on the same geometry
         den = DenseEngine(fl, st, p, "aa", device=0, check="deferred")
@@ -259,6 +260,7 @@ def c5(steps):
         dense_equiv = HBM * 1e9 / dense_bpc * phi / 1e6
         model_bytes = edge**3 * (19 * 8 + 18 * 4 + 5 * 8) * phi
         emit({"config": "c5", "porosity": phi, "n_fluid": nf, "mflups": round(mfl, 1),
+              "sweep_ctas_per_sm": ctas,
               "dense_mflups_measured": round(mfl_d, 1),
               "dense_equivalent_mflups_model": round(dense_equiv, 1),
               "sparse_over_dense_measured": round(mfl / mfl_d, 3),
