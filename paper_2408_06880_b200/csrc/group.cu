@@ -70,6 +70,14 @@ template <int CAP>
 struct BoundaryHot {
   double* pdf[CAP];
   uint32_t base[CAP][28];
+  __device__ double* buf(int e) const { return pdf[e]; }
+  __device__ const uint32_t* starts(int e) const { return base[e]; }
+};
+// ... and the same lookups through the device table (groups of > 128 blocks)
+struct BoundaryTable {
+  const GroupArgs* t;
+  __device__ double* buf(int e) const { return t[e].pdf; }
+  __device__ const uint32_t* starts(int e) const { return t[e].base; }
 };
 }  // namespace slbm
 
@@ -314,87 +322,6 @@ __global__ void __launch_bounds__(kGB, KIND == 2 ? 6 : 4) k_group(const GroupArg
 constexpr int kBT = 128;
 constexpr int kBItems = 4;
 
-template <class L>
-__global__ void __launch_bounds__(kBT) k_group_boundary(
-    const __grid_constant__ PdfTable lt, LocalEdges le, const GroupArgs* __restrict__ table,
-    const uint16_t* __restrict__ ueng, const uint32_t* __restrict__ uslot,
-    const uint32_t* __restrict__ upartner, const double* __restrict__ ucorr, int64_t n_ubb,
-    const OutletTab* __restrict__ ot, const uint16_t* __restrict__ oeng,
-    const uint32_t* __restrict__ oidx, int64_t n_out, unsigned long long** steps, int n_eng,
-    int parity, uint32_t cta_halo, uint32_t cta_ubb) {
-  pdl_launch_dependents();
-  const uint32_t b = blockIdx.x;
-  if (b == 0) {
-    pdl_wait();  // the previous sweep reads the step counters
-    for (int e = threadIdx.x; e < n_eng; e += kBT) *steps[e] += 1;
-  }
-  if (b < cta_halo) {
-    __shared__ double* sp[kMaxHaloEngines];
-    for (int e = threadIdx.x; e < le.n_eng; e += kBT) sp[e] = gmem(lt.p[e]);
-    __syncthreads();
-    const int64_t i0 = int64_t(b) * kBT * kBItems + threadIdx.x;
-    uint16_t se[kBItems], de[kBItems];
-    uint32_t ss[kBItems], ds[kBItems];
-    double v[kBItems];
-#pragma unroll
-    for (int k = 0; k < kBItems; ++k) {
-      const int64_t i = i0 + k * kBT;
-      if (i < le.n) {
-        se[k] = le.se[i];
-        ss[k] = le.ss[i];
-        de[k] = le.de[i];
-        ds[k] = le.ds[i];
-      }
-    }
-    pdl_wait();  // the previous sweep wrote the source slots
-#pragma unroll
-    for (int k = 0; k < kBItems; ++k)
-      if (i0 + k * kBT < le.n) v[k] = gmem(sp[se[k]])[ss[k]];
-#pragma unroll
-    for (int k = 0; k < kBItems; ++k)
-      if (i0 + k * kBT < le.n) gmem(sp[de[k]])[ds[k]] = v[k];
-    return;
-  }
-  if (b < cta_halo + cta_ubb) {  // sparse.py:301-304
-    const int64_t i0 = int64_t(b - cta_halo) * kBT * kBItems + threadIdx.x;
-    double* pdf[kBItems];
-    uint32_t from[kBItems], to[kBItems];
-    double corr[kBItems], v[kBItems];
-#pragma unroll
-    for (int k = 0; k < kBItems; ++k) {
-      const int64_t i = i0 + k * kBT;
-      if (i < n_ubb) {
-        pdf[k] = gmem(table[ueng[i]].pdf);
-        from[k] = parity == SLBM_EVEN ? upartner[i] : uslot[i];
-        to[k] = parity == SLBM_EVEN ? uslot[i] : upartner[i];
-        corr[k] = ucorr[i];
-      }
-    }
-    pdl_wait();
-#pragma unroll
-    for (int k = 0; k < kBItems; ++k)
-      if (i0 + k * kBT < n_ubb) v[k] = gmem(pdf[k])[from[k]];
-#pragma unroll
-    for (int k = 0; k < kBItems; ++k)
-      if (i0 + k * kBT < n_ubb) gmem(pdf[k])[to[k]] = v[k] + corr[k];
-    return;
-  }
-  const int64_t i = int64_t(b - cta_halo - cta_ubb) * kBT + threadIdx.x;
-  int e = 0;
-  uint32_t k = 0;
-  if (i < n_out) {
-    e = oeng[i];
-    k = oidx[i];
-  }
-  pdl_wait();  // in every thread, so the chain's completion stays transitive
-  if (i < n_out) {
-    const OutletTab& o = ot[e];
-    const GroupArgs& a = table[e];
-    outlet_entry<L>(gmem(a.pdf), a.base, gmem(o.slot)[k], gmem(o.partner)[k], gmem(o.cell)[k],
-                    gmem(o.dir)[k], gmem(o.rho)[k], gmem(o.u) + 3 * size_t(k), parity);
-  }
-}
-
 // ---- direct local halo edges (slbm_group_link_halo) ----
 __global__ void k_add_offset(uint32_t* out, const uint32_t* in, int64_t n, uint32_t off) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -446,14 +373,13 @@ __global__ void k_flatten_outlet(const OutletTab* ot, const uint16_t* oeng, cons
   u[i] = o.u + 3 * size_t(k);
 }
 
-// The boundary launch with the engines' buffers and group starts in the
-// kernel parameters and the outlet program flattened: every entry is one
-// round of coalesced index loads, then its PDF loads (the table version
-// went entry -> engine table row -> arrays -> PDFs).  Same work and order
-// per entry as k_group_boundary (halo CTAs included).
-template <class L, int CAP>
-__global__ void __launch_bounds__(kBT) k_group_boundary_hot(
-    const __grid_constant__ BoundaryHot<CAP> bh, const __grid_constant__ PdfTable lt,
+// The boundary launch.  LK looks up an engine's buffer and group starts:
+// BoundaryHot (kernel parameters, groups of <= 128 blocks) or BoundaryTable
+// (the device table).  The outlet program is flattened in entry order, so
+// every entry is one round of coalesced index loads, then its PDF loads.
+template <class L, class LK>
+__global__ void __launch_bounds__(kBT) k_group_boundary(
+    const __grid_constant__ LK bh, const __grid_constant__ PdfTable lt,
     LocalEdges le, const uint16_t* __restrict__ ueng, const uint32_t* __restrict__ uslot,
     const uint32_t* __restrict__ upartner, const double* __restrict__ ucorr, int64_t n_ubb,
     const uint16_t* __restrict__ oeng, const uint32_t* __restrict__ fo_slot,
@@ -503,7 +429,7 @@ __global__ void __launch_bounds__(kBT) k_group_boundary_hot(
     for (int k = 0; k < kBItems; ++k) {
       const int64_t i = i0 + k * kBT;
       if (i < n_ubb) {
-        pdf[k] = gmem(bh.pdf[ueng[i]]);
+        pdf[k] = gmem(bh.buf(ueng[i]));
         from[k] = parity == SLBM_EVEN ? upartner[i] : uslot[i];
         to[k] = parity == SLBM_EVEN ? uslot[i] : upartner[i];
         corr[k] = ucorr[i];
@@ -535,7 +461,7 @@ __global__ void __launch_bounds__(kBT) k_group_boundary_hot(
   }
   pdl_wait();  // in every thread, so the chain's completion stays transitive
   if (i < n_out)
-    outlet_entry<L>(gmem(bh.pdf[e]), bh.base[e], slot, partner, cell, dir, rho, u, parity);
+    outlet_entry<L>(gmem(bh.buf(e)), bh.starts(e), slot, partner, cell, dir, rho, u, parity);
 }
 
 // CTA prefix of a phase on the device: start[e] = first CTA of engine e
@@ -979,31 +905,22 @@ int group_boundary(SlbmGroup* g, SlbmHalo* halo, int phase, int parity, cudaStre
   const uint32_t cta_out = uint32_t((g->n_out + kBT - 1) / kBT);
   const uint32_t grid = std::max(1u, cta_halo + cta_ubb + cta_out);
   cudaError_t err = cudaSuccess;
-  bool done = false;
-  auto hot = [&](auto* bh) {
-    if (done || !bh || (g->n_out && !g->fo_slot)) return;
-    constexpr int CAP = int(sizeof(bh->pdf) / sizeof(double*));
+  auto go = [&](const auto& lk) {
+    using LK = std::decay_t<decltype(lk)>;
     on_lattice(g->q, [&](auto lat) {
       using L = decltype(lat);
-      err = launch_pdl(k_group_boundary_hot<L, CAP>, dim3(grid), dim3(kBT), 0, s, *bh, lt, le,
+      err = launch_pdl(k_group_boundary<L, LK>, dim3(grid), dim3(kBT), 0, s, lk, lt, le,
                        g->ubb_eng, g->ubb_slot, g->ubb_partner, g->ubb_corr, g->n_ubb, g->out_eng,
                        g->fo_slot, g->fo_partner, g->fo_cell, g->fo_dir, g->fo_rho, g->fo_u,
                        g->n_out, g->steps, n, parity, cta_halo, cta_ubb);
     });
-    done = true;
   };
-  hot(g->bhot16[flip]);
-  hot(g->bhot128[flip]);
-  if (done) {
-    SLBM_CUDA_TRY(err);
-    return SLBM_OK;
-  }
-  on_lattice(g->q, [&](auto lat) {
-    using L = decltype(lat);
-    err = launch_pdl(k_group_boundary<L>, dim3(grid), dim3(kBT), 0, s, lt, le, g->table[0][flip],
-                     g->ubb_eng, g->ubb_slot, g->ubb_partner, g->ubb_corr, g->n_ubb, g->out_tab,
-                     g->out_eng, g->out_idx, g->n_out, g->steps, n, parity, cta_halo, cta_ubb);
-  });
+  if (g->bhot16[flip])
+    go(*g->bhot16[flip]);
+  else if (g->bhot128[flip])
+    go(*g->bhot128[flip]);
+  else
+    go(BoundaryTable{g->table[0][flip]});
   SLBM_CUDA_TRY(err);
   return SLBM_OK;
 }

@@ -67,3 +67,25 @@ def test_linked_engines_refuse_engine_level_steps(gpu_lib):
     with pytest.raises(errors.error_class("ConfigurationError")):
         e.step()
     d.run(2)  # the domain still steps them
+
+
+def test_many_block_group_equals_one_block(gpu_lib):
+    """> 128 blocks: the boundary launch looks engines up in the device table
+    (BoundaryTable), the sweep reads the 512-capacity parameter block; with
+    a moving lid (UBB) and direct local edges the result equals one block."""
+    from paper_2408_06880_b200 import geometry
+    from paper_2408_06880_b200.collision import CollisionParams
+    from paper_2408_06880_b200.domain import Domain
+    from paper_2408_06880_b200.lattice import make_stencil
+
+    st = make_stencil("d3q19")
+    p = CollisionParams(1.3, "trt", 0.9)
+    gf = geometry.riverbed_flags((48, 40, 48), (8, 8, 8), 0.5, 5, 0.03)
+    many = Domain(gf, (8, 8, 8), st, p, pattern="aa", frame_width=1, check="deferred")
+    assert len(many.local_blocks()) > 128 and many.direct_halo
+    one = Domain(gf, (48, 40, 48), st, p, pattern="aa", frame_width=1, check="deferred")
+    for d in (many, one):
+        d.init_random(5)
+        d.run(3, use_graph=True)
+        d.run(5)  # an even total: odd-parity readouts are block-local (reference)
+    np.testing.assert_array_equal(many.gather_canonical(), one.gather_canonical())
