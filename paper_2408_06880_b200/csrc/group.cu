@@ -251,7 +251,10 @@ __global__ void __launch_bounds__(kGB, KIND == 2 ? 6 : 4) k_group(const GroupArg
   // engine of this CTA: binary search over the (L1-resident) CTA prefix --
   // a per-CTA engine map measured slower (its line is an L2 round trip per
   // CTA, consecutive CTAs land on different SMs)
-  const int eng = find_engine(start, n_eng, blockIdx.x);
+  // the cell-local sweep runs its CTAs last to first (as k_aa_odd): it
+  // starts on the lines the index-list sweep before it left in L2
+  const uint32_t bid = KIND == 2 ? gridDim.x - 1 - blockIdx.x : blockIdx.x;
+  const int eng = find_engine(start, n_eng, bid);
   const uint32_t first = start[eng];
   // the odd sweep addresses 2Q group rows through base[]: staged in shared
   // memory those offsets stay out of registers (77 vs 128 + spills)
@@ -262,7 +265,7 @@ __global__ void __launch_bounds__(kGB, KIND == 2 ? 6 : 4) k_group(const GroupArg
   }
   const GroupArgs& a = KIND == 2 ? staged : table[eng];
   constexpr int kTiles = KIND == 2 ? kOddTiles : kEvenTiles;
-  const uint32_t pos0 = (blockIdx.x - first) * kGB * kTiles;  // this CTA's first sweep position
+  const uint32_t pos0 = (bid - first) * kGB * kTiles;  // this CTA's first sweep position
   const uint32_t* idx = gmem(a.sidx);
   const uint32_t* cids = a.cids ? gmem(a.cids) : nullptr;
   const uint32_t* skip = a.skip ? gmem(a.skip) : nullptr;

@@ -131,7 +131,10 @@ __global__ void __launch_bounds__(kIB) k_probe(const SweepArgs a) {
 // coalesced row of a direction group, no index list.
 template <class L, int MODEL, int MINB>
 __global__ void __launch_bounds__(kBlock, MINB) k_aa_odd(const SweepArgs a) {
-  const uint32_t i = blockIdx.x * kBlock + threadIdx.x;
+  // CTAs run from the last cells to the first: the index-list sweep before
+  // ran first to last, so this sweep starts on the lines it left in L2, and
+  // the next index-list sweep starts on the lines this one leaves
+  const uint32_t i = (gridDim.x - 1 - blockIdx.x) * kBlock + threadIdx.x;
   if (i >= a.n_cells) return;
   const uint32_t c = a.cids ? a.cids[i] : a.offset + i;
   if (c < a.lo || (a.skip && ((__ldg(a.skip + (c >> 5)) >> (c & 31)) & 1u))) return;
