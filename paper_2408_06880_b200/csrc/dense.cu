@@ -235,7 +235,10 @@ struct DenseOddArgs {
 template <class L, int MODEL>
 __global__ void __launch_bounds__(128, L::Q == 27 ? 5 : 6) k_dense_odd(const DenseOddArgs a) {
   const uint32_t chunks = (a.X + 127) / 128;
-  const uint32_t row = blockIdx.x / chunks, chunk = blockIdx.x - row * chunks;
+  // CTAs last to first: the combined step before ran first to last, so this
+  // sweep starts on the lines it left in L2 (as the sparse cell-local sweep)
+  const uint32_t b = gridDim.x - 1 - blockIdx.x;
+  const uint32_t row = b / chunks, chunk = b - row * chunks;
   const uint32_t x = chunk * 128 + threadIdx.x;
   if (x >= a.X) return;
   const uint32_t y = row % a.Y, z = row / a.Y;
