@@ -22,6 +22,10 @@ from paper_2408_06880_b200.lattice import make_stencil  # noqa: E402
 
 st = make_stencil("d3q19")
 p = CollisionParams(bench.OMEGA, "trt", bench.magic_lambda(bench.OMEGA))
+from paper_2408_06880_b200 import _abi  # noqa: E402
+
+if os.environ.get("PROBE"):  # SLBM_PROBES=1 build: the even sweep's memory pattern only
+    _abi.load().slbm_set_tuning(0, 2)
 eng = SparseEngine(bench.make_flags(512, 0), st, p, "aa", device=0, check="deferred")
 eng.init_equilibrium(1.0, np.array([0.01, 0.0, 0.0]))
 eng.run(12, use_graph=False)
