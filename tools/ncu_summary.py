@@ -55,6 +55,12 @@ def algorithmic_bytes(name, n_cells):
         return 2 * q * 8 * n_cells
     if "aa_even" in name or "pull" in name or "index_sweep" in name:
         return (2 * q * 8 + (q - 1) * 4) * n_cells
+    if "k_group_hot<" in name or "k_group<" in name:
+        # block-group sweeps over every engine of the group: template
+        # arguments <lattice, model, KIND[, CAP]>, KIND 2 = cell-local
+        fn = "k_group_hot<" if "k_group_hot<" in name else "k_group<"
+        kind = int(name.split(fn, 1)[1].split(">")[0].split(",")[2])
+        return (2 * q * 8 + (0 if kind == 2 else (q - 1) * 4)) * n_cells
     return None
 
 
