@@ -604,34 +604,9 @@ int build_tables(SlbmGroup* g) {
 }
 
 
-}  // namespace
-
-extern "C" {
-
-int slbm_group_create(SlbmEngine** engines, int n, SlbmGroup** out) {
-  if (!engines || n < 1 || !out) return fail(SLBM_ECONFIG, "group needs engines");
-  SlbmEngine* e0 = engines[0];
-  for (int i = 0; i < n; ++i) {
-    SlbmEngine* e = engines[i];
-    if (!e) return fail(SLBM_ECONFIG, "null engine in group");
-    if (e->layout != 0) return fail(SLBM_ECONFIG, "block groups hold sparse engines only");
-    if (e->q != e0->q || e->model != e0->model || e->pattern != e0->pattern ||
-        e->omega != e0->omega || e->lambda_odd != e0->lambda_odd || e->device != e0->device ||
-        e->parity != e0->parity || e->has_split != e0->has_split ||
-        std::memcmp(e->hr, e0->hr, sizeof(e->hr)) != 0)
-      return fail(SLBM_ECONFIG, "group engines must share stencil, collision, pattern, device "
-                                "and parity");
-  }
-  cudaSetDevice(e0->device);
-  SlbmGroup* g = new SlbmGroup();
-  g->device = e0->device;
-  g->q = e0->q;
-  g->model = e0->model;
-  g->pattern = e0->pattern;
-  g->omega = e0->omega;
-  g->lam = e0->lambda_odd;
-  g->hr = e0->d_hr;
-  g->engines.assign(engines, engines + n);
+// everything of slbm_group_create past the checks (the caller destroys a
+// partly built group on failure)
+int init_group(SlbmGroup* g, SlbmEngine** engines, int n) {
   // pull: each engine's e->pdf is "current"; record the flip as 0
   SLBM_TRY(build_tables(g));
   // concatenated UBB program with engine ids
@@ -706,6 +681,42 @@ int slbm_group_create(SlbmEngine** engines, int n, SlbmGroup** out) {
   SLBM_CUDA_TRY(cudaMalloc(&g->steps, n * sizeof(unsigned long long*)));
   SLBM_CUDA_TRY(cudaMemcpy(g->steps, st.data(), n * sizeof(unsigned long long*),
                            cudaMemcpyHostToDevice));
+  return SLBM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int slbm_group_create(SlbmEngine** engines, int n, SlbmGroup** out) {
+  if (!engines || n < 1 || !out) return fail(SLBM_ECONFIG, "group needs engines");
+  SlbmEngine* e0 = engines[0];
+  for (int i = 0; i < n; ++i) {
+    SlbmEngine* e = engines[i];
+    if (!e) return fail(SLBM_ECONFIG, "null engine in group");
+    if (e->layout != 0) return fail(SLBM_ECONFIG, "block groups hold sparse engines only");
+    if (e->q != e0->q || e->model != e0->model || e->pattern != e0->pattern ||
+        e->omega != e0->omega || e->lambda_odd != e0->lambda_odd || e->device != e0->device ||
+        e->parity != e0->parity || e->has_split != e0->has_split ||
+        std::memcmp(e->hr, e0->hr, sizeof(e->hr)) != 0)
+      return fail(SLBM_ECONFIG, "group engines must share stencil, collision, pattern, device "
+                                "and parity");
+  }
+  cudaSetDevice(e0->device);
+  SlbmGroup* g = new SlbmGroup();
+  g->device = e0->device;
+  g->q = e0->q;
+  g->model = e0->model;
+  g->pattern = e0->pattern;
+  g->omega = e0->omega;
+  g->lam = e0->lambda_odd;
+  g->hr = e0->d_hr;
+  g->engines.assign(engines, engines + n);
+  const int st = init_group(g, engines, n);
+  if (st != SLBM_OK) {
+    slbm_group_destroy(g);
+    return st;
+  }
   *out = g;
   return SLBM_OK;
 }
@@ -766,17 +777,33 @@ int slbm_group_link_halo(SlbmGroup* g, SlbmHalo* h) {
   }
   SLBM_CUDA_TRY(cudaDeviceSynchronize());
   double* pool = nullptr;
-  SLBM_CUDA_TRY(cudaMalloc(&pool, size_t(total) * sizeof(double)));
   std::vector<uint32_t*> gidx(n, nullptr);
+  uint32_t *pos = nullptr, *dg = nullptr, *dv = nullptr;
+  // on failure everything allocated here is released and the group and its
+  // engines are left as they were (the pdf buffers move only at the end)
+  auto release = [&]() {
+    for (void* p : {(void*)pos, (void*)dg, (void*)dv, (void*)g->save_src, (void*)g->save_dst,
+                    (void*)pool})
+      if (p) cudaFree(p);
+    for (auto* p : gidx)
+      if (p) cudaFree(p);
+    g->save_src = g->save_dst = nullptr;
+    g->n_save = 0;
+  };
+#define LINK_TRY(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess) {                                                             \
+      release();                                                                         \
+      return fail(SLBM_ECUDA, std::string("slbm_group_link_halo: " #expr ": ") +         \
+                                  cudaGetErrorString(_e));                               \
+    }                                                                                    \
+  } while (0)
+  LINK_TRY(cudaMalloc(&pool, size_t(total) * sizeof(double)));
   for (int i = 0; i < n; ++i) {
     SlbmEngine* e = g->engines[i];
     const int64_t entries = int64_t(e->q - 1) * e->idx_pitch;
-    if (cudaMalloc(&gidx[i], size_t(entries) * sizeof(uint32_t)) != cudaSuccess) {
-      for (auto* p : gidx)
-        if (p) cudaFree(p);
-      cudaFree(pool);
-      return fail(SLBM_ECUDA, "out of device memory for the group index lists");
-    }
+    LINK_TRY(cudaMalloc(&gidx[i], size_t(entries) * sizeof(uint32_t)));
     if (entries) {
       k_add_offset<<<1024, 256>>>(gidx[i], e->idx, entries, off[i]);
       slbm::count_launch();
@@ -789,10 +816,10 @@ int slbm_group_link_halo(SlbmGroup* g, SlbmHalo* h) {
       ss_[k] = off[gid[cse[k]]] + css[k];
       dd_[k] = off[gid[cde[k]]] + cds[k];
     }
-    SLBM_CUDA_TRY(cudaMalloc(&g->save_src, ss_.size() * 4));
-    SLBM_CUDA_TRY(cudaMalloc(&g->save_dst, dd_.size() * 4));
-    SLBM_CUDA_TRY(cudaMemcpy(g->save_src, ss_.data(), ss_.size() * 4, cudaMemcpyHostToDevice));
-    SLBM_CUDA_TRY(cudaMemcpy(g->save_dst, dd_.data(), dd_.size() * 4, cudaMemcpyHostToDevice));
+    LINK_TRY(cudaMalloc(&g->save_src, ss_.size() * 4));
+    LINK_TRY(cudaMalloc(&g->save_dst, dd_.size() * 4));
+    LINK_TRY(cudaMemcpy(g->save_src, ss_.data(), ss_.size() * 4, cudaMemcpyHostToDevice));
+    LINK_TRY(cudaMemcpy(g->save_dst, dd_.data(), dd_.size() * 4, cudaMemcpyHostToDevice));
     g->n_save = int64_t(ss_.size());
   }
   // rewrite the ghost entries of local edges, per destination engine
@@ -805,30 +832,36 @@ int slbm_group_link_halo(SlbmGroup* g, SlbmHalo* h) {
   for (int i = 0; i < n; ++i) {
     if (ghost[i].empty()) continue;
     SlbmEngine* e = g->engines[i];
-    uint32_t *pos = nullptr, *dg = nullptr, *dv = nullptr;
     const size_t m = ghost[i].size();
-    SLBM_CUDA_TRY(cudaMalloc(&pos, size_t(e->phys_slots) * sizeof(uint32_t)));
-    SLBM_CUDA_TRY(cudaMemset(pos, 0xFF, size_t(e->phys_slots) * sizeof(uint32_t)));
+    LINK_TRY(cudaMalloc(&pos, size_t(e->phys_slots) * sizeof(uint32_t)));
+    LINK_TRY(cudaMemset(pos, 0xFF, size_t(e->phys_slots) * sizeof(uint32_t)));
     k_slot_pos<<<1024, 256>>>(pos, e->idx, uint32_t(e->idx_pitch), uint32_t(e->n_fluid), e->q - 1,
                               (e->q == 19) ? 1 : 0);
     slbm::count_launch();
-    SLBM_CUDA_TRY(cudaMalloc(&dg, m * sizeof(uint32_t)));
-    SLBM_CUDA_TRY(cudaMalloc(&dv, m * sizeof(uint32_t)));
-    SLBM_CUDA_TRY(cudaMemcpy(dg, ghost[i].data(), m * 4, cudaMemcpyHostToDevice));
-    SLBM_CUDA_TRY(cudaMemcpy(dv, val[i].data(), m * 4, cudaMemcpyHostToDevice));
+    LINK_TRY(cudaMalloc(&dg, m * sizeof(uint32_t)));
+    LINK_TRY(cudaMalloc(&dv, m * sizeof(uint32_t)));
+    LINK_TRY(cudaMemcpy(dg, ghost[i].data(), m * 4, cudaMemcpyHostToDevice));
+    LINK_TRY(cudaMemcpy(dv, val[i].data(), m * 4, cudaMemcpyHostToDevice));
     k_rewrite<<<unsigned((m + 255) / 256), 256>>>(gidx[i], pos, dg, dv, int64_t(m));
     slbm::count_launch();
-    SLBM_CUDA_TRY(cudaDeviceSynchronize());
-    cudaFree(pos);
-    cudaFree(dg);
-    cudaFree(dv);
+    LINK_TRY(cudaDeviceSynchronize());
+    for (uint32_t** p : {&pos, &dg, &dv}) {
+      cudaFree(*p);
+      *p = nullptr;
+    }
   }
-  // move every engine's pdf into the pool
+  // copy every engine's pdf into the pool; the engines switch to it only
+  // once all copies have succeeded
+  for (int i = 0; i < n; ++i)
+    LINK_TRY(cudaMemcpy(pool + off[i], g->engines[i]->pdf,
+                        size_t(g->engines[i]->phys_slots) * sizeof(double),
+                        cudaMemcpyDeviceToDevice));
+  LINK_TRY(cudaGetLastError());
+  LINK_TRY(cudaDeviceSynchronize());
+#undef LINK_TRY
   PdfPool* ref = new PdfPool{pool, 0};
   for (int i = 0; i < n; ++i) {
     SlbmEngine* e = g->engines[i];
-    SLBM_CUDA_TRY(cudaMemcpy(pool + off[i], e->pdf, size_t(e->phys_slots) * sizeof(double),
-                             cudaMemcpyDeviceToDevice));
     cudaFree(e->pdf);
     e->pdf = pool + off[i];
     e->pool = ref;
@@ -838,7 +871,6 @@ int slbm_group_link_halo(SlbmGroup* g, SlbmHalo* h) {
       gx = nullptr;
     }
   }
-  SLBM_CUDA_TRY(cudaGetLastError());
   g->direct = true;
   g->pool = pool;
   g->pool_off = off;
