@@ -1078,6 +1078,11 @@ class DistributedDomain(Domain):
                          frame_width=frame_width, device=device, check=check, _rank=rank,
                          _world=world, _assignment=assignment, _comm=comm,
                          engine_factory=engine_factory, halo_factory=halo_factory)
+        # NCCL sets up its peer connections on the first send/recv to a peer;
+        # the first step pair of a graph run goes eagerly so that happens
+        # outside stream capture
+        self._eager_first = (world > 1 and transport == "nccl" and halo_factory is None
+                             and not loopback)
 
     def gather_canonical_global(self) -> np.ndarray:
         """gather_canonical summed over ranks (rank 0 gets the full field)."""
@@ -1115,6 +1120,12 @@ class DistributedDomain(Domain):
                    transport=transport)
 
     def run(self, steps: int, driver: str = "overlapped", use_graph: bool = False) -> None:
+        steps = int(steps)
+        if use_graph and steps > 0 and getattr(self, "_eager_first", False):
+            first = min(steps, 2)
+            super().run(first, driver, False)
+            self._eager_first = False
+            steps -= first
         super().run(steps, driver, use_graph)
 
 
