@@ -468,7 +468,8 @@ def impl_ours(args, rank, world, local_rank):
         {
             "bound": "hbm",
             "kernel": "AA step pair per GPU: index-list + cell-local sweeps (interior + frame), "
-                      "halo pack / NCCL / unpack overlapped",
+                      f"halo pack / {os.environ.get('SLBM_TRANSPORT', 'nccl')} transfer / unpack "
+                      "overlapped",
             "timing": "CUDA events after every step pair (graph replay) inside the timed region, "
                       "max over ranks",
             "achieved": round(pair, 1), "peak": hbm, "unit": "GB/s", "frac": round(pair / hbm, 4),
@@ -644,8 +645,8 @@ def e2e_domain(dom, steps, torch, reduce, total_fluid):
             "h2d_bytes_per_step": int(h2d // steps), "d2h_bytes_per_step": int(d2h // steps),
             "seconds": round(dt, 4), "steps": steps,
             "note": "per rank: init_canonical from pinned host + DistributedDomain.run (overlapped "
-                    "driver, NCCL halo) + macroscopic_fields into pinned host buffers; max over "
-                    "ranks"}
+                    f"driver, {os.environ.get('SLBM_TRANSPORT', 'nccl')} halo transport) + "
+                    "macroscopic_fields into pinned host buffers; max over ranks"}
 
 
 def load_traffic():
